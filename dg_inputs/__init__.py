@@ -65,8 +65,9 @@ def _signed_volume6(VX, tet):
     return float(np.dot(b - a, np.cross(c - a, d - a)))
 
 
-def kuhn_box(n: int, L: float = 1.0):
-    """Kuhn box mesh of [0,L]^3: returns (VX [nv][3] float64, EToV [K][4] int64), K = 6 n^3.
+def kuhn_box(n: int, L: float = 1.0, nz: int | None = None):
+    """Kuhn box mesh of [0,L]^2 x [0, L*nz/n]: returns (VX [nv][3] float64, EToV [K][4] int64),
+    K = 6 n^2 nz (nz defaults to n: the cube [0,L]^3).
 
     Vertex id(i,j,k) = i + (n+1)(j + (n+1)k); cells ordered k, j, i (i fastest);
     each cell emits one tet per axis permutation p (lexicographic order), with
@@ -75,9 +76,10 @@ def kuhn_box(n: int, L: float = 1.0):
     """
     if n < 1:
         raise ValueError("n must be >= 1")
+    nz = n if nz is None else nz
     m = n + 1
     idx = np.arange(m)
-    kk, jj, ii = np.meshgrid(idx, idx, idx, indexing="ij")
+    kk, jj, ii = np.meshgrid(np.arange(nz + 1), idx, idx, indexing="ij")
     VX = np.stack([ii.ravel(), jj.ravel(), kk.ravel()], axis=1).astype(np.float64) * (L / n)
     perms = [(0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0)]
     step = (1, m, m * m)
@@ -94,7 +96,7 @@ def kuhn_box(n: int, L: float = 1.0):
         proto.append(t)
     proto = np.array(proto, dtype=np.int64)  # [6][4] relative to the cell-origin vertex
     # cells ordered k, j, i with i fastest
-    ck, cj, ci = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+    ck, cj, ci = np.meshgrid(np.arange(nz), np.arange(n), np.arange(n), indexing="ij")
     origin = (ci + m * (cj + m * ck)).ravel()
     EToV = (origin[:, None, None] + proto[None, :, :]).reshape(-1, 4)
     return VX, EToV.astype(np.int64)

@@ -1,0 +1,169 @@
+/*
+ * dg.h — C ABI of the B200 nodal-DG Maxwell library (libdg.so).
+ *
+ * What it computes: the semi-discrete DG operator of PAPER.md eq. (4)
+ *
+ *
+ *     d_t u^k = - sum_nu D^{k,d nu} F(u^k) + L^k [ n.F - (n.F)^* ]
+ *
+ * for 3-D Maxwell in vacuum (d_t E = curl H, d_t H = -curl E, eps = mu = 1) on
+ * straight-sided, face-conforming tetrahedra, with
+ * nodal trace picking, the upwind flux of fig:flux-code a
+ * with jump [[u]] = u+ - u- (reading R1), PEC
+ * walls E+ = -E-, H+ = H- (reading R4), the lifting matrix of fig:lifting-matrix
+ * (PAPER.md:170-216), advanced by 5-stage 2N-storage LSERK4 ("RK4 time stepping",
+ * PAPER.md:1179-1181; reading R5).  Every step of the hot path runs in the
+ * library's own sm_100a CUDA kernels; there is no CPU fallback.
+ *
+ * Conventions (all entry points)
+ *   - Every call returns dg_status; nothing throws or aborts across the ABI.
+ *     On failure dg_last_error() returns a thread-local description.
+ *   - Host arrays are borrowed for the duration of the call and copied.
+ *     Device buffers the solver allocates are owned by it and freed by
+ *     dg_destroy.  Caller device pointers (the *_device variants) are borrowed
+ *     and must stay valid until the enqueued work completes.
+ *   - One host thread per solver; separate solvers are independent.
+ *   - Call order: dg_create -> dg_mesh_upload -> dg_fields_upload[_device] ->
+ *     { dg_rhs[_device] | dg_lserk_step }* -> dg_fields_download[_device].
+ *     A call out of order returns DG_ERR_STATE.
+ *   - Fields on the host are FP64, component-major [6][K_local][Np] in the
+ *     order (Ex, Ey, Ez, Hx, Hy, Hz), node index fastest (HW's Np x K per
+ *     component).  Node n of element k is the n-th warp&blend node mapped
+ *     affinely (dg_get_nodes).  FP32 solvers round on upload and widen exactly
+ *     on download.
+ *   - Work is enqueued on the solver's stream (dg_config.stream, or a
+ *     solver-owned stream).  Calls that return host data synchronise it;
+ *     asynchronous CUDA errors surface at the next synchronising call.
+ *   - dt is always explicit: the library never chooses a time step.
+ */
+#ifndef DG_H_
+#define DG_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DG_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define DG_API __attribute__((visibility("default")))
+#else
+#define DG_API
+#endif
+
+typedef struct dg_solver dg_solver; /* opaque */
+
+typedef enum {
+  DG_OK = 0,
+  DG_ERR_ARG = 1,   /* null pointer, bad size or bad enum value */
+  DG_ERR_ORDER = 2, /* order N outside 1..9 */
+  DG_ERR_MESH = 3,  /* J <= 0, face shared by > 2 tets, unmatched face nodes, bad ids */
+  DG_ERR_STATE = 4, /* call out of order, or a compute call on a host-only solver */
+  DG_ERR_CUDA = 5,  /* CUDA runtime error (message has the CUDA error string) */
+  DG_ERR_NCCL = 6,  /* NCCL error or NCCL not loadable */
+  DG_ERR_OOM = 7    /* device allocation failed */
+} dg_status;
+
+typedef enum {
+  DG_VARIANT_AUTO = 0,  /* library picks per (N, precision) */
+  DG_VARIANT_BASIC = 1, /* one fused element-tile kernel per stage, FMA contractions */
+  DG_VARIANT_MMA = 2    /* tensor-core contractions (FP64 DMMA / FP32 3xTF32) where available */
+} dg_variant;
+
+typedef struct {
+  int32_t order;        /* polynomial order N, 1..9 */
+  int32_t precision;    /* 8 = FP64, 4 = FP32 arithmetic and storage on the device */
+  double alpha;         /* flux upwinding: 1.0 upwind (default), 0.0 central (fig:flux-code a) */
+  int32_t device;       /* CUDA device ordinal; -1 = host-only solver (setup/maps/nodes only) */
+  void* stream;         /* cudaStream_t to enqueue on; NULL = solver-owned stream */
+  int32_t rank;         /* this process's rank, 0..nranks-1 */
+  int32_t nranks;       /* number of ranks (one GPU each); 1 = single GPU */
+  const void* nccl_id;  /* 128-byte ncclUniqueId from rank 0 (nranks > 1), else NULL */
+  int32_t variant;      /* dg_variant */
+} dg_config;
+
+/* Fill *cfg with defaults: N=3, FP64, alpha=1, device 0, own stream, 1 rank, AUTO. */
+DG_API void dg_config_default(dg_config* cfg);
+
+/* Create a solver.  Builds the reference element of order N on the host (FP64).
+ * Errors: DG_ERR_ARG (null, precision not 4/8, nranks < 1, rank out of range,
+ * nccl_id NULL with nranks > 1), DG_ERR_ORDER, DG_ERR_CUDA (device unusable). */
+DG_API dg_status dg_create(const dg_config* cfg, dg_solver** out);
+
+/* Upload the (global) mesh: nv vertices VX[nv][3] (FP64), K tets EToV[K][4]
+ * (0-based, positively oriented; not re-oriented).  part[K] gives the owner
+ * rank of every element, or NULL for the built-in partition (contiguous element
+ * ranges, i.e. z-slabs on the Kuhn box).  Builds connectivity, maps, geometry
+ * and moves them to the device.  Errors:
+ * DG_ERR_ARG, DG_ERR_MESH, DG_ERR_OOM, DG_ERR_CUDA, DG_ERR_NCCL.
+ * May be called again to replace the mesh (fields must be re-uploaded). */
+DG_API dg_status dg_mesh_upload(dg_solver* s, int64_t nv, const double* VX, int64_t K,
+                         const int64_t* EToV, const int32_t* part);
+
+/* Number of elements this rank owns and (optional) their global ids, ascending. */
+DG_API dg_status dg_local_elements(dg_solver* s, int64_t* K_local, int64_t* global_ids);
+
+/* Sizes: Np, Nfp, local and global element counts (any may be NULL). */
+DG_API dg_status dg_get_sizes(dg_solver* s, int32_t* Np, int32_t* Nfp, int64_t* K_local, int64_t* K_global);
+
+/* Upload fields f[6][K_local][Np] (host FP64).  Resets the LSERK residual to 0. */
+DG_API dg_status dg_fields_upload(dg_solver* s, const double* f);
+/* Same from device memory in the solver precision, layout [6][K_local][Np]. */
+DG_API dg_status dg_fields_upload_device(dg_solver* s, const void* f_dev);
+
+/* rhs[6][K_local][Np] (host FP64) = d_t u of the current fields (eq. 4).  Synchronises. */
+DG_API dg_status dg_rhs(dg_solver* s, double* rhs);
+/* Same into device memory in the solver precision, layout [6][K_local][Np]; asynchronous. */
+DG_API dg_status dg_rhs_device(dg_solver* s, void* rhs_dev);
+
+/* Advance nsteps >= 0 LSERK4 steps of size dt (5 stages each; asynchronous,
+ * graph-launched).  With nranks > 1 each stage exchanges partition-face traces. */
+DG_API dg_status dg_lserk_step(dg_solver* s, double dt, int32_t nsteps);
+
+/* Copy the current fields out: host FP64 [6][K_local][Np] (synchronises) or
+ * device memory in the solver precision (asynchronous). */
+DG_API dg_status dg_fields_download(dg_solver* s, double* f);
+DG_API dg_status dg_fields_download_device(dg_solver* s, void* f_dev);
+
+/* Wait for all work enqueued by this solver; surfaces asynchronous CUDA errors. */
+DG_API dg_status dg_synchronize(dg_solver* s);
+
+/* Parity exports of the host setup (work on host-only solvers too).
+ * dg_get_maps: global mesh, EToE[K][4], EToF[K][4] (boundary face -> itself),
+ *   vmapM/vmapP[K][4][Nfp] global node ids k*Np+n (boundary: vmapP = vmapM).
+ * dg_get_nodes: physical node coordinates of the LOCAL elements, [K_local][Np].
+ * dg_get_reference: r,s,t[Np], Dr,Ds,Dt,M[Np][Np], LIFT[Np][4Nfp], Fmask[4][Nfp]
+ *   (row-major FP64; any pointer may be NULL). */
+DG_API dg_status dg_get_maps(dg_solver* s, int64_t* EToE, int8_t* EToF, int64_t* vmapM, int64_t* vmapP);
+DG_API dg_status dg_get_nodes(dg_solver* s, double* x, double* y, double* z);
+DG_API dg_status dg_get_reference(dg_solver* s, double* r, double* st, double* t, double* Dr, double* Ds,
+                           double* Dt, double* M, double* LIFT, int32_t* Fmask);
+/* Geometry of the global mesh: J[K], rst_x[K][9] (rx ry rz sx sy sz tx ty tz),
+ * nrm[K][4][4] (nx ny nz Fscale). */
+DG_API dg_status dg_get_geometry(dg_solver* s, double* J, double* rst_x, double* nrm);
+
+/* Measurement helper: time `reps` back-to-back launches of the LSERK stage
+ * kernel (stage-1 coefficients, reading the current fields, writing the
+ * ping-pong buffer and the residual) with CUDA events on the solver stream;
+ * *ms_per_launch = mean device time per launch.  The current fields are
+ * unchanged; the residual is clobbered, which is harmless because the next
+ * step's first stage ignores it (a_0 = 0). */
+DG_API dg_status dg_time_stage_kernel(dg_solver* s, int32_t reps, double* ms_per_launch);
+
+/* Number of kernel launches one LSERK4 step enqueues on this rank. */
+DG_API dg_status dg_launches_per_step(dg_solver* s, int32_t* n);
+
+/* Thread-local description of the last error ("" if none). */
+DG_API const char* dg_last_error(void);
+/* Library version string (build id, ABI version, compiled arch). */
+DG_API const char* dg_version(void);
+
+/* Free every device and host resource of the solver (NULL is a no-op). */
+DG_API void dg_destroy(dg_solver* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DG_H_ */

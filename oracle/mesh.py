@@ -100,12 +100,12 @@ class Setup:
                     continue                      # boundary face: vmapP = vmapM
                 idM = vmapM[k, f]
                 idP = vmapM[k2, f2]
-                for i in range(Nfp):
-                    d2 = ((xf[idP] - xf[idM[i]]) ** 2 + (yf[idP] - yf[idM[i]]) ** 2
-                          + (zf[idP] - zf[idM[i]]) ** 2)
-                    hit = np.nonzero(d2 < tol2)[0]
-                    if len(hit) != 1:
-                        raise MeshError("unmatched face node")
-                    vmapP[k, f, i] = idP[hit[0]]
+                # d2[i, j] = |x(face node i of k) - x(face node j of k2)|^2
+                d2 = ((xf[idM][:, None] - xf[idP][None, :]) ** 2 + (yf[idM][:, None] - yf[idP][None, :]) ** 2
+                      + (zf[idM][:, None] - zf[idP][None, :]) ** 2)
+                hit = d2 < tol2
+                if not np.all(hit.sum(axis=1) == 1):
+                    raise MeshError("unmatched face node")
+                vmapP[k, f] = idP[np.argmax(hit, axis=1)]
         self.vmapM, self.vmapP = vmapM, vmapP
         self.mapB = vmapP == vmapM                                  # [K][4][Nfp] boundary slots

@@ -1,0 +1,671 @@
+// C-ABI implementation of libdg (see include/dg.h for the contract).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/dg.h"
+#include "host/mesh.h"
+#include "host/partition.h"
+#include "host/refelem.h"
+#include "kernels/stage_params.h"
+
+namespace dg {
+template <typename S, typename T>
+void cm_to_tiles(const S* src, T* dst, int64_t K, int Np, int64_t ES, void* st);
+template <typename T, typename D>
+void tiles_to_cm(const T* src, D* dst, int64_t K, int Np, int64_t ES, void* st);
+template <typename T>
+void pack_traces(const T* u, T* buf, const int32_t* sidx, int64_t nfaces, int Np, int Nfp, void* st);
+}  // namespace dg
+
+namespace {
+
+thread_local std::string g_err;
+
+dg_status fail(dg_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+// NCCL is loaded lazily and only for nranks > 1; its types are re-declared
+// here (ABI-stable across 2.x) so the library has no link-time NCCL dependency.
+typedef struct ncclComm* ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef int ncclResult_t;
+enum { ncclFloat32_ = 7, ncclFloat64_ = 8 };
+struct NcclApi {
+  bool ok = false;
+  std::string err;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) { a.err = std::string("cannot dlopen libnccl.so.2: ") + dlerror(); return a; }
+    a.CommInitRank = (decltype(a.CommInitRank))dlsym(h, "ncclCommInitRank");
+    a.CommDestroy = (decltype(a.CommDestroy))dlsym(h, "ncclCommDestroy");
+    a.Send = (decltype(a.Send))dlsym(h, "ncclSend");
+    a.Recv = (decltype(a.Recv))dlsym(h, "ncclRecv");
+    a.GroupStart = (decltype(a.GroupStart))dlsym(h, "ncclGroupStart");
+    a.GroupEnd = (decltype(a.GroupEnd))dlsym(h, "ncclGroupEnd");
+    a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
+    a.ok = a.CommInitRank && a.CommDestroy && a.Send && a.Recv && a.GroupStart && a.GroupEnd;
+    if (!a.ok) a.err = "libnccl is missing required symbols";
+    return a;
+  }();
+  return api;
+}
+
+// LSERK4 coefficients: Carpenter & Kennedy (5,4), as tabulated in HW (reading R5)
+const double kRkA[5] = {0.0, -567301805773.0 / 1357537059087.0, -2404267990393.0 / 2016746695238.0,
+                        -3550918686646.0 / 2091501179385.0, -1275806237668.0 / 842570457699.0};
+const double kRkB[5] = {1432997174477.0 / 9575080441755.0, 5161836677717.0 / 13612068292357.0,
+                        1720146321549.0 / 2090206949498.0, 3134564353537.0 / 4481467310338.0,
+                        2277821191437.0 / 14882151754819.0};
+
+}  // namespace
+
+struct dg_solver {
+  dg_config cfg{};
+  int N = 0, Np = 0, Nfp = 0;
+  bool host_only = false;
+  bool fp64 = true;
+  size_t wsize = 8;
+  dg::RefElem ref;
+  dg::MeshData mesh;
+  dg::Partition part;
+  bool has_mesh = false, has_fields = false;
+  // device
+  int64_t ES = 0, ghost_base = 0, ghost_words = 0, Kl = 0;
+  void* d_u[2] = {nullptr, nullptr};
+  void* d_res = nullptr;
+  void* d_scratch = nullptr;   // [Kl][ES] (solver precision)
+  double* d_stage64 = nullptr; // [6][Kl][Np] FP64 host-layout staging
+  void* d_geo = nullptr;
+  int32_t* d_gidx = nullptr;
+  void* d_ops = nullptr;
+  int16_t* d_fmask = nullptr;
+  void* d_send = nullptr;      // [n_ghost][6][Nfp]
+  int32_t* d_sidx = nullptr;   // [n_ghost][Nfp] element-node offsets for packing
+  cudaStream_t stream = nullptr, comm = nullptr;
+  bool own_stream = false;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+  ncclComm_t ncomm = nullptr;
+  int cur = 0;
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  double graph_dt[2] = {0, 0};
+  int variant = DG_VARIANT_AUTO;
+};
+
+namespace {
+
+dg_status cuda_fail(cudaError_t e, const char* what) {
+  if (e == cudaErrorMemoryAllocation) return fail(DG_ERR_OOM, std::string(what) + ": out of device memory");
+  return fail(DG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(call)                                   \
+  do {                                             \
+    cudaError_t e_ = (call);                       \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+void free_dev(void*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+void release_device(dg_solver* s) {
+  for (int i = 0; i < 2; ++i) {
+    if (s->graph[i]) cudaGraphExecDestroy(s->graph[i]);
+    s->graph[i] = nullptr;
+    free_dev(s->d_u[i]);
+  }
+  free_dev(s->d_res);
+  free_dev(s->d_scratch);
+  void* p = s->d_stage64; free_dev(p); s->d_stage64 = nullptr;
+  free_dev(s->d_geo);
+  p = s->d_gidx; free_dev(p); s->d_gidx = nullptr;
+  free_dev(s->d_ops);
+  p = s->d_fmask; free_dev(p); s->d_fmask = nullptr;
+  free_dev(s->d_send);
+  p = s->d_sidx; free_dev(p); s->d_sidx = nullptr;
+}
+
+dg_status need_device(dg_solver* s) {
+  if (!s) return fail(DG_ERR_ARG, "null solver");
+  if (s->host_only) return fail(DG_ERR_STATE, "compute call on a host-only solver (device = -1)");
+  cudaError_t e = cudaSetDevice(s->cfg.device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  return DG_OK;
+}
+
+template <typename T>
+dg::StageParams<T> base_params(dg_solver* s) {
+  dg::StageParams<T> p{};
+  p.geo = static_cast<const T*>(s->d_geo);
+  p.gidx = s->d_gidx;
+  p.ops = static_cast<const T*>(s->d_ops);
+  p.fmask = s->d_fmask;
+  p.ES = s->ES;
+  p.ghost_base = s->ghost_base;
+  p.alpha = T(s->cfg.alpha);
+  p.K = s->Kl;
+  p.k_begin = 0;
+  return p;
+}
+
+template <typename T>
+void launch_stage(dg_solver* s, dg::StageParams<T> p, int mode, int64_t k0, int64_t k1, cudaStream_t st) {
+  dg::StageLauncher<T> L;
+  if constexpr (sizeof(T) == 8)
+    L = dg::stage_launcher_f64(s->N);
+  else
+    L = dg::stage_launcher_f32(s->N);
+  p.k_begin = k0;
+  p.K = k1 - k0;
+  L(p, mode, s->variant, st);
+}
+
+// Exchange partition-face traces of u (multi-rank): pack on the comm stream,
+// grouped ncclSend/ncclRecv into u's ghost region.
+template <typename T>
+dg_status enqueue_exchange(dg_solver* s, T* u) {
+  const auto& P = s->part;
+  if (P.n_ghost_faces == 0) return DG_OK;
+  dg::pack_traces<T>(u, static_cast<T*>(s->d_send), s->d_sidx, P.n_ghost_faces, s->Np, s->Nfp, s->comm);
+  NcclApi& n = nccl();
+  const size_t rec = size_t(6) * s->Nfp;
+  const int dtype = sizeof(T) == 8 ? ncclFloat64_ : ncclFloat32_;
+  if (n.GroupStart() != 0) return fail(DG_ERR_NCCL, "ncclGroupStart failed");
+  for (const auto& pp : P.peers) {
+    T* sb = static_cast<T*>(s->d_send) + pp.send_off * rec;
+    T* rb = u + s->ghost_base + pp.recv_off * rec;
+    ncclResult_t r1 = n.Send(sb, pp.nfaces * rec, dtype, pp.rank, s->ncomm, s->comm);
+    ncclResult_t r2 = n.Recv(rb, pp.nfaces * rec, dtype, pp.rank, s->ncomm, s->comm);
+    if (r1 != 0 || r2 != 0) { n.GroupEnd(); return fail(DG_ERR_NCCL, "ncclSend/ncclRecv failed"); }
+  }
+  if (n.GroupEnd() != 0) return fail(DG_ERR_NCCL, "ncclGroupEnd failed");
+  return DG_OK;
+}
+
+// One LSERK stage s: u[cur] -> u[cur^1]; with ghosts: interior range overlaps the exchange.
+template <typename T>
+dg_status enqueue_stage(dg_solver* s, int stage, double dt, int cur) {
+  dg::StageParams<T> p = base_params<T>(s);
+  T* uin = static_cast<T*>(s->d_u[cur]);
+  p.u_in = uin;
+  p.u_out = static_cast<T*>(s->d_u[cur ^ 1]);
+  p.res = static_cast<T*>(s->d_res);
+  p.rk_a = T(kRkA[stage]);
+  p.rk_b = T(kRkB[stage]);
+  p.dt = T(dt);
+  p.first_stage = stage == 0 ? 1 : 0;
+  if (s->part.n_ghost_faces > 0) {
+    CK(cudaEventRecord(s->ev_fork, s->stream));
+    CK(cudaStreamWaitEvent(s->comm, s->ev_fork, 0));
+    dg_status st = enqueue_exchange<T>(s, uin);
+    if (st != DG_OK) return st;
+    CK(cudaEventRecord(s->ev_join, s->comm));
+    launch_stage<T>(s, p, 1, 0, s->part.K_interior, s->stream);
+    CK(cudaStreamWaitEvent(s->stream, s->ev_join, 0));
+    launch_stage<T>(s, p, 1, s->part.K_interior, s->Kl, s->stream);
+  } else {
+    launch_stage<T>(s, p, 1, 0, s->Kl, s->stream);
+  }
+  CK(cudaGetLastError());
+  return DG_OK;
+}
+
+template <typename T>
+dg_status enqueue_rhs(dg_solver* s, T* out_tiles) {
+  dg::StageParams<T> p = base_params<T>(s);
+  T* uin = static_cast<T*>(s->d_u[s->cur]);
+  p.u_in = uin;
+  p.rhs_out = out_tiles;
+  if (s->part.n_ghost_faces > 0) {
+    CK(cudaEventRecord(s->ev_fork, s->stream));
+    CK(cudaStreamWaitEvent(s->comm, s->ev_fork, 0));
+    dg_status st = enqueue_exchange<T>(s, uin);
+    if (st != DG_OK) return st;
+    CK(cudaEventRecord(s->ev_join, s->comm));
+    CK(cudaStreamWaitEvent(s->stream, s->ev_join, 0));
+  }
+  launch_stage<T>(s, p, 0, 0, s->Kl, s->stream);
+  CK(cudaGetLastError());
+  return DG_OK;
+}
+
+template <typename T>
+dg_status upload_setup(dg_solver* s) {
+  const auto& m = s->mesh;
+  const auto& P = s->part;
+  const int Np = s->Np, Nfp = s->Nfp, NF = 4 * Nfp;
+  const int64_t Kl = P.K_local;
+  s->Kl = Kl;
+  s->ES = sizeof(T) == 8 ? 6 * Np : ((6 * Np + 3) / 4) * 4;
+  s->ghost_base = Kl * s->ES;
+  s->ghost_words = P.n_ghost_faces * 6 * Nfp;
+  const int64_t uwords = s->ghost_base + s->ghost_words;
+  if (uwords >= (int64_t(1) << 31))
+    return fail(DG_ERR_ARG, "local problem too large for 32-bit gather indices on one rank (partition further)");
+  const size_t wb = sizeof(T);
+  for (int i = 0; i < 2; ++i) {
+    CK(cudaMalloc(&s->d_u[i], std::max<int64_t>(uwords, 1) * wb));
+    CK(cudaMemsetAsync(s->d_u[i], 0, std::max<int64_t>(uwords, 1) * wb, s->stream));
+  }
+  CK(cudaMalloc(&s->d_res, std::max<int64_t>(Kl * s->ES, 1) * wb));
+  CK(cudaMalloc(&s->d_scratch, std::max<int64_t>(Kl * s->ES, 1) * wb));
+  CK(cudaMalloc((void**)&s->d_stage64, std::max<int64_t>(6 * Kl * Np, 1) * sizeof(double)));
+  // geometry [Kl][GEO_W]
+  std::vector<T> geo(size_t(std::max<int64_t>(Kl, 1)) * dg::GEO_W, T(0));
+  for (int64_t l = 0; l < Kl; ++l) {
+    const int64_t k = P.local_ids[l];
+    for (int i = 0; i < 9; ++i) geo[l * dg::GEO_W + i] = T(m.rst_x[9 * k + i]);
+    for (int i = 0; i < 16; ++i) geo[l * dg::GEO_W + 9 + i] = T(m.nrm[16 * k + i]);
+  }
+  CK(cudaMalloc(&s->d_geo, geo.size() * wb));
+  CK(cudaMemcpy(s->d_geo, geo.data(), geo.size() * wb, cudaMemcpyHostToDevice));
+  std::vector<int32_t> gidx;
+  dg::build_gather_index(s->ref, m, P, s->ES, s->ghost_base, gidx);
+  if (gidx.empty()) gidx.push_back(-1);
+  CK(cudaMalloc((void**)&s->d_gidx, gidx.size() * sizeof(int32_t)));
+  CK(cudaMemcpy(s->d_gidx, gidx.data(), gidx.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  // operators Dr|Ds|Dt|LIFT
+  std::vector<T> ops(size_t(3) * Np * Np + size_t(Np) * NF);
+  for (int i = 0; i < Np; ++i)
+    for (int j = 0; j < Np; ++j) {
+      ops[size_t(i) * Np + j] = T(s->ref.Dr(i, j));
+      ops[size_t(Np) * Np + size_t(i) * Np + j] = T(s->ref.Ds(i, j));
+      ops[size_t(2) * Np * Np + size_t(i) * Np + j] = T(s->ref.Dt(i, j));
+    }
+  for (int i = 0; i < Np; ++i)
+    for (int j = 0; j < NF; ++j) ops[size_t(3) * Np * Np + size_t(i) * NF + j] = T(s->ref.LIFT(i, j));
+  CK(cudaMalloc(&s->d_ops, ops.size() * wb));
+  CK(cudaMemcpy(s->d_ops, ops.data(), ops.size() * wb, cudaMemcpyHostToDevice));
+  std::vector<int16_t> fm(NF);
+  for (int i = 0; i < NF; ++i) fm[i] = int16_t(s->ref.Fmask[i]);
+  CK(cudaMalloc((void**)&s->d_fmask, NF * sizeof(int16_t)));
+  CK(cudaMemcpy(s->d_fmask, fm.data(), NF * sizeof(int16_t), cudaMemcpyHostToDevice));
+  if (P.n_ghost_faces > 0) {
+    CK(cudaMalloc(&s->d_send, P.n_ghost_faces * 6 * Nfp * wb));
+    std::vector<int32_t> sidx(size_t(P.n_ghost_faces) * Nfp);
+    for (int64_t g = 0; g < P.n_ghost_faces; ++g)
+      for (int j = 0; j < Nfp; ++j)
+        sidx[g * Nfp + j] = int32_t(P.send_elem[g] * s->ES + s->ref.Fmask[P.send_face[g] * Nfp + j]);
+    CK(cudaMalloc((void**)&s->d_sidx, sidx.size() * sizeof(int32_t)));
+    CK(cudaMemcpy(s->d_sidx, sidx.data(), sidx.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
+  CK(cudaStreamSynchronize(s->stream));
+  return DG_OK;
+}
+
+template <typename T>
+dg_status capture_step(dg_solver* s, int parity, double dt) {
+  if (s->graph[parity]) {
+    cudaGraphExecDestroy(s->graph[parity]);
+    s->graph[parity] = nullptr;
+  }
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+  dg_status st = DG_OK;
+  int cur = parity;
+  for (int stage = 0; stage < 5 && st == DG_OK; ++stage) {
+    st = enqueue_stage<T>(s, stage, dt, cur);
+    cur ^= 1;
+  }
+  cudaError_t e = cudaStreamEndCapture(s->stream, &g);
+  if (st != DG_OK) { if (g) cudaGraphDestroy(g); return st; }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+  e = cudaGraphInstantiate(&s->graph[parity], g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+  s->graph_dt[parity] = dt;
+  return DG_OK;
+}
+
+template <typename T>
+dg_status lserk_steps(dg_solver* s, double dt, int nsteps) {
+  for (int n = 0; n < nsteps; ++n) {
+    const int par = s->cur;
+    if (!s->graph[par] || s->graph_dt[par] != dt) {
+      dg_status st = capture_step<T>(s, par, dt);
+      if (st != DG_OK) return st;
+    }
+    CK(cudaGraphLaunch(s->graph[par], s->stream));
+    s->cur ^= 1;  // five stages: odd number of ping-pong swaps
+  }
+  return DG_OK;
+}
+
+template <typename T>
+dg_status time_stage(dg_solver* s, int reps, double* ms) {
+  for (int i = 0; i < reps + 1; ++i) {
+    if (i == 1) CK(cudaEventRecord(s->ev_t0, s->stream));
+    dg::StageParams<T> p = base_params<T>(s);
+    p.u_in = static_cast<T*>(s->d_u[s->cur]);
+    p.u_out = static_cast<T*>(s->d_u[s->cur ^ 1]);
+    p.res = static_cast<T*>(s->d_res);
+    p.rk_a = T(kRkA[1]);
+    p.rk_b = T(kRkB[1]);
+    p.dt = T(1e-6);
+    p.first_stage = 0;
+    launch_stage<T>(s, p, 1, 0, s->Kl, s->stream);
+  }
+  CK(cudaEventRecord(s->ev_t1, s->stream));
+  CK(cudaEventSynchronize(s->ev_t1));
+  CK(cudaGetLastError());
+  float f = 0;
+  CK(cudaEventElapsedTime(&f, s->ev_t0, s->ev_t1));
+  *ms = double(f) / reps;
+  return DG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void dg_config_default(dg_config* c) {
+  if (!c) return;
+  std::memset(c, 0, sizeof(*c));
+  c->order = 3;
+  c->precision = 8;
+  c->alpha = 1.0;
+  c->device = 0;
+  c->stream = nullptr;
+  c->rank = 0;
+  c->nranks = 1;
+  c->nccl_id = nullptr;
+  c->variant = DG_VARIANT_AUTO;
+}
+
+const char* dg_last_error(void) { return g_err.c_str(); }
+
+const char* dg_version(void) {
+  return "dg-b200 abi " "1" " sm_100a (" __DATE__ " " __TIME__ ")";
+}
+
+dg_status dg_create(const dg_config* cfg, dg_solver** out) {
+  g_err.clear();
+  if (!cfg || !out) return fail(DG_ERR_ARG, "null argument");
+  *out = nullptr;
+  if (cfg->order < 1 || cfg->order > 9) return fail(DG_ERR_ORDER, "order N must be in 1..9");
+  if (cfg->precision != 4 && cfg->precision != 8) return fail(DG_ERR_ARG, "precision must be 4 or 8");
+  if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return fail(DG_ERR_ARG, "bad rank/nranks");
+  if (cfg->variant < 0 || cfg->variant > 2) return fail(DG_ERR_ARG, "bad variant");
+  std::unique_ptr<dg_solver> s(new dg_solver());
+  s->cfg = *cfg;
+  s->N = cfg->order;
+  s->fp64 = cfg->precision == 8;
+  s->wsize = s->fp64 ? 8 : 4;
+  s->variant = cfg->variant;
+  s->host_only = cfg->device < 0;
+  try {
+    s->ref = dg::build_ref_elem(s->N);
+  } catch (const std::exception& e) {
+    return fail(DG_ERR_ORDER, std::string("reference element: ") + e.what());
+  }
+  s->Np = s->ref.Np;
+  s->Nfp = s->ref.Nfp;
+  if (!s->host_only) {
+    if (cfg->nranks > 1 && !cfg->nccl_id) return fail(DG_ERR_ARG, "nccl_id required with nranks > 1");
+    CK(cudaSetDevice(cfg->device));
+    if (cfg->stream) {
+      s->stream = static_cast<cudaStream_t>(cfg->stream);
+    } else {
+      CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+      s->own_stream = true;
+    }
+    CK(cudaStreamCreateWithFlags(&s->comm, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
+    CK(cudaEventCreate(&s->ev_t0));
+    CK(cudaEventCreate(&s->ev_t1));
+    if (cfg->nranks > 1) {
+      NcclApi& n = nccl();
+      if (!n.ok) return fail(DG_ERR_NCCL, n.err);
+      ncclUniqueId id;
+      std::memcpy(&id, cfg->nccl_id, sizeof(id));
+      ncclResult_t r = n.CommInitRank(&s->ncomm, cfg->nranks, id, cfg->rank);
+      if (r != 0)
+        return fail(DG_ERR_NCCL, std::string("ncclCommInitRank: ") + (n.GetErrorString ? n.GetErrorString(r) : "?"));
+    }
+  }
+  *out = s.release();
+  return DG_OK;
+}
+
+dg_status dg_mesh_upload(dg_solver* s, int64_t nv, const double* VX, int64_t K, const int64_t* EToV,
+                         const int32_t* part) {
+  g_err.clear();
+  if (!s || !VX || !EToV || nv <= 0 || K <= 0) return fail(DG_ERR_ARG, "bad mesh arguments");
+  std::string err;
+  try {
+    err = dg::build_mesh(s->ref, nv, VX, K, EToV, s->mesh);
+    if (err.empty()) err = dg::build_partition(s->mesh, s->cfg.rank, s->cfg.nranks, part, s->part);
+  } catch (const std::exception& e) {
+    err = e.what();
+  }
+  if (!err.empty()) {
+    s->has_mesh = false;
+    return fail(DG_ERR_MESH, err);
+  }
+  s->has_mesh = true;
+  s->has_fields = false;
+  s->Kl = s->part.K_local;
+  if (s->host_only) return DG_OK;
+  dg_status st = need_device(s);
+  if (st != DG_OK) return st;
+  CK(cudaStreamSynchronize(s->stream));
+  release_device(s);
+  s->cur = 0;
+  return s->fp64 ? upload_setup<double>(s) : upload_setup<float>(s);
+}
+
+dg_status dg_local_elements(dg_solver* s, int64_t* K_local, int64_t* ids) {
+  if (!s) return fail(DG_ERR_ARG, "null solver");
+  if (!s->has_mesh) return fail(DG_ERR_STATE, "no mesh uploaded");
+  if (K_local) *K_local = s->part.K_local;
+  if (ids) std::memcpy(ids, s->part.local_ids.data(), s->part.K_local * sizeof(int64_t));
+  return DG_OK;
+}
+
+dg_status dg_get_sizes(dg_solver* s, int32_t* Np, int32_t* Nfp, int64_t* K_local, int64_t* K_global) {
+  if (!s) return fail(DG_ERR_ARG, "null solver");
+  if (Np) *Np = s->Np;
+  if (Nfp) *Nfp = s->Nfp;
+  if (K_local) *K_local = s->has_mesh ? s->part.K_local : 0;
+  if (K_global) *K_global = s->has_mesh ? s->mesh.K : 0;
+  return DG_OK;
+}
+
+static dg_status upload_common(dg_solver* s, const void* src, bool from_host) {
+  dg_status st = need_device(s);
+  if (st != DG_OK) return st;
+  if (!s->has_mesh) return fail(DG_ERR_STATE, "no mesh uploaded");
+  if (!src) return fail(DG_ERR_ARG, "null field pointer");
+  const int64_t n = 6 * s->Kl * s->Np;
+  s->cur = 0;
+  if (from_host) {
+    CK(cudaMemcpyAsync(s->d_stage64, src, n * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+    if (s->fp64)
+      dg::cm_to_tiles<double, double>(s->d_stage64, static_cast<double*>(s->d_u[0]), s->Kl, s->Np, s->ES, s->stream);
+    else
+      dg::cm_to_tiles<double, float>(s->d_stage64, static_cast<float*>(s->d_u[0]), s->Kl, s->Np, s->ES, s->stream);
+  } else {
+    if (s->fp64)
+      dg::cm_to_tiles<double, double>(static_cast<const double*>(src), static_cast<double*>(s->d_u[0]), s->Kl,
+                                      s->Np, s->ES, s->stream);
+    else
+      dg::cm_to_tiles<float, float>(static_cast<const float*>(src), static_cast<float*>(s->d_u[0]), s->Kl, s->Np,
+                                    s->ES, s->stream);
+  }
+  CK(cudaGetLastError());
+  CK(cudaMemsetAsync(s->d_res, 0, std::max<int64_t>(s->Kl * s->ES, 1) * s->wsize, s->stream));
+  if (from_host) CK(cudaStreamSynchronize(s->stream));
+  s->has_fields = true;
+  return DG_OK;
+}
+
+dg_status dg_fields_upload(dg_solver* s, const double* f) { g_err.clear(); return upload_common(s, f, true); }
+dg_status dg_fields_upload_device(dg_solver* s, const void* f) { g_err.clear(); return upload_common(s, f, false); }
+
+static dg_status download_common(dg_solver* s, void* dst, bool to_host, bool rhs) {
+  dg_status st = need_device(s);
+  if (st != DG_OK) return st;
+  if (!s->has_fields) return fail(DG_ERR_STATE, "no fields uploaded");
+  if (!dst) return fail(DG_ERR_ARG, "null output pointer");
+  const int64_t n = 6 * s->Kl * s->Np;
+  const void* tiles = s->d_u[s->cur];
+  if (rhs) {
+    st = s->fp64 ? enqueue_rhs<double>(s, static_cast<double*>(s->d_scratch))
+                 : enqueue_rhs<float>(s, static_cast<float*>(s->d_scratch));
+    if (st != DG_OK) return st;
+    tiles = s->d_scratch;
+  }
+  if (to_host) {
+    if (s->fp64)
+      dg::tiles_to_cm<double, double>(static_cast<const double*>(tiles), s->d_stage64, s->Kl, s->Np, s->ES, s->stream);
+    else
+      dg::tiles_to_cm<float, double>(static_cast<const float*>(tiles), s->d_stage64, s->Kl, s->Np, s->ES, s->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(dst, s->d_stage64, n * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+  } else {
+    if (s->fp64)
+      dg::tiles_to_cm<double, double>(static_cast<const double*>(tiles), static_cast<double*>(dst), s->Kl, s->Np,
+                                      s->ES, s->stream);
+    else
+      dg::tiles_to_cm<float, float>(static_cast<const float*>(tiles), static_cast<float*>(dst), s->Kl, s->Np, s->ES,
+                                    s->stream);
+    CK(cudaGetLastError());
+  }
+  return DG_OK;
+}
+
+dg_status dg_fields_download(dg_solver* s, double* f) { g_err.clear(); return download_common(s, f, true, false); }
+dg_status dg_fields_download_device(dg_solver* s, void* f) { g_err.clear(); return download_common(s, f, false, false); }
+dg_status dg_rhs(dg_solver* s, double* r) { g_err.clear(); return download_common(s, r, true, true); }
+dg_status dg_rhs_device(dg_solver* s, void* r) { g_err.clear(); return download_common(s, r, false, true); }
+
+dg_status dg_lserk_step(dg_solver* s, double dt, int32_t nsteps) {
+  g_err.clear();
+  dg_status st = need_device(s);
+  if (st != DG_OK) return st;
+  if (!s->has_fields) return fail(DG_ERR_STATE, "no fields uploaded");
+  if (nsteps < 0) return fail(DG_ERR_ARG, "nsteps < 0");
+  return s->fp64 ? lserk_steps<double>(s, dt, nsteps) : lserk_steps<float>(s, dt, nsteps);
+}
+
+dg_status dg_synchronize(dg_solver* s) {
+  dg_status st = need_device(s);
+  if (st != DG_OK) return st;
+  CK(cudaStreamSynchronize(s->stream));
+  CK(cudaStreamSynchronize(s->comm));
+  CK(cudaGetLastError());
+  return DG_OK;
+}
+
+dg_status dg_get_maps(dg_solver* s, int64_t* EToE, int8_t* EToF, int64_t* vmapM, int64_t* vmapP) {
+  if (!s) return fail(DG_ERR_ARG, "null solver");
+  if (!s->has_mesh) return fail(DG_ERR_STATE, "no mesh uploaded");
+  const auto& m = s->mesh;
+  if (EToE) std::memcpy(EToE, m.EToE.data(), m.EToE.size() * sizeof(int64_t));
+  if (EToF) std::memcpy(EToF, m.EToF.data(), m.EToF.size());
+  if (vmapM) std::memcpy(vmapM, m.vmapM.data(), m.vmapM.size() * sizeof(int64_t));
+  if (vmapP) std::memcpy(vmapP, m.vmapP.data(), m.vmapP.size() * sizeof(int64_t));
+  return DG_OK;
+}
+
+dg_status dg_get_nodes(dg_solver* s, double* x, double* y, double* z) {
+  if (!s || !x || !y || !z) return fail(DG_ERR_ARG, "null argument");
+  if (!s->has_mesh) return fail(DG_ERR_STATE, "no mesh uploaded");
+  const int64_t K = s->mesh.K, Np = s->Np;
+  std::vector<double> X(K * Np), Y(K * Np), Z(K * Np);
+  dg::node_coords(s->ref, s->mesh, X.data(), Y.data(), Z.data());
+  for (int64_t l = 0; l < s->part.K_local; ++l) {
+    const int64_t k = s->part.local_ids[l];
+    std::memcpy(x + l * Np, &X[k * Np], Np * sizeof(double));
+    std::memcpy(y + l * Np, &Y[k * Np], Np * sizeof(double));
+    std::memcpy(z + l * Np, &Z[k * Np], Np * sizeof(double));
+  }
+  return DG_OK;
+}
+
+dg_status dg_get_reference(dg_solver* s, double* r, double* st_, double* t, double* Dr, double* Ds, double* Dt,
+                           double* M, double* LIFT, int32_t* Fmask) {
+  if (!s) return fail(DG_ERR_ARG, "null solver");
+  const auto& R = s->ref;
+  const size_t Np = R.Np;
+  if (r) std::memcpy(r, R.r.data(), Np * sizeof(double));
+  if (st_) std::memcpy(st_, R.s.data(), Np * sizeof(double));
+  if (t) std::memcpy(t, R.t.data(), Np * sizeof(double));
+  if (Dr) std::memcpy(Dr, R.Dr.a.data(), Np * Np * sizeof(double));
+  if (Ds) std::memcpy(Ds, R.Ds.a.data(), Np * Np * sizeof(double));
+  if (Dt) std::memcpy(Dt, R.Dt.a.data(), Np * Np * sizeof(double));
+  if (M) std::memcpy(M, R.M.a.data(), Np * Np * sizeof(double));
+  if (LIFT) std::memcpy(LIFT, R.LIFT.a.data(), R.LIFT.a.size() * sizeof(double));
+  if (Fmask)
+    for (size_t i = 0; i < R.Fmask.size(); ++i) Fmask[i] = R.Fmask[i];
+  return DG_OK;
+}
+
+dg_status dg_get_geometry(dg_solver* s, double* J, double* rst_x, double* nrm) {
+  if (!s) return fail(DG_ERR_ARG, "null solver");
+  if (!s->has_mesh) return fail(DG_ERR_STATE, "no mesh uploaded");
+  const auto& m = s->mesh;
+  if (J) std::memcpy(J, m.J.data(), m.J.size() * sizeof(double));
+  if (rst_x) std::memcpy(rst_x, m.rst_x.data(), m.rst_x.size() * sizeof(double));
+  if (nrm) std::memcpy(nrm, m.nrm.data(), m.nrm.size() * sizeof(double));
+  return DG_OK;
+}
+
+dg_status dg_time_stage_kernel(dg_solver* s, int32_t reps, double* ms) {
+  g_err.clear();
+  dg_status st = need_device(s);
+  if (st != DG_OK) return st;
+  if (!s->has_fields) return fail(DG_ERR_STATE, "no fields uploaded");
+  if (reps < 1 || !ms) return fail(DG_ERR_ARG, "reps < 1 or null output");
+  return s->fp64 ? time_stage<double>(s, reps, ms) : time_stage<float>(s, reps, ms);
+}
+
+dg_status dg_launches_per_step(dg_solver* s, int32_t* n) {
+  if (!s || !n) return fail(DG_ERR_ARG, "null argument");
+  const bool halo = s->has_mesh && s->part.n_ghost_faces > 0;
+  *n = 5 * (halo ? 3 : 1);  // per stage: stage kernel (+ pack kernel + second stage range)
+  return DG_OK;
+}
+
+void dg_destroy(dg_solver* s) {
+  if (!s) return;
+  if (!s->host_only) {
+    cudaSetDevice(s->cfg.device);
+    if (s->stream) cudaStreamSynchronize(s->stream);
+    if (s->comm) cudaStreamSynchronize(s->comm);
+    release_device(s);
+    if (s->ncomm && nccl().ok) nccl().CommDestroy(s->ncomm);
+    if (s->ev_fork) cudaEventDestroy(s->ev_fork);
+    if (s->ev_join) cudaEventDestroy(s->ev_join);
+    if (s->ev_t0) cudaEventDestroy(s->ev_t0);
+    if (s->ev_t1) cudaEventDestroy(s->ev_t1);
+    if (s->comm) cudaStreamDestroy(s->comm);
+    if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
+  }
+  delete s;
+}
+
+}  // extern "C"

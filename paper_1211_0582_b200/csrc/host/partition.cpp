@@ -1,0 +1,94 @@
+// Partition, ghost-face plan and gather indices (see partition.h).
+#include "partition.h"
+
+#include <algorithm>
+#include <map>
+
+namespace dg {
+
+std::string build_partition(const MeshData& m, int rank, int nranks, const int32_t* owner,
+                            Partition& P) {
+  const int64_t K = m.K;
+  P = Partition();
+  P.rank = rank;
+  P.nranks = nranks;
+  P.K_global = K;
+  std::vector<int32_t> own(K);
+  for (int64_t k = 0; k < K; ++k) {
+    own[k] = owner ? owner[k] : int32_t((k * nranks) / K);
+    if (own[k] < 0 || own[k] >= nranks) return "partition owner out of range at element " + std::to_string(k);
+  }
+  // per rank pair: cross faces keyed by the lower-rank side's slot
+  std::map<int, std::vector<std::pair<int64_t, int64_t>>> cross;  // peer -> (key, my slot)
+  std::vector<char> is_bnd(K, 0);
+  for (int64_t k = 0; k < K; ++k) {
+    if (own[k] != rank) continue;
+    for (int f = 0; f < 4; ++f) {
+      const int64_t k2 = m.EToE[4 * k + f];
+      const int f2 = m.EToF[4 * k + f];
+      const int q = own[k2];
+      if (q == rank) continue;
+      is_bnd[k] = 1;
+      const int64_t mine = 4 * k + f, theirs = 4 * k2 + f2;
+      const int64_t key = rank < q ? mine : theirs;
+      cross[q].push_back({key, mine});
+    }
+  }
+  for (int64_t k = 0; k < K; ++k)
+    if (own[k] == rank && !is_bnd[k]) P.local_ids.push_back(k);
+  P.K_interior = int64_t(P.local_ids.size());
+  for (int64_t k = 0; k < K; ++k)
+    if (own[k] == rank && is_bnd[k]) P.local_ids.push_back(k);
+  P.K_local = int64_t(P.local_ids.size());
+  P.g2l.assign(K, -1);
+  for (int64_t l = 0; l < P.K_local; ++l) P.g2l[P.local_ids[l]] = l;
+  P.ghost_of.assign(4 * P.K_local, -1);
+  int64_t off = 0;
+  for (auto& kv : cross) {
+    auto& v = kv.second;
+    std::sort(v.begin(), v.end());
+    PeerPlan pp;
+    pp.rank = kv.first;
+    pp.nfaces = int64_t(v.size());
+    pp.send_off = off;
+    pp.recv_off = off;  // symmetric: the peer has the same cross faces
+    for (size_t i = 0; i < v.size(); ++i) {
+      const int64_t slot = v[i].second;
+      const int64_t l = P.g2l[slot / 4];
+      P.send_elem.push_back(l);
+      P.send_face.push_back(int8_t(slot % 4));
+      P.ghost_of[4 * l + slot % 4] = off + int64_t(i);
+    }
+    off += pp.nfaces;
+    P.peers.push_back(pp);
+  }
+  P.n_ghost_faces = off;
+  return "";
+}
+
+void build_gather_index(const RefElem& ref, const MeshData& m, const Partition& P, int64_t ES,
+                        int64_t ghost_base, std::vector<int32_t>& gidx) {
+  const int Nfp = ref.Nfp;
+  gidx.assign(size_t(P.K_local) * 4 * Nfp, -1);
+  for (int64_t l = 0; l < P.K_local; ++l) {
+    const int64_t k = P.local_ids[l];
+    for (int f = 0; f < 4; ++f) {
+      const int64_t k2 = m.EToE[4 * k + f];
+      const int f2 = m.EToF[4 * k + f];
+      if (k2 == k && f2 == f) continue;  // PEC wall
+      const int code = m.orient[4 * k + f];
+      const int64_t g = P.ghost_of[4 * l + f];
+      for (int i = 0; i < Nfp; ++i) {
+        const int j = m.fperm[code * Nfp + i];  // neighbour face-node position
+        int64_t v;
+        if (g >= 0)
+          v = ghost_base + g * 6 * Nfp + j;
+        else
+          v = P.g2l[k2] * ES + ref.Fmask[f2 * Nfp + j];
+        gidx[(4 * l + f) * Nfp + i] = int32_t(v);
+      }
+    }
+  }
+}
+
+}  // namespace dg

@@ -1,0 +1,53 @@
+// Mesh partition for multi-GPU runs (distributed DG, one
+// exchange of face data per stage; volume ~ N^3 vs surface ~ N^2).
+//
+// Each rank owns a set of elements.  Local storage order: elements with no
+// face on another rank ("interior") first, then the partition-boundary
+// elements, each group in ascending global id, so that a stage can run the
+// interior range while the face traces are in flight.
+//
+// Ghost faces: for every rank pair (r, q) the cross faces are ordered by the
+// global slot 4k+f of the face on the LOWER rank; rank r sends, for each of its
+// cross faces in that order, the 6*Nfp traces u[k][c][Fmask[f][j]] in its own
+// face-node order (record [c][j]); the receiver reads its u+ from the record
+// through the same orientation permutation it uses for a local neighbour.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "mesh.h"
+
+namespace dg {
+
+struct PeerPlan {
+  int rank = -1;            // peer rank
+  int64_t nfaces = 0;       // cross faces with this peer
+  int64_t send_off = 0;     // offset (faces) into this rank's send buffer
+  int64_t recv_off = 0;     // offset (faces) into this rank's ghost region
+};
+
+struct Partition {
+  int rank = 0, nranks = 1;
+  int64_t K_global = 0, K_local = 0, K_interior = 0;
+  std::vector<int64_t> local_ids;   // [K_local] global id of local element l (storage order)
+  std::vector<int64_t> g2l;         // [K_global] local index or -1
+  std::vector<PeerPlan> peers;      // ascending peer rank
+  int64_t n_ghost_faces = 0;        // total received faces (= total sent faces)
+  // send list: for send face s (in buffer order) the local element and face
+  std::vector<int64_t> send_elem;   // [n_ghost_faces]
+  std::vector<int8_t> send_face;    // [n_ghost_faces]
+  // for local element l, face f: ghost record index (or -1 if not a cross face)
+  std::vector<int64_t> ghost_of;    // [K_local][4]
+};
+
+// owner: [K] rank per element, or empty -> contiguous ranges.  Returns "" or an error.
+std::string build_partition(const MeshData& m, int rank, int nranks, const int32_t* owner,
+                            Partition& out);
+
+// Gather index of the exterior trace for every local face node (see
+// stage_params.h): k2_local*ES + n2, or ghost_base + g*6*Nfp + j, or -1 (PEC).
+void build_gather_index(const RefElem& ref, const MeshData& m, const Partition& P, int64_t ES,
+                        int64_t ghost_base, std::vector<int32_t>& gidx);
+
+}  // namespace dg

@@ -1,0 +1,88 @@
+// Layout conversion between the C-ABI field layout [6][K][Np] (component-major,
+// HW's Np x K per component) and the device element-tile layout [K][ES]
+// (element-major, see stage_params.h).  Not on the timed device path; they run
+// inside dg_fields_upload/download and dg_rhs.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace dg {
+
+template <typename S, typename T>
+__global__ void k_cm_to_tiles(const S* __restrict__ src, T* __restrict__ dst, int64_t K, int Np, int64_t ES) {
+  const int64_t total = K * ES;
+  for (int64_t w = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; w < total; w += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t k = w / ES;
+    const int r = int(w - k * ES);
+    T v = T(0);
+    if (r < 6 * Np) {
+      const int c = r / Np, n = r - c * Np;
+      v = T(src[(int64_t(c) * K + k) * Np + n]);
+    }
+    dst[w] = v;
+  }
+}
+
+template <typename T, typename D>
+__global__ void k_tiles_to_cm(const T* __restrict__ src, D* __restrict__ dst, int64_t K, int Np, int64_t ES) {
+  const int64_t total = 6 * K * Np;
+  for (int64_t w = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; w < total; w += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t c = w / (K * Np);
+    const int64_t rem = w - c * K * Np;
+    const int64_t k = rem / Np;
+    const int n = int(rem - k * Np);
+    dst[w] = D(src[k * ES + c * Np + n]);
+  }
+}
+
+static unsigned grid_for(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  if (g > 148 * 64) g = 148 * 64;
+  if (g < 1) g = 1;
+  return unsigned(g);
+}
+
+template <typename S, typename T>
+void cm_to_tiles(const S* src, T* dst, int64_t K, int Np, int64_t ES, void* st) {
+  k_cm_to_tiles<S, T><<<grid_for(K * ES), 256, 0, static_cast<cudaStream_t>(st)>>>(src, dst, K, Np, ES);
+}
+
+template <typename T, typename D>
+void tiles_to_cm(const T* src, D* dst, int64_t K, int Np, int64_t ES, void* st) {
+  k_tiles_to_cm<T, D><<<grid_for(6 * K * Np), 256, 0, static_cast<cudaStream_t>(st)>>>(src, dst, K, Np, ES);
+}
+
+template void cm_to_tiles<double, double>(const double*, double*, int64_t, int, int64_t, void*);
+template void cm_to_tiles<double, float>(const double*, float*, int64_t, int, int64_t, void*);
+template void cm_to_tiles<float, float>(const float*, float*, int64_t, int, int64_t, void*);
+template void tiles_to_cm<double, double>(const double*, double*, int64_t, int, int64_t, void*);
+template void tiles_to_cm<float, double>(const float*, double*, int64_t, int, int64_t, void*);
+template void tiles_to_cm<float, float>(const float*, float*, int64_t, int, int64_t, void*);
+
+}  // namespace dg
+
+namespace dg {
+
+// Pack the partition-face traces (a6): for send face g, component c, face node j:
+// buf[g][c][j] = u[sidx[g][j] + c*Np]  (sender's own face-node order).
+template <typename T>
+__global__ void k_pack_traces(const T* __restrict__ u, T* __restrict__ buf, const int32_t* __restrict__ sidx,
+                              int64_t nfaces, int Np, int Nfp) {
+  const int64_t total = nfaces * 6 * Nfp;
+  for (int64_t w = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; w < total; w += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t g = w / (6 * Nfp);
+    const int r = int(w - g * 6 * Nfp);
+    const int c = r / Nfp, j = r - c * Nfp;
+    buf[w] = u[sidx[g * Nfp + j] + int64_t(c) * Np];
+  }
+}
+
+template <typename T>
+void pack_traces(const T* u, T* buf, const int32_t* sidx, int64_t nfaces, int Np, int Nfp, void* st) {
+  k_pack_traces<T><<<grid_for(nfaces * 6 * Nfp), 256, 0, static_cast<cudaStream_t>(st)>>>(u, buf, sidx, nfaces,
+                                                                                          Np, Nfp);
+}
+template void pack_traces<double>(const double*, double*, const int32_t*, int64_t, int, int, void*);
+template void pack_traces<float>(const float*, float*, const int32_t*, int64_t, int, int, void*);
+
+}  // namespace dg

@@ -1,0 +1,16 @@
+// Stage-kernel instantiations for order N=5 (see stage_basic.cuh).
+#include "stage_basic.cuh"
+
+namespace dg {
+
+void launch_stage_f64_N5(const StageParams<double>& p, int mode, int variant, void* st) {
+  (void)variant;
+  launch_stage_basic<double, 5>(p, mode, static_cast<cudaStream_t>(st));
+}
+
+void launch_stage_f32_N5(const StageParams<float>& p, int mode, int variant, void* st) {
+  (void)variant;
+  launch_stage_basic<float, 5>(p, mode, static_cast<cudaStream_t>(st));
+}
+
+}  // namespace dg

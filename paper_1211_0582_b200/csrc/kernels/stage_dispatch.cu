@@ -1,0 +1,26 @@
+// Order dispatch for the stage kernels.
+#include "stage_params.h"
+
+namespace dg {
+
+#define DG_DECL(n)                                                                  \
+  void launch_stage_f64_N##n(const StageParams<double>&, int, int, void*);          \
+  void launch_stage_f32_N##n(const StageParams<float>&, int, int, void*);
+DG_DECL(1) DG_DECL(2) DG_DECL(3) DG_DECL(4) DG_DECL(5) DG_DECL(6) DG_DECL(7) DG_DECL(8) DG_DECL(9)
+#undef DG_DECL
+
+StageLauncher<double> stage_launcher_f64(int N) {
+  static const StageLauncher<double> t[9] = {
+      launch_stage_f64_N1, launch_stage_f64_N2, launch_stage_f64_N3, launch_stage_f64_N4, launch_stage_f64_N5,
+      launch_stage_f64_N6, launch_stage_f64_N7, launch_stage_f64_N8, launch_stage_f64_N9};
+  return (N >= 1 && N <= 9) ? t[N - 1] : nullptr;
+}
+
+StageLauncher<float> stage_launcher_f32(int N) {
+  static const StageLauncher<float> t[9] = {
+      launch_stage_f32_N1, launch_stage_f32_N2, launch_stage_f32_N3, launch_stage_f32_N4, launch_stage_f32_N5,
+      launch_stage_f32_N6, launch_stage_f32_N7, launch_stage_f32_N8, launch_stage_f32_N9};
+  return (N >= 1 && N <= 9) ? t[N - 1] : nullptr;
+}
+
+}  // namespace dg

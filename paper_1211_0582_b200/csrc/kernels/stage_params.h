@@ -1,0 +1,48 @@
+// Parameters shared by the host launcher and the stage kernels.
+//
+// Device data layout:
+//   u, res      [Kl + ghosts][ES] words; element k's component c, node n at
+//               k*ES + c*Np + n (ES = 6*Np, rounded up to 4 words for FP32 so every
+//               element tile is 16-B aligned: the microblock idea of PAPER.md:745-765)
+//   ghost traces (multi-GPU) follow the local tiles: ghost face g, component c,
+//               face node i at ghost_base + g*6*Nfp + c*Nfp + i
+//   gidx        int32 [Kl][4*Nfp]: offset of the exterior trace u+ of face node m
+//               (component 0); component stride Np for element nodes, Nfp for ghost
+//               traces (offset >= ghost_base); -1 on a PEC boundary face
+//   geo         [Kl][GEO_W]: rx ry rz sx sy sz tx ty tz, then 4 x (nx ny nz Fscale)
+//   ops         Dr | Ds | Dt ([Np][Np] each, row-major) | LIFT ([Np][4Nfp])
+//   fmask       int16 [4*Nfp]
+#pragma once
+#include <cstdint>
+
+namespace dg {
+
+constexpr int GEO_W = 25;
+
+template <typename T>
+struct StageParams {
+  const T* u_in;       // current stage fields
+  T* u_out;            // LSERK: next stage fields (ping-pong); RHS mode: unused
+  T* res;              // LSERK residual (in place)
+  T* rhs_out;          // RHS mode: d_t u in device layout
+  const T* geo;
+  const int32_t* gidx;
+  const T* ops;
+  const int16_t* fmask;
+  int64_t K;           // number of elements processed by this launch
+  int64_t k_begin;     // first element (launches may cover a sub-range)
+  int64_t ES;          // element stride (words)
+  int64_t ghost_base;  // offset of the ghost-trace region
+  T rk_a, rk_b, dt, alpha;
+  int first_stage;     // 1: a_s == 0, do not read res
+};
+
+// Launchers, one per (order, precision), defined in stage_N*.cu.
+// mode 0: RHS only (writes rhs_out); mode 1: fused lift + LSERK update.
+template <typename T>
+using StageLauncher = void (*)(const StageParams<T>&, int mode, int variant, void* stream);
+
+StageLauncher<double> stage_launcher_f64(int N);
+StageLauncher<float> stage_launcher_f32(int N);
+
+}  // namespace dg

@@ -1,0 +1,156 @@
+"""C-ABI tests that need no GPU: the library loads, exports every symbol the
+header declares, validates arguments, and its host setup (reference element,
+maps, geometry, partition) matches the oracle.  Compute calls on a host-only
+solver must fail with DG_ERR_STATE (no CPU fallback)."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import dg_inputs as di
+import oracle
+from paper_1211_0582_b200 import dg
+from paper_1211_0582_b200.dg import Solver, DGError
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "dg.h")).read()
+    return sorted(set(re.findall(r"^DG_API [^(]*?\b(dg_\w+)\s*\(", src, flags=re.M)))
+
+
+def test_header_symbols_exported_and_bound():
+    declared = _declared_symbols()
+    assert len(declared) >= 20
+    out = subprocess.run(["nm", "-D", "--defined-only", dg.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (dg_\w+)", out))
+    assert set(declared) <= exported, set(declared) - exported
+    assert set(declared) == set(dg.EXPORTED)
+
+
+def test_version_string():
+    v = dg.dg_version().decode()
+    assert "sm_100a" in v and "abi 1" in v
+
+
+def test_argument_errors():
+    with pytest.raises(DGError) as e:
+        Solver(0, device=-1)
+    assert e.value.status == dg.DG_ERR_ORDER
+    with pytest.raises(DGError) as e:
+        Solver(10, device=-1)
+    assert e.value.status == dg.DG_ERR_ORDER
+    with pytest.raises(DGError) as e:
+        Solver(3, precision=2, device=-1)
+    assert e.value.status == dg.DG_ERR_ARG
+    with pytest.raises(DGError) as e:
+        Solver(3, device=-1, rank=2, nranks=2)
+    assert e.value.status == dg.DG_ERR_ARG
+
+
+def test_host_only_solver_refuses_compute():
+    VX, E = di.kuhn_box(1)
+    s = Solver(2, device=-1)
+    s.mesh_upload(VX, E)
+    with pytest.raises(DGError) as e:
+        s.fields_upload(np.zeros((6, s.K_local, s.Np)))
+    assert e.value.status == dg.DG_ERR_STATE
+    with pytest.raises(DGError) as e:
+        s.lserk_step(1e-3, 1)
+    assert e.value.status == dg.DG_ERR_STATE
+
+
+def test_call_order_state_errors():
+    s = Solver(2, device=-1)
+    with pytest.raises(DGError) as e:
+        s.get_maps()
+    assert e.value.status == dg.DG_ERR_STATE
+
+
+def test_mesh_errors():
+    VX, E = di.kuhn_box(1)
+    s = Solver(1, device=-1)
+    bad = E.copy()
+    bad[0, [2, 3]] = bad[0, [3, 2]]
+    with pytest.raises(DGError) as e:
+        s.mesh_upload(VX, bad)
+    assert e.value.status == dg.DG_ERR_MESH and "Jacobian" in str(e.value)
+    bad = E.copy()
+    bad[0, 0] = 10 ** 6
+    with pytest.raises(DGError) as e:
+        s.mesh_upload(VX, bad)
+    assert e.value.status == dg.DG_ERR_MESH
+    VX3 = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [0, 0, -1], [1, 1, 1]], float)
+    E3 = np.array([[0, 1, 2, 3], [0, 2, 1, 4], [0, 1, 2, 5]])
+    a, b, c, d = VX3[E3[2]]
+    if np.dot(b - a, np.cross(c - a, d - a)) < 0:
+        E3[2, [2, 3]] = E3[2, [3, 2]]
+    with pytest.raises(DGError) as e:
+        s.mesh_upload(VX3, E3)
+    assert e.value.status == dg.DG_ERR_MESH and "more than two" in str(e.value)
+
+
+@pytest.mark.parametrize("N", range(1, 10))
+def test_reference_operators_match_oracle(N):
+    # independent routes (oracle: Dubiner/Vandermonde; library: homogeneous PKD +
+    # quadrature) must agree; tolerance 1e-12 relative to the operator's size
+    s = Solver(N, device=-1)
+    R = s.get_reference()
+    O = oracle.build_reference(N)
+    for a, b in ((R["r"], O.r), (R["s"], O.s), (R["t"], O.t)):
+        assert np.abs(a - b).max() < 1e-14
+    for key, ref in (("Dr", O.Dr), ("Ds", O.Ds), ("Dt", O.Dt), ("M", O.M), ("LIFT", O.LIFT)):
+        err = np.abs(R[key] - ref).max() / np.abs(ref).max()
+        assert err < 1e-12, (key, err)
+    assert (R["Fmask"] == O.Fmask).all()
+
+
+MESHES = [
+    ("kuhn2", 2, None, None, None),
+    ("kuhn3-shuf-rot-jit", 3, 1, 2, 3),
+    ("kuhn2-shuf-rot", 2, 5, 6, None),
+]
+
+
+@pytest.mark.parametrize("N", [1, 3, 6, 9])
+@pytest.mark.parametrize("name,n,sh,rot,jit", MESHES, ids=[m[0] for m in MESHES])
+def test_maps_bit_exact_and_geometry(N, name, n, sh, rot, jit):
+    VX, E = di.kuhn_box(n)
+    if sh is not None:
+        E, _ = di.shuffle_elements(E, sh)
+    if rot is not None:
+        E = di.rotate_local_vertices(E, rot)
+    if jit is not None:
+        VX = di.jitter_interior(VX, n, jit)
+    s = Solver(N, device=-1)
+    s.mesh_upload(VX, E)
+    st = oracle.Setup(VX, E, N)
+    EToE, EToF, vM, vP = s.get_maps()
+    assert (EToE == st.EToE).all() and (EToF == st.EToF).all()
+    assert (vM == st.vmapM).all() and (vP == st.vmapP).all()      # bit-exact
+    J, G, nrm = s.get_geometry()
+    assert np.abs(J - st.J).max() <= 1e-15 * np.abs(st.J).max()
+    for i, a in enumerate((st.rx, st.ry, st.rz, st.sx, st.sy, st.sz, st.tx, st.ty, st.tz)):
+        assert np.abs(G[:, i] - a).max() <= 1e-14 * np.abs(a).max() + 1e-15
+    for i, a in enumerate((st.nx, st.ny, st.nz, st.Fscale)):
+        assert np.abs(nrm[:, :, i] - a).max() <= 1e-14 * max(1.0, np.abs(a).max())
+    x, y, z = s.get_nodes()
+    assert np.abs(x - st.x).max() < 1e-14 and np.abs(z - st.z).max() < 1e-14
+
+
+def test_partition_local_order_and_ids():
+    VX, E = di.kuhn_box(2)
+    K = E.shape[0]
+    seen = []
+    for r in range(2):
+        s = Solver(2, device=-1, rank=r, nranks=2)
+        s.mesh_upload(VX, E)
+        ids = s.local_elements()
+        seen.append(ids)
+        assert s.K_local == len(ids)
+        # contiguous default owner: k*P//K
+        assert set(ids.tolist()) == {k for k in range(K) if (k * 2) // K == r}
+    assert sorted(np.concatenate(seen).tolist()) == list(range(K))

@@ -1,0 +1,217 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle,
+element by element, on identical seeded inputs.
+
+Tolerances (DESIGN.md §"Tolerances"):
+  * FP64: max|gpu - oracle| / max|oracle| <= 1e-12 (north_star), for a single RHS
+    and after a fixed number of LSERK4 steps;
+  * FP32: <= 1e-4 after the steps (north_star); a single FP32 RHS <= 2e-5
+    (single-precision rounding of Np-term dot products, ~Np * 6e-8, plus the
+    rounded geometry/operators);
+  * maps and connectivity: bit-exact (tests/test_abi.py).
+"""
+import numpy as np
+import pytest
+
+import dg_inputs as di
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1211_0582_b200.dg import Solver  # noqa: E402
+
+TOL_RHS = {8: 1e-12, 4: 2e-5}
+TOL_STEP = {8: 1e-12, 4: 1e-4}
+
+
+def relerr(a, b):
+    return float(np.abs(a - b).max() / np.abs(b).max())
+
+
+def mesh(n, sh=None, rot=None, jit=None):
+    VX, E = di.kuhn_box(n)
+    if sh is not None:
+        E, _ = di.shuffle_elements(E, sh)
+    if rot is not None:
+        E = di.rotate_local_vertices(E, rot)
+    if jit is not None:
+        VX = di.jitter_interior(VX, n, jit)
+    return VX, E
+
+
+_SETUPS = {}
+
+
+def setup(key, VX, E, N):
+    k = (key, N)
+    if k not in _SETUPS:
+        _SETUPS[k] = oracle.Setup(VX, E, N)
+    return _SETUPS[k]
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+@pytest.mark.parametrize("N", range(1, 10))
+def test_rhs_random_fields_shuffled_jittered(N, prec):
+    VX, E = mesh(3, 1, 2, 3)                      # K = 162: ragged tail for every tile size
+    st = setup("m3", VX, E, N)
+    U = di.random_fields(st.K, N, seed=0)
+    s = Solver(N, precision=prec)
+    s.mesh_upload(VX, E)
+    s.fields_upload(U)
+    R = s.rhs()
+    Ro = oracle.rhs(st, U)
+    assert relerr(R, Ro) < TOL_RHS[prec]
+    # fields round-trip (FP32: exact widening of the rounded upload)
+    back = s.fields_download()
+    if prec == 8:
+        assert np.array_equal(back, U)
+    else:
+        assert np.array_equal(back, U.astype(np.float32).astype(np.float64))
+    s.close()
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+def test_c1_cavity_100_steps(prec):
+    # config C1: unit cube, 2x2x2 cubes x 6 tets, N=3, 100 LSERK4 steps
+    N = 3
+    VX, E = di.kuhn_box(2)
+    st = setup("c1", VX, E, N)
+    U0 = di.cavity_mode_101(st.x, st.y, st.z)
+    dt = di.dt_rule(VX, E, N)
+    s = Solver(N, precision=prec)
+    s.mesh_upload(VX, E)
+    x, y, z = s.get_nodes()
+    s.fields_upload(di.cavity_mode_101(x, y, z))
+    s.lserk_step(dt, 100)
+    U = s.fields_download()
+    Uo = oracle.lserk4(st, U0, dt, 100)
+    assert relerr(U, Uo) < TOL_STEP[prec]
+    s.close()
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+@pytest.mark.parametrize("N", range(1, 10))
+def test_lserk_steps_all_orders(N, prec):
+    VX, E = mesh(2, 5, 6, 7)
+    st = setup("m2", VX, E, N)
+    U0 = di.random_fields(st.K, N, seed=1)
+    dt = di.dt_rule(VX, E, N)
+    s = Solver(N, precision=prec)
+    s.mesh_upload(VX, E)
+    s.fields_upload(U0)
+    # split the steps across calls: exercises both graph parities and re-use
+    s.lserk_step(dt, 3)
+    s.lserk_step(dt, 4)
+    U = s.fields_download()
+    Uo = oracle.lserk4(st, U0, dt, 7)
+    assert relerr(U, Uo) < TOL_STEP[prec]
+    s.close()
+
+
+def test_single_element_all_pec():
+    VX = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]], float)
+    E = np.array([[0, 1, 2, 3]])
+    for N in (1, 5, 9):
+        st = oracle.Setup(VX, E, N)
+        U = di.random_fields(1, N, seed=4)
+        s = Solver(N)
+        s.mesh_upload(VX, E)
+        s.fields_upload(U)
+        assert relerr(s.rhs(), oracle.rhs(st, U)) < 1e-12
+        s.close()
+
+
+def test_zero_fields_zero_rhs_and_dt_zero_identity():
+    VX, E = di.kuhn_box(2)
+    s = Solver(4)
+    s.mesh_upload(VX, E)
+    s.fields_upload(np.zeros((6, s.K_local, s.Np)))
+    assert np.all(s.rhs() == 0)
+    U = di.random_fields(s.K_local, 4, seed=2)
+    s.fields_upload(U)
+    s.lserk_step(0.0, 3)
+    assert np.array_equal(s.fields_download(), U)
+    s.close()
+
+
+def test_central_flux_alpha0():
+    N = 3
+    VX, E = mesh(2, 3, 4, 5)
+    st = oracle.Setup(VX, E, N)
+    U = di.random_fields(st.K, N, seed=3)
+    s = Solver(N, alpha=0.0)
+    s.mesh_upload(VX, E)
+    s.fields_upload(U)
+    assert relerr(s.rhs(), oracle.rhs(st, U, alpha=0.0)) < 1e-12
+    s.close()
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+@pytest.mark.parametrize("N", [1, 4, 9])
+def test_bench_mesh_full_size(N, prec):
+    # the bench workload (config C2: Kuhn n=15, K=20250), full-size comparison
+    # of one RHS and one graph-launched LSERK4 step
+    VX, E = di.kuhn_box(15)
+    st = setup("c2", VX, E, N)
+    U0 = di.random_fields(st.K, N, seed=0)
+    s = Solver(N, precision=prec)
+    s.mesh_upload(VX, E)
+    s.fields_upload(U0)
+    assert relerr(s.rhs(), oracle.rhs(st, U0)) < TOL_RHS[prec]
+    dt = di.dt_rule(VX, E, N)
+    s.lserk_step(dt, 1)
+    assert relerr(s.fields_download(), oracle.lserk4(st, U0, dt, 1)) < TOL_STEP[prec]
+    s.close()
+
+
+def _submesh(VX, E, EToE, seeds, layers):
+    keep = set(int(k) for k in seeds)
+    front = set(keep)
+    for _ in range(layers):
+        nxt = set()
+        for k in front:
+            nxt.update(int(v) for v in EToE[k])
+        front = nxt - keep
+        keep |= nxt
+    keep = np.array(sorted(keep))
+    verts = np.unique(E[keep])
+    remap = -np.ones(VX.shape[0], dtype=np.int64)
+    remap[verts] = np.arange(len(verts))
+    return keep, VX[verts], remap[E[keep]]
+
+
+def test_sampled_oracle_at_c4_size():
+    # config C4's mesh (Kuhn n=56, K=1,053,696, N=4, FP64) in the bench launch
+    # configuration.  The oracle cannot run the whole mesh; it recomputes sampled
+    # elements exactly on a sub-mesh of their face neighbourhood: 1 layer for one
+    # RHS, 6 layers for one LSERK4 step (5 stages; the artificial boundary of the
+    # sub-mesh cannot reach the centre).
+    N, n = 4, 56
+    VX, E = di.kuhn_box(n)
+    K = E.shape[0]
+    s = Solver(N)
+    s.mesh_upload(VX, E)
+    EToE, _, _, _ = s.get_maps()
+    U0 = di.random_fields(K, N, seed=9)
+    s.fields_upload(U0)
+    R = s.rhs()
+    rng = np.random.default_rng(0)
+    samples = np.concatenate([[0, K - 1], rng.integers(0, K, 6)])
+    keep, sVX, sE = _submesh(VX, E, EToE, samples, 1)
+    st = oracle.Setup(sVX, sE, N)
+    Rs = oracle.rhs(st, U0[:, keep])
+    pos = np.searchsorted(keep, samples)
+    assert relerr(R[:, samples], Rs[:, pos]) < 1e-12
+    dt = di.dt_rule(VX, E, N)
+    s.lserk_step(dt, 1)
+    U1 = s.fields_download()
+    for k in samples[:3]:
+        keep, sVX, sE = _submesh(VX, E, EToE, [k], 6)
+        st = oracle.Setup(sVX, sE, N)
+        Us = oracle.lserk4(st, U0[:, keep], dt, 1)
+        p = np.searchsorted(keep, k)
+        assert relerr(U1[:, k], Us[:, p]) < 1e-12
+    s.close()
