@@ -99,6 +99,7 @@ struct dg_solver {
   void* d_geo = nullptr;
   int32_t* d_gidx = nullptr;
   void* d_ops = nullptr;
+  void* d_ops_pad = nullptr;   // FP64 MMA variant operators, zero-padded
   int16_t* d_fmask = nullptr;
   void* d_send = nullptr;      // [n_ghost][6][Nfp]
   int32_t* d_sidx = nullptr;   // [n_ghost][Nfp] element-node offsets for packing
@@ -141,6 +142,7 @@ void release_device(dg_solver* s) {
   free_dev(s->d_geo);
   p = s->d_gidx; free_dev(p); s->d_gidx = nullptr;
   free_dev(s->d_ops);
+  free_dev(s->d_ops_pad);
   p = s->d_fmask; free_dev(p); s->d_fmask = nullptr;
   free_dev(s->d_send);
   p = s->d_sidx; free_dev(p); s->d_sidx = nullptr;
@@ -160,6 +162,7 @@ dg::StageParams<T> base_params(dg_solver* s) {
   p.geo = static_cast<const T*>(s->d_geo);
   p.gidx = s->d_gidx;
   p.ops = static_cast<const T*>(s->d_ops);
+  p.ops_pad = static_cast<const T*>(s->d_ops_pad);
   p.fmask = s->d_fmask;
   p.ES = s->ES;
   p.ghost_base = s->ghost_base;
@@ -297,6 +300,19 @@ dg_status upload_setup(dg_solver* s) {
     for (int j = 0; j < NF; ++j) ops[size_t(3) * Np * Np + size_t(i) * NF + j] = T(s->ref.LIFT(i, j));
   CK(cudaMalloc(&s->d_ops, ops.size() * wb));
   CK(cudaMemcpy(s->d_ops, ops.data(), ops.size() * wb, cudaMemcpyHostToDevice));
+  if (sizeof(T) == 8) {
+    // [3][M8][KV] + [M8][NF], zero padding (stage_mma.cuh)
+    const int M8 = (Np + 7) / 8 * 8, KV = (Np + 3) / 4 * 4;
+    std::vector<T> pad(size_t(3) * M8 * KV + size_t(M8) * NF, T(0));
+    const dg::Mat* D[3] = {&s->ref.Dr, &s->ref.Ds, &s->ref.Dt};
+    for (int b = 0; b < 3; ++b)
+      for (int i = 0; i < Np; ++i)
+        for (int j = 0; j < Np; ++j) pad[(size_t(b) * M8 + i) * KV + j] = T((*D[b])(i, j));
+    for (int i = 0; i < Np; ++i)
+      for (int j = 0; j < NF; ++j) pad[size_t(3) * M8 * KV + size_t(i) * NF + j] = T(s->ref.LIFT(i, j));
+    CK(cudaMalloc(&s->d_ops_pad, pad.size() * wb));
+    CK(cudaMemcpy(s->d_ops_pad, pad.data(), pad.size() * wb, cudaMemcpyHostToDevice));
+  }
   std::vector<int16_t> fm(NF);
   for (int i = 0; i < NF; ++i) fm[i] = int16_t(s->ref.Fmask[i]);
   CK(cudaMalloc((void**)&s->d_fmask, NF * sizeof(int16_t)));

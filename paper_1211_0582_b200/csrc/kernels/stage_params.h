@@ -12,6 +12,8 @@
 //   geo         [Kl][GEO_W]: rx ry rz sx sy sz tx ty tz, then 4 x (nx ny nz Fscale)
 //   ops         Dr | Ds | Dt ([Np][Np] each, row-major) | LIFT ([Np][4Nfp])
 //   fmask       int16 [4*Nfp]
+//   ops_pad     (MMA variant) Dr|Ds|Dt zero-padded to [3][M8][KV], LIFT to [M8][4Nfp]
+//               (M8 = Np rounded up to 8, KV = Np rounded up to 4)
 #pragma once
 #include <cstdint>
 
@@ -28,6 +30,7 @@ struct StageParams {
   const T* geo;
   const int32_t* gidx;
   const T* ops;
+  const T* ops_pad;    // MMA variant: Dr|Ds|Dt as [3][M8][KV] + LIFT [M8][4Nfp], zero-padded
   const int16_t* fmask;
   int64_t K;           // number of elements processed by this launch
   int64_t k_begin;     // first element (launches may cover a sub-range)

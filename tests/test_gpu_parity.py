@@ -52,13 +52,16 @@ def setup(key, VX, E, N):
     return _SETUPS[k]
 
 
-@pytest.mark.parametrize("prec", [8, 4])
+VARIANTS = [(8, 1), (8, 2), (4, 1)]   # (precision, variant): FP64 BASIC, FP64 MMA (DMMA), FP32 BASIC
+
+
+@pytest.mark.parametrize("prec,variant", VARIANTS, ids=["f64-basic", "f64-mma", "f32-basic"])
 @pytest.mark.parametrize("N", range(1, 10))
-def test_rhs_random_fields_shuffled_jittered(N, prec):
+def test_rhs_random_fields_shuffled_jittered(N, prec, variant):
     VX, E = mesh(3, 1, 2, 3)                      # K = 162: ragged tail for every tile size
     st = setup("m3", VX, E, N)
     U = di.random_fields(st.K, N, seed=0)
-    s = Solver(N, precision=prec)
+    s = Solver(N, precision=prec, variant=variant)
     s.mesh_upload(VX, E)
     s.fields_upload(U)
     R = s.rhs()
@@ -92,14 +95,14 @@ def test_c1_cavity_100_steps(prec):
     s.close()
 
 
-@pytest.mark.parametrize("prec", [8, 4])
+@pytest.mark.parametrize("prec,variant", VARIANTS, ids=["f64-basic", "f64-mma", "f32-basic"])
 @pytest.mark.parametrize("N", range(1, 10))
-def test_lserk_steps_all_orders(N, prec):
+def test_lserk_steps_all_orders(N, prec, variant):
     VX, E = mesh(2, 5, 6, 7)
     st = setup("m2", VX, E, N)
     U0 = di.random_fields(st.K, N, seed=1)
     dt = di.dt_rule(VX, E, N)
-    s = Solver(N, precision=prec)
+    s = Solver(N, precision=prec, variant=variant)
     s.mesh_upload(VX, E)
     s.fields_upload(U0)
     # split the steps across calls: exercises both graph parities and re-use
