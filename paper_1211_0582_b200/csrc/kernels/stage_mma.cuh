@@ -1,26 +1,38 @@
 // MMA variant (FP64): the two dense contractions of a stage on the FP64 tensor
-// pipe (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4), everything else fused around them.
+// pipe (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4), everything else fused around
+// them, in a persistent, software-pipelined kernel.
 //
-// "View the field vectors in aggregate as a matrix": a CTA owns
-// E elements; its 6E element-component columns are the MMA N dimension.
+// "View the field vectors in aggregate as a matrix": a tile
+// is E elements; its 6E element-component columns are the MMA N dimension.
 //   volume (a1):  Y_b = D_b . U      D_b in {Dr, Ds, Dt}: [M8 x KV],  U: [KV x 6E]
 //   lift   (a4):  R  = curl(Y) + LIFT . Flux                 LIFT: [M8 x NF]
-// A operands (operators, zero-padded to M8 rows / KV cols) are read through L1
-// (__ldg) — they are shared by every CTA; B operands (the element tile U and the
-// face buffer Flux) live in shared memory with a leading dimension = 4 (mod 16)
-// doubles so every fragment load is bank-conflict free.  The face buffer
-// (a2+a3) never leaves the chip; the LSERK update (a5) is applied straight from
-// the lift accumulators.
+// A operands (the reference operators, zero-padded to M8 rows / KV columns) are
+// resident in shared memory for N <= OPS_SMEM_MAX_N (loaded once per CTA, the
+// paper's "matrix in shared memory" strategy) and read through
+// L1 otherwise.  B operands (the element tile U and the face buffer) live in
+// shared memory with leading dimension = 4 (mod 16) doubles: conflict-free
+// fragment loads.
 //
-// Work split: task = (node m-tile t of 8 rows, column group g of 4 elements = 24
-// columns = 3 n-tiles).  A warp computes all three derivative blocks of its task,
-// so the chain rule + curl (eq. 6) need only a per-warp 8x24 scratch exchange.
+// Pipeline per CTA (grid = resident CTAs; tiles strided over the grid):
+//   while computing tile i, cp.async brings tile i+1's U, geometry and gather
+//   indices into the other buffer; after tile i's MMA phase the gathered
+//   exterior traces u+ and the residual of tile i+1 are fetched with cp.async
+//   (a2's irregular gather, made asynchronous).  Every
+//   cp.async group is waited on by its issuing thread and followed by a block
+//   barrier before any other thread reads it.  The face buffer (a2+a3) never leaves the chip; the
+//   LSERK update (a5) is applied straight from the lift accumulators.
+//
+// Work split: task = (node m-tile t of 8 rows, column group g of 4 elements =
+// 24 columns = 3 n-tiles).  A warp computes all three derivative blocks of its
+// task, so the chain rule + curl (eq. 6) need only a per-warp scratch exchange.
 #pragma once
 #include <cuda_runtime.h>
 
 #include "stage_basic.cuh"
 
 namespace dg {
+
+constexpr int OPS_SMEM_MAX_N = 0;  // measured: L1-served operators + 2 CTAs/SM beat smem-resident + 1 CTA/SM
 
 template <int N>
 struct MmaCfg {
@@ -29,22 +41,35 @@ struct MmaCfg {
   static constexpr int MT = M8 / 8;
   static constexpr int KV = (Np + 3) / 4 * 4;
   static constexpr int KL = NF;  // multiple of 4 for every N
-  // leading dimensions = 4 (mod 16) doubles: conflict-free 8x4 fragment loads
   static constexpr int ld4(int x) { return x + ((4 - x % 16) + 16) % 16; }
   static constexpr int LDU = ld4(KV);
   static constexpr int LDF = ld4(KL);
-  // elements per CTA (multiple of 4) and warps per CTA, chosen per order so that
-  // MT * (E/4) tasks split evenly over the warps
-  static constexpr int E = N <= 1 ? 32 : N <= 2 ? 16 : N <= 3 ? 16 : N <= 6 ? 8 : 4;
+  static constexpr int LDA = ld4(KV);  // smem-resident operators
+  static constexpr int LDL = ld4(KL);
+  static constexpr bool OPS_SMEM = N <= OPS_SMEM_MAX_N;
+  // elements per tile (multiple of 4) and warps per CTA: MT*(E/4)
+  // tasks split evenly over the warps
+  static constexpr int E = N <= 1 ? 32 : N <= 3 ? 16 : N <= 6 ? 8 : 4;
   static constexpr int G = E / 4;
   static constexpr int TASKS = MT * G;
-  static constexpr int NW = N <= 2 ? 8 : N == 3 ? 4 : N == 4 ? 5 : N == 5 ? 7 : N == 6 ? 11 : N == 7 ? 5 : 7;
+  static constexpr int NW = N == 1 ? 8 : N == 2 ? 8 : N == 3 ? 6 : N == 4 ? 5 : N == 5 ? 7 : N == 6 ? 11 : N == 7 ? 5 : 7;
   static constexpr int NT = NW * 32;
   static constexpr int COLS = 6 * E;
-  static constexpr int SCR = 3 * 8 * 24;  // per-warp derivative scratch
-  static constexpr size_t SMEM_DOUBLES = size_t(COLS) * LDU + size_t(COLS) * LDF + size_t(E) * GEO_W + size_t(NW) * SCR;
-  static constexpr size_t SMEM_BYTES = SMEM_DOUBLES * 8 + NF * 2 + 16;
-  // padded operator buffer: Dr|Ds|Dt as [3][M8][KV], then LIFT as [M8][KL]
+  static constexpr int SCR = 3 * 24 * 10;  // per-warp derivative scratch [d][col][row], stride 10: <= 2-way conflicts
+  // shared memory carve-up (doubles)
+  static constexpr int U_SZ = COLS * LDU;
+  static constexpr int GEO_SZ = E * GEO_W + (E * GEO_W) % 2;
+  static constexpr int TR_SZ = 6 * E * NF;  // gathered u+ traces [e][c][m]
+  static constexpr int SCRATCH_SZ = (TR_SZ > NW * SCR ? TR_SZ : NW * SCR);  // traces and scratch share
+  static constexpr int GIDX_SZ = (E * NF + 1) / 2;                          // int32 -> doubles
+  static constexpr int F_SZ = COLS * LDF;
+  static constexpr int OPS_SZ = OPS_SMEM ? 3 * M8 * LDA + M8 * LDL : 0;
+  static constexpr int FM_SZ = (NF + 3) / 4;                                // int16 -> doubles
+  static constexpr size_t SMEM_DOUBLES =
+      size_t(2) * U_SZ + 2 * GEO_SZ + U_SZ /*res*/ + SCRATCH_SZ + 2 * GIDX_SZ + F_SZ + OPS_SZ + FM_SZ;
+  static constexpr size_t SMEM_BYTES = SMEM_DOUBLES * 8;
+  static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+  // padded operator buffer in global memory: Dr|Ds|Dt as [3][M8][KV], then LIFT [M8][KL]
   static constexpr size_t OPS_DOUBLES = size_t(3) * M8 * KV + size_t(M8) * KL;
 };
 
@@ -54,184 +79,324 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem_src));
+}
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gmem_src) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem_src));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int n>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(n)); }
+
 template <int N, bool UPDATE>
-__global__ void __launch_bounds__(MmaCfg<N>::NT) dg_stage_mma(const StageParams<double> p, const double* __restrict__ opsA) {
+__global__ void __launch_bounds__(MmaCfg<N>::NT, 1)
+    dg_stage_mma(const StageParams<double> p, const double* __restrict__ opsA) {
   using C = MmaCfg<N>;
   constexpr int Np = C::Np, Nfp = C::Nfp, NF = C::NF, M8 = C::M8, KV = C::KV, KL = C::KL;
   constexpr int E = C::E, LDU = C::LDU, LDF = C::LDF, NT = C::NT;
   extern __shared__ __align__(16) double smem[];
-  double* sU = smem;                       // [6E][LDU]  element-component columns
-  double* sF = sU + C::COLS * LDU;         // [6E][LDF]  face buffer (flux x Fscale/2)
-  double* sG = sF + C::COLS * LDF;         // [E][GEO_W]
-  double* sS = sG + E * GEO_W;             // [NW][3][8][24]
-  int16_t* sFm = reinterpret_cast<int16_t*>(sS + C::NW * C::SCR);
+  double* sU0 = smem;
+  double* sU1 = sU0 + C::U_SZ;
+  double* sG0 = sU1 + C::U_SZ;
+  double* sG1 = sG0 + C::GEO_SZ;
+  double* sR = sG1 + C::GEO_SZ;                 // residual of the current tile [6E][LDU]
+  double* sT = sR + C::U_SZ;                    // gathered traces [e][c][m]  (aliases the curl scratch)
+  int32_t* sI0 = reinterpret_cast<int32_t*>(sT + C::SCRATCH_SZ);  // gather indices [e][m] (x2)
+  int32_t* sI1 = reinterpret_cast<int32_t*>(sT + C::SCRATCH_SZ + C::GIDX_SZ);
+  double* sF = sT + C::SCRATCH_SZ + 2 * C::GIDX_SZ;  // face buffer [6E][LDF]
+  double* sA = sF + C::F_SZ;                    // operators (N <= OPS_SMEM_MAX_N)
+  int16_t* sFm = reinterpret_cast<int16_t*>(sA + C::OPS_SZ);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gid = lane >> 2, tig = lane & 3;
-  const int64_t k0 = p.k_begin + int64_t(blockIdx.x) * E;
-  const int64_t kend = p.k_begin + p.K;
-  const int ne = int(kend - k0 < E ? kend - k0 : E);
   const int64_t ES = p.ES;  // = 6 Np for FP64
+  const int64_t ntiles = (p.K + E - 1) / E;
 
-  // ---- stage the element tile (coalesced: the E tiles are one contiguous chunk)
-  const double* ug = p.u_in + k0 * ES;
-  for (int w = tid; w < E * 6 * Np; w += NT) {
-    const int col = w / Np, n = w - col * Np;
-    sU[col * LDU + n] = (col < ne * 6) ? ug[w] : 0.0;
+  // ---- one-time: operators and Fmask into shared memory
+  for (int m = tid; m < NF; m += NT) sFm[m] = p.fmask[m];
+  if constexpr (C::OPS_SMEM) {
+    for (int w = tid; w < 3 * M8 * KV; w += NT) {
+      const int r = w / KV, k = w - r * KV;
+      sA[r * C::LDA + k] = opsA[w];
+    }
+    const double* Lg = opsA + 3 * M8 * KV;
+    for (int w = tid; w < M8 * KL; w += NT) {
+      const int r = w / KL, k = w - r * KL;
+      sA[3 * M8 * C::LDA + r * C::LDL + k] = Lg[w];
+    }
   }
+
+  auto tile_count = [&](int64_t tile) -> int {
+    const int64_t k0 = p.k_begin + tile * E, kend = p.k_begin + p.K;
+    return int(kend - k0 < E ? kend - k0 : E);
+  };
+  // issue cp.async for tile's U, geometry, gather indices (zero-fill the padding / absent elements)
+  auto issue_tile = [&](int64_t tile, double* sU, double* sG, int32_t* sI) {
+    const int64_t k0 = p.k_begin + tile * E;
+    const int ne = tile_count(tile);
+    const double* ug = p.u_in + k0 * ES;
+    for (int w = tid; w < E * 6 * Np; w += NT) {
+      const int col = w / Np, n = w - col * Np;
+      if (col < ne * 6)
+        cp_async8(sU + col * LDU + n, ug + w);
+      else
+        sU[col * LDU + n] = 0.0;
+    }
+    for (int w = tid; w < E * GEO_W; w += NT) {
+      if (w < ne * GEO_W)
+        cp_async8(sG + w, p.geo + k0 * GEO_W + w);
+      else
+        sG[w] = 0.0;
+    }
+    for (int w = tid; w < E * NF; w += NT) {
+      if (w < ne * NF)
+        cp_async4(sI + w, p.gidx + k0 * NF + w);
+      else
+        sI[w] = -1;
+    }
+  };
+  // issue cp.async for the exterior traces u+ of the tile whose indices are in sI.
+  // Each thread handles exactly the index slots it copied itself, so only its own
+  // cp.async groups must have completed (no block barrier needed).
+  auto issue_traces = [&](const int32_t* sI) {
+    for (int w = tid; w < E * NF; w += NT) {
+      const int32_t gi = sI[w];
+      if (gi >= 0) {
+        const int e = w / NF, m = w - e * NF;
+        const int64_t cs = (gi >= p.ghost_base) ? Nfp : Np;
+        const double* src = p.u_in + gi;
+#pragma unroll
+        for (int c = 0; c < 6; ++c) cp_async8(sT + (e * 6 + c) * NF + m, src + c * cs);
+      }
+    }
+  };
+  // residual of a tile into sR (read in the epilogue; issued one tile ahead)
+  auto issue_res = [&](int64_t tl) {
+    if (!UPDATE || p.first_stage) return;
+    const int64_t kk0 = p.k_begin + tl * E;
+    const int nn = tile_count(tl);
+    const double* rg = p.res + kk0 * ES;
+    for (int w = tid; w < nn * 6 * Np; w += NT) {
+      const int col = w / Np, n = w - col * Np;
+      cp_async8(sR + col * LDU + n, rg + w);
+    }
+  };
+  // zero the K padding of both U buffers once (never overwritten by tile loads)
   if constexpr (LDU > Np) {
-    constexpr int PAD = LDU - Np;  // zero the K padding (the A operand is zero there too)
+    constexpr int PAD = LDU - Np;
     for (int w = tid; w < C::COLS * PAD; w += NT) {
       const int col = w / PAD, n = Np + (w - col * PAD);
-      sU[col * LDU + n] = 0.0;
+      sU0[col * LDU + n] = 0.0;
+      sU1[col * LDU + n] = 0.0;
     }
   }
-  for (int w = tid; w < E * GEO_W; w += NT) sG[w] = (w < ne * GEO_W) ? p.geo[k0 * GEO_W + w] : 0.0;
-  for (int m = tid; m < NF; m += NT) sFm[m] = p.fmask[m];
+
+  int64_t tile = blockIdx.x;
+  if (tile < ntiles) {
+    issue_tile(tile, sU0, sG0, sI0);
+    cp_commit();
+    cp_wait<0>();
+    issue_traces(sI0);
+    issue_res(tile);
+    cp_commit();
+  }
   __syncthreads();
 
-  // ---- a2 + a3: traces and upwind/PEC flux into the face buffer
-  for (int w = tid; w < E * NF; w += NT) {
-    const int e = w / NF, m = w - e * NF, f = m / Nfp;
-    double fl[6] = {0, 0, 0, 0, 0, 0};
-    if (e < ne) {
-      const double* g = sG + e * GEO_W + 9 + 4 * f;
-      const double nx = g[0], ny = g[1], nz = g[2], fs = g[3];
-      const int nM = sFm[m];
-      const double* uM = sU + (e * 6) * LDU + nM;
-      const int32_t gi = p.gidx[(k0 + e) * NF + m];
-      double dE[3], dH[3];
-      if (gi >= 0) {
-        const int64_t cs = (gi >= p.ghost_base) ? Nfp : Np;
-        const double* uP = p.u_in + gi;
+  int buf = 0;
+  for (; tile < ntiles; tile += gridDim.x, buf ^= 1) {
+    double* sU = buf ? sU1 : sU0;
+    double* sG = buf ? sG1 : sG0;
+    const int32_t* sI = buf ? sI1 : sI0;
+    const int64_t k0 = p.k_begin + tile * E;
+    const int ne = tile_count(tile);
+    const int64_t next = tile + gridDim.x;
+    // prefetch the next tile's U / geometry / indices into the other buffer
+    if (next < ntiles) issue_tile(next, buf ? sU0 : sU1, buf ? sG0 : sG1, buf ? sI0 : sI1);
+    cp_commit();
+    cp_wait<1>();  // everything but the prefetch group: this tile's traces and residual have landed
+    __syncthreads();
+    // ---- a2 + a3: upwind/PEC flux into the face buffer (all operands in smem)
+    for (int w = tid; w < E * NF; w += NT) {
+      const int e = w / NF, m = w - e * NF, f = m / Nfp;
+      double fl[6] = {0, 0, 0, 0, 0, 0};
+      if (e < ne) {
+        const double* g = sG + e * GEO_W + 9 + 4 * f;
+        const double nx = g[0], ny = g[1], nz = g[2], fs = g[3];
+        const double* uM = sU + (e * 6) * LDU + sFm[m];
+        double dE[3], dH[3];
+        if (sI[w] >= 0) {
+          const double* uP = sT + (e * 6) * NF + m;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          dE[c] = __ldg(uP + c * cs) - uM[c * LDU];
-          dH[c] = __ldg(uP + (c + 3) * cs) - uM[(c + 3) * LDU];
+          for (int c = 0; c < 3; ++c) {
+            dE[c] = uP[c * NF] - uM[c * LDU];
+            dH[c] = uP[(c + 3) * NF] - uM[(c + 3) * LDU];
+          }
+        } else {  // PEC wall: E+ = -E-, H+ = H-
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            dE[c] = -2.0 * uM[c * LDU];
+            dH[c] = 0.0;
+          }
+        }
+        maxwell_flux<double>(nx, ny, nz, p.alpha, dE, dH, fl);
+        const double sc = fs * 0.5;
+#pragma unroll
+        for (int c = 0; c < 6; ++c) fl[c] *= sc;
+      }
+#pragma unroll
+      for (int c = 0; c < 6; ++c) sF[(e * 6 + c) * LDF + m] = fl[c];
+    }
+    __syncthreads();  // face buffer complete; the traces buffer is now free (curl scratch)
+
+    // ---- a1 + curl + a4 + a5 per warp task
+    double* scr = sT + warp * C::SCR;
+    for (int task = warp; task < C::TASKS; task += C::NW) {
+      const int t = task % C::MT, g = task / C::MT;
+      const int row = 8 * t + gid;
+      double acc[3][3][2];
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int nt = 0; nt < 3; ++nt) acc[b][nt][0] = acc[b][nt][1] = 0.0;
+      const double* bp = sU + (24 * g + gid) * LDU + tig;
+      if constexpr (C::OPS_SMEM) {
+        const double* ap = sA + row * C::LDA + tig;
+#pragma unroll
+        for (int kk = 0; kk < KV; kk += 4) {
+          const double ar = ap[kk], as = ap[M8 * C::LDA + kk], at = ap[2 * M8 * C::LDA + kk];
+#pragma unroll
+          for (int nt = 0; nt < 3; ++nt) {
+            const double bv = bp[nt * 8 * LDU + kk];
+            dmma(acc[0][nt], ar, bv);
+            dmma(acc[1][nt], as, bv);
+            dmma(acc[2][nt], at, bv);
+          }
         }
       } else {
+        const double* ap = opsA + size_t(row) * KV + tig;
+#pragma unroll 4
+        for (int kk = 0; kk < KV; kk += 4) {
+          const double ar = __ldg(ap + kk);
+          const double as = __ldg(ap + size_t(M8) * KV + kk);
+          const double at = __ldg(ap + size_t(2) * M8 * KV + kk);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          dE[c] = -2.0 * uM[c * LDU];
-          dH[c] = 0.0;
+          for (int nt = 0; nt < 3; ++nt) {
+            const double bv = bp[nt * 8 * LDU + kk];
+            dmma(acc[0][nt], ar, bv);
+            dmma(acc[1][nt], as, bv);
+            dmma(acc[2][nt], at, bv);
+          }
         }
       }
-      maxwell_flux<double>(nx, ny, nz, p.alpha, dE, dH, fl);
-      const double sc = fs * 0.5;
-#pragma unroll
-      for (int c = 0; c < 6; ++c) fl[c] *= sc;
-    }
-#pragma unroll
-    for (int c = 0; c < 6; ++c) sF[(e * 6 + c) * LDF + m] = fl[c];
-  }
-  __syncthreads();
-
-  // ---- a1 + curl + a4 + a5 per warp task
-  const double* Dall = opsA;
-  const double* Lp = opsA + size_t(3) * M8 * KV;
-  double* scr = sS + warp * C::SCR;
-  for (int task = warp; task < C::TASKS; task += C::NW) {
-    const int t = task % C::MT, g = task / C::MT;
-    const int row = 8 * t + gid;
-    double acc[3][3][2];
-#pragma unroll
-    for (int b = 0; b < 3; ++b)
-#pragma unroll
-      for (int nt = 0; nt < 3; ++nt) acc[b][nt][0] = acc[b][nt][1] = 0.0;
-    const double* a0p = Dall + size_t(row) * KV + tig;
-    const double* bp = sU + (24 * g + gid) * LDU + tig;
-#pragma unroll 4
-    for (int kk = 0; kk < KV; kk += 4) {
-      const double ar = __ldg(a0p + kk);
-      const double as = __ldg(a0p + size_t(M8) * KV + kk);
-      const double at = __ldg(a0p + size_t(2) * M8 * KV + kk);
-#pragma unroll
-      for (int nt = 0; nt < 3; ++nt) {
-        const double bv = bp[nt * 8 * LDU + kk];
-        dmma(acc[0][nt], ar, bv);
-        dmma(acc[1][nt], as, bv);
-        dmma(acc[2][nt], at, bv);
-      }
-    }
-    // chain rule (eq. 6) for this thread's 6 columns -> per-warp scratch
-#pragma unroll
-    for (int nt = 0; nt < 3; ++nt)
-#pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const int lc = 8 * nt + 2 * tig + v;          // column within the group
-        const double* G = sG + (4 * g + lc / 6) * GEO_W;
-        const double ur = acc[0][nt][v], us = acc[1][nt][v], ut = acc[2][nt][v];
-        scr[(0 * 8 + gid) * 24 + lc] = G[0] * ur + G[3] * us + G[6] * ut;  // d/dx
-        scr[(1 * 8 + gid) * 24 + lc] = G[1] * ur + G[4] * us + G[7] * ut;  // d/dy
-        scr[(2 * 8 + gid) * 24 + lc] = G[2] * ur + G[5] * us + G[8] * ut;  // d/dz
-      }
-    __syncwarp();
-    double r[3][2];
-#pragma unroll
-    for (int nt = 0; nt < 3; ++nt)
-#pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const int lc = 8 * nt + 2 * tig + v;
-        const int base = (lc / 6) * 6, c = lc % 6;
-        const double* sx = scr + (0 * 8 + gid) * 24 + base;
-        const double* sy = scr + (1 * 8 + gid) * 24 + base;
-        const double* sz = scr + (2 * 8 + gid) * 24 + base;
-        double val;
-        // d_t E = curl H, d_t H = -curl E   (components: 0..2 E, 3..5 H)
-        switch (c) {
-          case 0: val = sy[5] - sz[4]; break;
-          case 1: val = sz[3] - sx[5]; break;
-          case 2: val = sx[4] - sy[3]; break;
-          case 3: val = -(sy[2] - sz[1]); break;
-          case 4: val = -(sz[0] - sx[2]); break;
-          default: val = -(sx[1] - sy[0]); break;
-        }
-        r[nt][v] = val;
-      }
-    __syncwarp();
-    // lift: r += LIFT . Flux
-    const double* lp = Lp + size_t(row) * KL + tig;
-    const double* fp = sF + (24 * g + gid) * LDF + tig;
-#pragma unroll 4
-    for (int kk = 0; kk < KL; kk += 4) {
-      const double a = __ldg(lp + kk);
-#pragma unroll
-      for (int nt = 0; nt < 3; ++nt) dmma(r[nt], a, fp[nt * 8 * LDF + kk]);
-    }
-    // LSERK update / RHS store
-    if (row < Np) {
+      // chain rule (eq. 6) for this thread's 6 columns -> per-warp scratch
 #pragma unroll
       for (int nt = 0; nt < 3; ++nt)
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-          const int col = 24 * g + 8 * nt + 2 * tig + v;
-          const int e = col / 6, c = col - 6 * (col / 6);
-          if (e < ne) {
-            const int64_t idx = (k0 + e) * ES + c * Np + row;
-            if (UPDATE) {
-              const double rr = (p.first_stage ? 0.0 : p.rk_a * p.res[idx]) + p.dt * r[nt][v];
-              p.res[idx] = rr;
-              p.u_out[idx] = sU[col * LDU + row] + p.rk_b * rr;
-            } else {
-              p.rhs_out[idx] = r[nt][v];
+          const int lc = 8 * nt + 2 * tig + v;  // column within the group
+          const double* Gm = sG + (4 * g + lc / 6) * GEO_W;
+          const double ur = acc[0][nt][v], us = acc[1][nt][v], ut = acc[2][nt][v];
+          scr[(0 * 24 + lc) * 10 + gid] = Gm[0] * ur + Gm[3] * us + Gm[6] * ut;  // d/dx
+          scr[(1 * 24 + lc) * 10 + gid] = Gm[1] * ur + Gm[4] * us + Gm[7] * ut;  // d/dy
+          scr[(2 * 24 + lc) * 10 + gid] = Gm[2] * ur + Gm[5] * us + Gm[8] * ut;  // d/dz
+        }
+      __syncwarp();
+      double r[3][2];
+#pragma unroll
+      for (int nt = 0; nt < 3; ++nt)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int lc = 8 * nt + 2 * tig + v;
+          const int base = (lc / 6) * 6, c = lc % 6;
+          // derivative d (0:x 1:y 2:z) of component q of this column's element
+#define DG_D(d, q) scr[((d) * 24 + base + (q)) * 10 + gid]
+          double val;
+          // d_t E = curl H, d_t H = -curl E   (components: 0..2 E, 3..5 H)
+          switch (c) {
+            case 0: val = DG_D(1, 5) - DG_D(2, 4); break;
+            case 1: val = DG_D(2, 3) - DG_D(0, 5); break;
+            case 2: val = DG_D(0, 4) - DG_D(1, 3); break;
+            case 3: val = -(DG_D(1, 2) - DG_D(2, 1)); break;
+            case 4: val = -(DG_D(2, 0) - DG_D(0, 2)); break;
+            default: val = -(DG_D(0, 1) - DG_D(1, 0)); break;
+          }
+#undef DG_D
+          r[nt][v] = val;
+        }
+      __syncwarp();
+      // lift: r += LIFT . Flux
+      const double* fp = sF + (24 * g + gid) * LDF + tig;
+      if constexpr (C::OPS_SMEM) {
+        const double* lp = sA + 3 * M8 * C::LDA + row * C::LDL + tig;
+#pragma unroll
+        for (int kk = 0; kk < KL; kk += 4) {
+          const double a = lp[kk];
+#pragma unroll
+          for (int nt = 0; nt < 3; ++nt) dmma(r[nt], a, fp[nt * 8 * LDF + kk]);
+        }
+      } else {
+        const double* lp = opsA + size_t(3) * M8 * KV + size_t(row) * KL + tig;
+#pragma unroll 4
+        for (int kk = 0; kk < KL; kk += 4) {
+          const double a = __ldg(lp + kk);
+#pragma unroll
+          for (int nt = 0; nt < 3; ++nt) dmma(r[nt], a, fp[nt * 8 * LDF + kk]);
+        }
+      }
+      // LSERK update / RHS store
+      if (row < Np) {
+#pragma unroll
+        for (int nt = 0; nt < 3; ++nt)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int col = 24 * g + 8 * nt + 2 * tig + v;
+            const int e = col / 6, c = col - 6 * (col / 6);
+            if (e < ne) {
+              const int64_t idx = (k0 + e) * ES + c * Np + row;
+              if (UPDATE) {
+                const double rold = p.first_stage ? 0.0 : sR[col * LDU + row];
+                const double rr = p.rk_a * rold + p.dt * r[nt][v];
+                p.res[idx] = rr;
+                p.u_out[idx] = sU[col * LDU + row] + p.rk_b * rr;
+              } else {
+                p.rhs_out[idx] = r[nt][v];
+              }
             }
           }
-        }
+      }
     }
+    // all warps are done with this tile's buffers, scratch and face buffer
+    cp_wait<0>();
+    __syncthreads();
+    // exterior traces and residual of the next tile (its indices landed with the prefetch group)
+    if (next < ntiles) {
+      issue_traces(buf ? sI0 : sI1);
+      issue_res(next);
+    }
+    cp_commit();
   }
+  cp_wait<0>();
 }
 
 template <int N>
 void launch_stage_mma(const StageParams<double>& p, const double* opsA, int mode, cudaStream_t st) {
   using C = MmaCfg<N>;
-  static bool attr_done = false;
-  if (!attr_done) {
+  static int grid_max = 0;
+  if (!grid_max) {
     cudaFuncSetAttribute(dg_stage_mma<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
     cudaFuncSetAttribute(dg_stage_mma<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
-    attr_done = true;
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, dg_stage_mma<N, true>, C::NT, C::SMEM_BYTES);
+    grid_max = sms * (per > 0 ? per : 1);
   }
   if (p.K <= 0) return;
-  const unsigned grid = unsigned((p.K + C::E - 1) / C::E);
+  const int64_t ntiles = (p.K + C::E - 1) / C::E;
+  const unsigned grid = unsigned(ntiles < grid_max ? ntiles : grid_max);
   if (mode == 1)
     dg_stage_mma<N, true><<<grid, C::NT, C::SMEM_BYTES, st>>>(p, opsA);
   else

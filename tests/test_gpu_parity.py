@@ -170,6 +170,24 @@ def test_bench_mesh_full_size(N, prec):
     s.close()
 
 
+@pytest.mark.parametrize("prec,variant", VARIANTS, ids=["f64-basic", "f64-mma", "f32-basic"])
+@pytest.mark.parametrize("N", range(1, 10))
+def test_many_tiles_per_cta_shuffled(N, prec, variant):
+    # K = 10368 on a shuffled/rotated/jittered mesh: the persistent MMA kernel runs
+    # several element tiles per CTA (exercises its cp.async double buffering)
+    VX, E = mesh(12, 21, 22, 23)
+    st = setup("m12", VX, E, N)
+    U0 = di.random_fields(st.K, N, seed=5)
+    s = Solver(N, precision=prec, variant=variant)
+    s.mesh_upload(VX, E)
+    s.fields_upload(U0)
+    assert relerr(s.rhs(), oracle.rhs(st, U0)) < TOL_RHS[prec]
+    dt = di.dt_rule(VX, E, N)
+    s.lserk_step(dt, 2)
+    assert relerr(s.fields_download(), oracle.lserk4(st, U0, dt, 2)) < TOL_STEP[prec]
+    s.close()
+
+
 def _submesh(VX, E, EToE, seeds, layers):
     keep = set(int(k) for k in seeds)
     front = set(keep)
