@@ -6,33 +6,33 @@
 // is E elements; its 6E element-component columns are the MMA N dimension.
 //   volume (a1):  Y_b = D_b . U      D_b in {Dr, Ds, Dt}: [M8 x KV],  U: [KV x 6E]
 //   lift   (a4):  R  = curl(Y) + LIFT . Flux                 LIFT: [M8 x NF]
-// A operands (the reference operators, zero-padded to M8 rows / KV columns) are
-// resident in shared memory for N <= OPS_SMEM_MAX_N (loaded once per CTA, the
-// paper's "matrix in shared memory" strategy) and read through
-// L1 otherwise.  B operands (the element tile U and the face buffer) live in
+// A operands (reference operators, zero-padded to M8 rows / KV columns) are
+// resident in shared memory where they fit (the paper's "matrix in shared
+// memory" strategy), else read through L1.  B operands live in
 // shared memory with leading dimension = 4 (mod 16) doubles: conflict-free
 // fragment loads.
 //
-// Pipeline per CTA (grid = resident CTAs; tiles strided over the grid):
-//   while computing tile i, cp.async brings tile i+1's U, geometry and gather
-//   indices into the other buffer; after tile i's MMA phase the gathered
-//   exterior traces u+ and the residual of tile i+1 are fetched with cp.async
-//   (a2's irregular gather, made asynchronous).  Every
-//   cp.async group is waited on by its issuing thread and followed by a block
-//   barrier before any other thread reads it.  The face buffer (a2+a3) never leaves the chip; the
-//   LSERK update (a5) is applied straight from the lift accumulators.
+// Column permutation.  Within a group of 4 elements (24 columns = 3 n-tiles) the
+// physical column of (element e, component c) is
+//     P = 8*(c/2) + 2*e + (c%2),
+// so the m8n8k4 accumulator layout (lane holds columns 2*tig+v of each n-tile)
+// puts all six components of element e = tig at node row gid into ONE thread:
+// the chain rule, the curl (eq. 4, eq. 6) and the LSERK update are thread-local.
 //
-// Work split: task = (node m-tile t of 8 rows, column group g of 4 elements =
-// 24 columns = 3 n-tiles).  A warp computes all three derivative blocks of its
-// task, so the chain rule + curl (eq. 6) need only a per-warp scratch exchange.
+// Pipeline per CTA (grid = resident CTAs; tiles strided over the grid): while
+// computing tile i, cp.async brings tile i+1's U, geometry and gather indices
+// into the other buffer; after tile i's MMA phase the exterior traces u+ of tile
+// i+1 (a2's irregular gather) are gathered with cp.async
+// straight into the face buffer, where the flux phase turns them into
+// Fscale/2 * n.(F-F*) in place; the residual of tile i+1 is fetched alongside.
+// Every cp.async group is waited on by its issuing thread and followed by a
+// block barrier before any other thread reads it.
 #pragma once
 #include <cuda_runtime.h>
 
 #include "stage_basic.cuh"
 
 namespace dg {
-
-constexpr int OPS_SMEM_MAX_N = 0;  // measured: L1-served operators + 2 CTAs/SM beat smem-resident + 1 CTA/SM
 
 template <int N>
 struct MmaCfg {
@@ -46,32 +46,31 @@ struct MmaCfg {
   static constexpr int LDF = ld4(KL);
   static constexpr int LDA = ld4(KV);  // smem-resident operators
   static constexpr int LDL = ld4(KL);
-  static constexpr bool OPS_SMEM = N <= OPS_SMEM_MAX_N;
-  // elements per tile (multiple of 4) and warps per CTA: MT*(E/4)
-  // tasks split evenly over the warps
-  static constexpr int E = N <= 1 ? 32 : N <= 3 ? 16 : N <= 6 ? 8 : 4;
+  // per-order tile (elements, multiple of 4), warps, operator residency
+  static constexpr int E = N == 1 ? 32 : N == 2 ? 16 : N == 3 ? 8 : 4;
+  static constexpr int NW = N == 1 ? 8 : N == 2 ? 8 : N == 3 ? 6 : N == 4 ? 5 : N == 5 ? 7 : N == 6 ? 11 : N == 7 ? 5 : 7;
+  static constexpr bool OPS_SMEM = N <= 5;
   static constexpr int G = E / 4;
   static constexpr int TASKS = MT * G;
-  static constexpr int NW = N == 1 ? 8 : N == 2 ? 8 : N == 3 ? 6 : N == 4 ? 5 : N == 5 ? 7 : N == 6 ? 11 : N == 7 ? 5 : 7;
   static constexpr int NT = NW * 32;
   static constexpr int COLS = 6 * E;
-  static constexpr int SCR = 3 * 24 * 10;  // per-warp derivative scratch [d][col][row], stride 10: <= 2-way conflicts
   // shared memory carve-up (doubles)
   static constexpr int U_SZ = COLS * LDU;
   static constexpr int GEO_SZ = E * GEO_W + (E * GEO_W) % 2;
-  static constexpr int TR_SZ = 6 * E * NF;  // gathered u+ traces [e][c][m]
-  static constexpr int SCRATCH_SZ = (TR_SZ > NW * SCR ? TR_SZ : NW * SCR);  // traces and scratch share
-  static constexpr int GIDX_SZ = (E * NF + 1) / 2;                          // int32 -> doubles
+  static constexpr int GIDX_SZ = (E * NF + 1) / 2;  // int32 -> doubles
   static constexpr int F_SZ = COLS * LDF;
   static constexpr int OPS_SZ = OPS_SMEM ? 3 * M8 * LDA + M8 * LDL : 0;
-  static constexpr int FM_SZ = (NF + 3) / 4;                                // int16 -> doubles
+  static constexpr int FM_SZ = (NF + 3) / 4;        // int16 -> doubles
   static constexpr size_t SMEM_DOUBLES =
-      size_t(2) * U_SZ + 2 * GEO_SZ + U_SZ /*res*/ + SCRATCH_SZ + 2 * GIDX_SZ + F_SZ + OPS_SZ + FM_SZ;
+      size_t(2) * U_SZ + U_SZ /*res*/ + 2 * GEO_SZ + 2 * GIDX_SZ + F_SZ + OPS_SZ + FM_SZ;
   static constexpr size_t SMEM_BYTES = SMEM_DOUBLES * 8;
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   // padded operator buffer in global memory: Dr|Ds|Dt as [3][M8][KV], then LIFT [M8][KL]
   static constexpr size_t OPS_DOUBLES = size_t(3) * M8 * KV + size_t(M8) * KL;
 };
+
+// physical B-operand column of (element e of the tile, component c)
+__device__ __forceinline__ int pcol(int e, int c) { return 24 * (e >> 2) + 8 * (c >> 1) + 2 * (e & 3) + (c & 1); }
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -92,7 +91,7 @@ template <int n>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(n)); }
 
 template <int N, bool UPDATE>
-__global__ void __launch_bounds__(MmaCfg<N>::NT, 1)
+__global__ void __launch_bounds__(MmaCfg<N>::NT)
     dg_stage_mma(const StageParams<double> p, const double* __restrict__ opsA) {
   using C = MmaCfg<N>;
   constexpr int Np = C::Np, Nfp = C::Nfp, NF = C::NF, M8 = C::M8, KV = C::KV, KL = C::KL;
@@ -100,14 +99,13 @@ __global__ void __launch_bounds__(MmaCfg<N>::NT, 1)
   extern __shared__ __align__(16) double smem[];
   double* sU0 = smem;
   double* sU1 = sU0 + C::U_SZ;
-  double* sG0 = sU1 + C::U_SZ;
+  double* sR = sU1 + C::U_SZ;                  // residual of the current tile [P][LDU]
+  double* sG0 = sR + C::U_SZ;
   double* sG1 = sG0 + C::GEO_SZ;
-  double* sR = sG1 + C::GEO_SZ;                 // residual of the current tile [6E][LDU]
-  double* sT = sR + C::U_SZ;                    // gathered traces [e][c][m]  (aliases the curl scratch)
-  int32_t* sI0 = reinterpret_cast<int32_t*>(sT + C::SCRATCH_SZ);  // gather indices [e][m] (x2)
-  int32_t* sI1 = reinterpret_cast<int32_t*>(sT + C::SCRATCH_SZ + C::GIDX_SZ);
-  double* sF = sT + C::SCRATCH_SZ + 2 * C::GIDX_SZ;  // face buffer [6E][LDF]
-  double* sA = sF + C::F_SZ;                    // operators (N <= OPS_SMEM_MAX_N)
+  int32_t* sI0 = reinterpret_cast<int32_t*>(sG1 + C::GEO_SZ);  // gather indices [e][m] (x2)
+  int32_t* sI1 = reinterpret_cast<int32_t*>(sG1 + C::GEO_SZ + C::GIDX_SZ);
+  double* sF = sG1 + C::GEO_SZ + 2 * C::GIDX_SZ;  // traces u+, then the face buffer [P][LDF]
+  double* sA = sF + C::F_SZ;                   // operators (OPS_SMEM)
   int16_t* sFm = reinterpret_cast<int16_t*>(sA + C::OPS_SZ);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -129,21 +127,24 @@ __global__ void __launch_bounds__(MmaCfg<N>::NT, 1)
     }
   }
 
-  auto tile_count = [&](int64_t tile) -> int {
-    const int64_t k0 = p.k_begin + tile * E, kend = p.k_begin + p.K;
+  auto tile_count = [&](int64_t tl) -> int {
+    const int64_t k0 = p.k_begin + tl * E, kend = p.k_begin + p.K;
     return int(kend - k0 < E ? kend - k0 : E);
   };
-  // issue cp.async for tile's U, geometry, gather indices (zero-fill the padding / absent elements)
-  auto issue_tile = [&](int64_t tile, double* sU, double* sG, int32_t* sI) {
-    const int64_t k0 = p.k_begin + tile * E;
-    const int ne = tile_count(tile);
+  // cp.async of a tile's U (permuted columns), geometry and gather indices;
+  // absent elements are zero-filled (their columns still enter the MMAs)
+  auto issue_tile = [&](int64_t tl, double* sU, double* sG, int32_t* sI) {
+    const int64_t k0 = p.k_begin + tl * E;
+    const int ne = tile_count(tl);
     const double* ug = p.u_in + k0 * ES;
     for (int w = tid; w < E * 6 * Np; w += NT) {
-      const int col = w / Np, n = w - col * Np;
-      if (col < ne * 6)
-        cp_async8(sU + col * LDU + n, ug + w);
+      const int ec = w / Np, n = w - ec * Np;
+      const int e = ec / 6, c = ec - 6 * e;
+      double* dst = sU + pcol(e, c) * LDU + n;
+      if (e < ne)
+        cp_async8(dst, ug + w);
       else
-        sU[col * LDU + n] = 0.0;
+        *dst = 0.0;
     }
     for (int w = tid; w < E * GEO_W; w += NT) {
       if (w < ne * GEO_W)
@@ -158,9 +159,8 @@ __global__ void __launch_bounds__(MmaCfg<N>::NT, 1)
         sI[w] = -1;
     }
   };
-  // issue cp.async for the exterior traces u+ of the tile whose indices are in sI.
-  // Each thread handles exactly the index slots it copied itself, so only its own
-  // cp.async groups must have completed (no block barrier needed).
+  // gather the exterior traces u+ of the tile whose indices are in sI into sF.
+  // Each thread handles exactly the index slots it copied itself (no barrier needed).
   auto issue_traces = [&](const int32_t* sI) {
     for (int w = tid; w < E * NF; w += NT) {
       const int32_t gi = sI[w];
@@ -169,22 +169,22 @@ __global__ void __launch_bounds__(MmaCfg<N>::NT, 1)
         const int64_t cs = (gi >= p.ghost_base) ? Nfp : Np;
         const double* src = p.u_in + gi;
 #pragma unroll
-        for (int c = 0; c < 6; ++c) cp_async8(sT + (e * 6 + c) * NF + m, src + c * cs);
+        for (int c = 0; c < 6; ++c) cp_async8(sF + pcol(e, c) * LDF + m, src + c * cs);
       }
     }
   };
-  // residual of a tile into sR (read in the epilogue; issued one tile ahead)
   auto issue_res = [&](int64_t tl) {
     if (!UPDATE || p.first_stage) return;
-    const int64_t kk0 = p.k_begin + tl * E;
-    const int nn = tile_count(tl);
-    const double* rg = p.res + kk0 * ES;
-    for (int w = tid; w < nn * 6 * Np; w += NT) {
-      const int col = w / Np, n = w - col * Np;
-      cp_async8(sR + col * LDU + n, rg + w);
+    const int64_t k0 = p.k_begin + tl * E;
+    const int ne = tile_count(tl);
+    const double* rg = p.res + k0 * ES;
+    for (int w = tid; w < ne * 6 * Np; w += NT) {
+      const int ec = w / Np, n = w - ec * Np;
+      const int e = ec / 6, c = ec - 6 * e;
+      cp_async8(sR + pcol(e, c) * LDU + n, rg + w);
     }
   };
-  // zero the K padding of both U buffers once (never overwritten by tile loads)
+  // zero the K padding of both U buffers once (tile loads never touch it)
   if constexpr (LDU > Np) {
     constexpr int PAD = LDU - Np;
     for (int w = tid; w < C::COLS * PAD; w += NT) {
@@ -207,37 +207,42 @@ __global__ void __launch_bounds__(MmaCfg<N>::NT, 1)
 
   int buf = 0;
   for (; tile < ntiles; tile += gridDim.x, buf ^= 1) {
-    double* sU = buf ? sU1 : sU0;
-    double* sG = buf ? sG1 : sG0;
+    const double* sU = buf ? sU1 : sU0;
+    const double* sG = buf ? sG1 : sG0;
     const int32_t* sI = buf ? sI1 : sI0;
     const int64_t k0 = p.k_begin + tile * E;
     const int ne = tile_count(tile);
     const int64_t next = tile + gridDim.x;
-    // prefetch the next tile's U / geometry / indices into the other buffer
     if (next < ntiles) issue_tile(next, buf ? sU0 : sU1, buf ? sG0 : sG1, buf ? sI0 : sI1);
     cp_commit();
-    cp_wait<1>();  // everything but the prefetch group: this tile's traces and residual have landed
+    cp_wait<1>();  // everything but the prefetch: this tile's traces and residual have landed
     __syncthreads();
-    // ---- a2 + a3: upwind/PEC flux into the face buffer (all operands in smem)
+
+    // ---- a2 + a3: upwind/PEC flux, in place over the gathered traces
     for (int w = tid; w < E * NF; w += NT) {
       const int e = w / NF, m = w - e * NF, f = m / Nfp;
+      double* fcol[6];
+#pragma unroll
+      for (int c = 0; c < 6; ++c) fcol[c] = sF + pcol(e, c) * LDF + m;
       double fl[6] = {0, 0, 0, 0, 0, 0};
       if (e < ne) {
         const double* g = sG + e * GEO_W + 9 + 4 * f;
         const double nx = g[0], ny = g[1], nz = g[2], fs = g[3];
-        const double* uM = sU + (e * 6) * LDU + sFm[m];
+        const int nM = sFm[m];
+        double uM[6];
+#pragma unroll
+        for (int c = 0; c < 6; ++c) uM[c] = sU[pcol(e, c) * LDU + nM];
         double dE[3], dH[3];
         if (sI[w] >= 0) {
-          const double* uP = sT + (e * 6) * NF + m;
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            dE[c] = uP[c * NF] - uM[c * LDU];
-            dH[c] = uP[(c + 3) * NF] - uM[(c + 3) * LDU];
+            dE[c] = *fcol[c] - uM[c];
+            dH[c] = *fcol[c + 3] - uM[c + 3];
           }
         } else {  // PEC wall: E+ = -E-, H+ = H-
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            dE[c] = -2.0 * uM[c * LDU];
+            dE[c] = -2.0 * uM[c];
             dH[c] = 0.0;
           }
         }
@@ -247,12 +252,11 @@ __global__ void __launch_bounds__(MmaCfg<N>::NT, 1)
         for (int c = 0; c < 6; ++c) fl[c] *= sc;
       }
 #pragma unroll
-      for (int c = 0; c < 6; ++c) sF[(e * 6 + c) * LDF + m] = fl[c];
+      for (int c = 0; c < 6; ++c) *fcol[c] = fl[c];
     }
-    __syncthreads();  // face buffer complete; the traces buffer is now free (curl scratch)
+    __syncthreads();
 
-    // ---- a1 + curl + a4 + a5 per warp task
-    double* scr = sT + warp * C::SCR;
+    // ---- a1 + curl + a4 + a5 per warp task (m-tile t, group g); thread = (node row, element 4g+tig)
     for (int task = warp; task < C::TASKS; task += C::NW) {
       const int t = task % C::MT, g = task / C::MT;
       const int row = 8 * t + gid;
@@ -291,42 +295,26 @@ __global__ void __launch_bounds__(MmaCfg<N>::NT, 1)
           }
         }
       }
-      // chain rule (eq. 6) for this thread's 6 columns -> per-warp scratch
-#pragma unroll
-      for (int nt = 0; nt < 3; ++nt)
-#pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          const int lc = 8 * nt + 2 * tig + v;  // column within the group
-          const double* Gm = sG + (4 * g + lc / 6) * GEO_W;
-          const double ur = acc[0][nt][v], us = acc[1][nt][v], ut = acc[2][nt][v];
-          scr[(0 * 24 + lc) * 10 + gid] = Gm[0] * ur + Gm[3] * us + Gm[6] * ut;  // d/dx
-          scr[(1 * 24 + lc) * 10 + gid] = Gm[1] * ur + Gm[4] * us + Gm[7] * ut;  // d/dy
-          scr[(2 * 24 + lc) * 10 + gid] = Gm[2] * ur + Gm[5] * us + Gm[8] * ut;  // d/dz
-        }
-      __syncwarp();
+      // chain rule (eq. 6) + curl, thread-local: acc[b][c/2][c%2] = D_b u_c of element 4g+tig
       double r[3][2];
+      {
+        const double* Gm = sG + (4 * g + tig) * GEO_W;
+        double dx[6], dy[6], dz[6];
 #pragma unroll
-      for (int nt = 0; nt < 3; ++nt)
-#pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          const int lc = 8 * nt + 2 * tig + v;
-          const int base = (lc / 6) * 6, c = lc % 6;
-          // derivative d (0:x 1:y 2:z) of component q of this column's element
-#define DG_D(d, q) scr[((d) * 24 + base + (q)) * 10 + gid]
-          double val;
-          // d_t E = curl H, d_t H = -curl E   (components: 0..2 E, 3..5 H)
-          switch (c) {
-            case 0: val = DG_D(1, 5) - DG_D(2, 4); break;
-            case 1: val = DG_D(2, 3) - DG_D(0, 5); break;
-            case 2: val = DG_D(0, 4) - DG_D(1, 3); break;
-            case 3: val = -(DG_D(1, 2) - DG_D(2, 1)); break;
-            case 4: val = -(DG_D(2, 0) - DG_D(0, 2)); break;
-            default: val = -(DG_D(0, 1) - DG_D(1, 0)); break;
-          }
-#undef DG_D
-          r[nt][v] = val;
+        for (int c = 0; c < 6; ++c) {
+          const double ur = acc[0][c >> 1][c & 1], us = acc[1][c >> 1][c & 1], ut = acc[2][c >> 1][c & 1];
+          dx[c] = Gm[0] * ur + Gm[3] * us + Gm[6] * ut;
+          dy[c] = Gm[1] * ur + Gm[4] * us + Gm[7] * ut;
+          dz[c] = Gm[2] * ur + Gm[5] * us + Gm[8] * ut;
         }
-      __syncwarp();
+        // d_t E = curl H, d_t H = -curl E   (components: 0..2 E, 3..5 H)
+        r[0][0] = dy[5] - dz[4];
+        r[0][1] = dz[3] - dx[5];
+        r[1][0] = dx[4] - dy[3];
+        r[1][1] = -(dy[2] - dz[1]);
+        r[2][0] = -(dz[0] - dx[2]);
+        r[2][1] = -(dx[1] - dy[0]);
+      }
       // lift: r += LIFT . Flux
       const double* fp = sF + (24 * g + gid) * LDF + tig;
       if constexpr (C::OPS_SMEM) {
@@ -346,29 +334,27 @@ __global__ void __launch_bounds__(MmaCfg<N>::NT, 1)
           for (int nt = 0; nt < 3; ++nt) dmma(r[nt], a, fp[nt * 8 * LDF + kk]);
         }
       }
-      // LSERK update / RHS store
-      if (row < Np) {
+      // LSERK update / RHS store for (node row, element 4g+tig, component c)
+      const int e = 4 * g + tig;
+      if (row < Np && e < ne) {
+        const int64_t base = (k0 + e) * ES + row;
 #pragma unroll
-        for (int nt = 0; nt < 3; ++nt)
-#pragma unroll
-          for (int v = 0; v < 2; ++v) {
-            const int col = 24 * g + 8 * nt + 2 * tig + v;
-            const int e = col / 6, c = col - 6 * (col / 6);
-            if (e < ne) {
-              const int64_t idx = (k0 + e) * ES + c * Np + row;
-              if (UPDATE) {
-                const double rold = p.first_stage ? 0.0 : sR[col * LDU + row];
-                const double rr = p.rk_a * rold + p.dt * r[nt][v];
-                p.res[idx] = rr;
-                p.u_out[idx] = sU[col * LDU + row] + p.rk_b * rr;
-              } else {
-                p.rhs_out[idx] = r[nt][v];
-              }
-            }
+        for (int c = 0; c < 6; ++c) {
+          const int64_t idx = base + c * Np;
+          const double rhs = r[c >> 1][c & 1];
+          const int col = 24 * g + 8 * (c >> 1) + 2 * tig + (c & 1);
+          if (UPDATE) {
+            const double rold = p.first_stage ? 0.0 : sR[col * LDU + row];
+            const double rr = p.rk_a * rold + p.dt * rhs;
+            p.res[idx] = rr;
+            p.u_out[idx] = sU[col * LDU + row] + p.rk_b * rr;
+          } else {
+            p.rhs_out[idx] = rhs;
           }
+        }
       }
     }
-    // all warps are done with this tile's buffers, scratch and face buffer
+    // all warps are done with this tile's buffers and face buffer
     cp_wait<0>();
     __syncthreads();
     // exterior traces and residual of the next tile (its indices landed with the prefetch group)
