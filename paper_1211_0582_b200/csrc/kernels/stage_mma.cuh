@@ -115,15 +115,15 @@ __global__ void __launch_bounds__(MmaCfg<N>::NT)
 
   // ---- one-time: operators and Fmask into shared memory
   for (int m = tid; m < NF; m += NT) sFm[m] = p.fmask[m];
-  if constexpr (C::OPS_SMEM) {
+  if constexpr (C::OPS_SMEM) {  // cp.async: overlaps with the first tile's loads
     for (int w = tid; w < 3 * M8 * KV; w += NT) {
       const int r = w / KV, k = w - r * KV;
-      sA[r * C::LDA + k] = opsA[w];
+      cp_async8(sA + r * C::LDA + k, opsA + w);
     }
     const double* Lg = opsA + 3 * M8 * KV;
     for (int w = tid; w < M8 * KL; w += NT) {
       const int r = w / KL, k = w - r * KL;
-      sA[3 * M8 * C::LDA + r * C::LDL + k] = Lg[w];
+      cp_async8(sA + 3 * M8 * C::LDA + r * C::LDL + k, Lg + w);
     }
   }
 
@@ -315,24 +315,41 @@ __global__ void __launch_bounds__(MmaCfg<N>::NT)
         r[2][0] = -(dz[0] - dx[2]);
         r[2][1] = -(dx[1] - dy[0]);
       }
-      // lift: r += LIFT . Flux
+      // lift: r += LIFT . Flux  (even/odd k-steps in two accumulator sets: 6 independent DMMA chains)
       const double* fp = sF + (24 * g + gid) * LDF + tig;
+      double r2[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+      static_assert(KL % 8 == 4 || KL % 8 == 0, "KL multiple of 4");
       if constexpr (C::OPS_SMEM) {
         const double* lp = sA + 3 * M8 * C::LDA + row * C::LDL + tig;
 #pragma unroll
-        for (int kk = 0; kk < KL; kk += 4) {
-          const double a = lp[kk];
+        for (int kk = 0; kk < KL; kk += 8) {
+          const double a0 = lp[kk];
 #pragma unroll
-          for (int nt = 0; nt < 3; ++nt) dmma(r[nt], a, fp[nt * 8 * LDF + kk]);
+          for (int nt = 0; nt < 3; ++nt) dmma(r[nt], a0, fp[nt * 8 * LDF + kk]);
+          if (kk + 4 < KL) {
+            const double a1 = lp[kk + 4];
+#pragma unroll
+            for (int nt = 0; nt < 3; ++nt) dmma(r2[nt], a1, fp[nt * 8 * LDF + kk + 4]);
+          }
         }
       } else {
         const double* lp = opsA + size_t(3) * M8 * KV + size_t(row) * KL + tig;
-#pragma unroll 4
-        for (int kk = 0; kk < KL; kk += 4) {
-          const double a = __ldg(lp + kk);
+#pragma unroll 2
+        for (int kk = 0; kk < KL; kk += 8) {
+          const double a0 = __ldg(lp + kk);
+          const double a1 = (kk + 4 < KL) ? __ldg(lp + kk + 4) : 0.0;
 #pragma unroll
-          for (int nt = 0; nt < 3; ++nt) dmma(r[nt], a, fp[nt * 8 * LDF + kk]);
+          for (int nt = 0; nt < 3; ++nt) dmma(r[nt], a0, fp[nt * 8 * LDF + kk]);
+          if (kk + 4 < KL) {
+#pragma unroll
+            for (int nt = 0; nt < 3; ++nt) dmma(r2[nt], a1, fp[nt * 8 * LDF + kk + 4]);
+          }
         }
+      }
+#pragma unroll
+      for (int nt = 0; nt < 3; ++nt) {
+        r[nt][0] += r2[nt][0];
+        r[nt][1] += r2[nt][1];
       }
       // LSERK update / RHS store for (node row, element 4g+tig, component c)
       const int e = 4 * g + tig;
