@@ -67,9 +67,10 @@ typedef enum {
 } dg_status;
 
 typedef enum {
-  DG_VARIANT_AUTO = 0,  /* library picks per (N, precision) */
-  DG_VARIANT_BASIC = 1, /* one fused element-tile kernel per stage, FMA contractions */
-  DG_VARIANT_MMA = 2    /* tensor-core contractions (FP64 DMMA / FP32 3xTF32) where available */
+  DG_VARIANT_AUTO = 0,   /* library picks per (N, precision): FP64 -> MMA_WS, FP32 -> BASIC */
+  DG_VARIANT_BASIC = 1,  /* one fused element-tile kernel per stage, FMA contractions */
+  DG_VARIANT_MMA = 2,    /* FP64: DMMA contractions, cp.async-pipelined persistent kernel */
+  DG_VARIANT_MMA_WS = 3  /* FP64: DMMA contractions, warp-specialized TMA/mbarrier pipeline */
 } dg_variant;
 
 typedef struct {

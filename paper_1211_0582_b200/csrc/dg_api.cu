@@ -17,11 +17,11 @@
 
 namespace dg {
 template <typename S, typename T>
-void cm_to_tiles(const S* src, T* dst, int64_t K, int Np, int64_t ES, void* st);
+void cm_to_tiles(const S* src, T* dst, int64_t K, int Np, const TileLayout& L, void* st);
 template <typename T, typename D>
-void tiles_to_cm(const T* src, D* dst, int64_t K, int Np, int64_t ES, void* st);
+void tiles_to_cm(const T* src, D* dst, int64_t K, int Np, const TileLayout& L, void* st);
 template <typename T>
-void pack_traces(const T* u, T* buf, const int32_t* sidx, int64_t nfaces, int Np, int Nfp, void* st);
+void pack_traces(const T* u, T* buf, const int32_t* sidx, int64_t nfaces, int Nfp, const TileLayout& L, void* st);
 }  // namespace dg
 
 namespace {
@@ -91,7 +91,8 @@ struct dg_solver {
   dg::Partition part;
   bool has_mesh = false, has_fields = false;
   // device
-  int64_t ES = 0, ghost_base = 0, ghost_words = 0, Kl = 0;
+  int64_t ES = 0, ghost_base = 0, ghost_words = 0, Kl = 0, ntiles = 0;
+  dg::TileLayout lay;          // device field layout (depends on precision/variant)
   void* d_u[2] = {nullptr, nullptr};
   void* d_res = nullptr;
   void* d_scratch = nullptr;   // [Kl][ES] (solver precision)
@@ -190,7 +191,7 @@ template <typename T>
 dg_status enqueue_exchange(dg_solver* s, T* u) {
   const auto& P = s->part;
   if (P.n_ghost_faces == 0) return DG_OK;
-  dg::pack_traces<T>(u, static_cast<T*>(s->d_send), s->d_sidx, P.n_ghost_faces, s->Np, s->Nfp, s->comm);
+  dg::pack_traces<T>(u, static_cast<T*>(s->d_send), s->d_sidx, P.n_ghost_faces, s->Nfp, s->lay, s->comm);
   NcclApi& n = nccl();
   const size_t rec = size_t(6) * s->Nfp;
   const int dtype = sizeof(T) == 8 ? ncclFloat64_ : ncclFloat32_;
@@ -224,9 +225,10 @@ dg_status enqueue_stage(dg_solver* s, int stage, double dt, int cur) {
     dg_status st = enqueue_exchange<T>(s, uin);
     if (st != DG_OK) return st;
     CK(cudaEventRecord(s->ev_join, s->comm));
-    launch_stage<T>(s, p, 1, 0, s->part.K_interior, s->stream);
+    const int64_t split = (s->part.K_interior / s->lay.E) * s->lay.E;  // tile-aligned
+    launch_stage<T>(s, p, 1, 0, split, s->stream);
     CK(cudaStreamWaitEvent(s->stream, s->ev_join, 0));
-    launch_stage<T>(s, p, 1, s->part.K_interior, s->Kl, s->stream);
+    launch_stage<T>(s, p, 1, split, s->Kl, s->stream);
   } else {
     launch_stage<T>(s, p, 1, 0, s->Kl, s->stream);
   }
@@ -260,8 +262,20 @@ dg_status upload_setup(dg_solver* s) {
   const int Np = s->Np, Nfp = s->Nfp, NF = 4 * Nfp;
   const int64_t Kl = P.K_local;
   s->Kl = Kl;
-  s->ES = sizeof(T) == 8 ? 6 * Np : ((6 * Np + 3) / 4) * 4;
-  s->ghost_base = Kl * s->ES;
+  if (sizeof(T) == 8 && (s->variant == DG_VARIANT_AUTO || s->variant == DG_VARIANT_MMA_WS)) {
+    s->lay = dg::ws_layout_f64(s->N);
+  } else {
+    s->lay = dg::TileLayout();
+    s->lay.E = 1;
+    s->lay.LD = Np;
+    s->lay.perm = 0;
+    s->lay.TS = sizeof(T) == 8 ? 6 * Np : ((6 * Np + 3) / 4) * 4;
+  }
+  s->ES = s->lay.TS;
+  s->ntiles = s->lay.ntiles(Kl);
+  const int64_t Kpad = s->ntiles * s->lay.E;
+  const int64_t twords = s->ntiles * s->lay.TS;
+  s->ghost_base = twords;
   s->ghost_words = P.n_ghost_faces * 6 * Nfp;
   const int64_t uwords = s->ghost_base + s->ghost_words;
   if (uwords >= (int64_t(1) << 31))
@@ -271,11 +285,13 @@ dg_status upload_setup(dg_solver* s) {
     CK(cudaMalloc(&s->d_u[i], std::max<int64_t>(uwords, 1) * wb));
     CK(cudaMemsetAsync(s->d_u[i], 0, std::max<int64_t>(uwords, 1) * wb, s->stream));
   }
-  CK(cudaMalloc(&s->d_res, std::max<int64_t>(Kl * s->ES, 1) * wb));
-  CK(cudaMalloc(&s->d_scratch, std::max<int64_t>(Kl * s->ES, 1) * wb));
+  CK(cudaMalloc(&s->d_res, std::max<int64_t>(twords, 1) * wb));
+  CK(cudaMemsetAsync(s->d_res, 0, std::max<int64_t>(twords, 1) * wb, s->stream));
+  CK(cudaMalloc(&s->d_scratch, std::max<int64_t>(twords, 1) * wb));
+  CK(cudaMemsetAsync(s->d_scratch, 0, std::max<int64_t>(twords, 1) * wb, s->stream));
   CK(cudaMalloc((void**)&s->d_stage64, std::max<int64_t>(6 * Kl * Np, 1) * sizeof(double)));
-  // geometry [Kl][GEO_W]
-  std::vector<T> geo(size_t(std::max<int64_t>(Kl, 1)) * dg::GEO_W, T(0));
+  // geometry [Kpad][GEO_W] (padding elements zero)
+  std::vector<T> geo(size_t(std::max<int64_t>(Kpad, 1)) * dg::GEO_W, T(0));
   for (int64_t l = 0; l < Kl; ++l) {
     const int64_t k = P.local_ids[l];
     for (int i = 0; i < 9; ++i) geo[l * dg::GEO_W + i] = T(m.rst_x[9 * k + i]);
@@ -284,7 +300,7 @@ dg_status upload_setup(dg_solver* s) {
   CK(cudaMalloc(&s->d_geo, geo.size() * wb));
   CK(cudaMemcpy(s->d_geo, geo.data(), geo.size() * wb, cudaMemcpyHostToDevice));
   std::vector<int32_t> gidx;
-  dg::build_gather_index(s->ref, m, P, s->ES, s->ghost_base, gidx);
+  dg::build_gather_index(s->ref, m, P, s->lay, s->ghost_base, gidx);
   if (gidx.empty()) gidx.push_back(-1);
   CK(cudaMalloc((void**)&s->d_gidx, gidx.size() * sizeof(int32_t)));
   CK(cudaMemcpy(s->d_gidx, gidx.data(), gidx.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
@@ -322,7 +338,7 @@ dg_status upload_setup(dg_solver* s) {
     std::vector<int32_t> sidx(size_t(P.n_ghost_faces) * Nfp);
     for (int64_t g = 0; g < P.n_ghost_faces; ++g)
       for (int j = 0; j < Nfp; ++j)
-        sidx[g * Nfp + j] = int32_t(P.send_elem[g] * s->ES + s->ref.Fmask[P.send_face[g] * Nfp + j]);
+        sidx[g * Nfp + j] = int32_t(s->lay.off(P.send_elem[g], 0, s->ref.Fmask[P.send_face[g] * Nfp + j]));
     CK(cudaMalloc((void**)&s->d_sidx, sidx.size() * sizeof(int32_t)));
     CK(cudaMemcpy(s->d_sidx, sidx.data(), sidx.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   }
@@ -393,6 +409,20 @@ dg_status time_stage(dg_solver* s, int reps, double* ms) {
 
 }  // namespace
 
+#ifdef DG_WS_PROFILE
+namespace dg {
+#define DG_PDECL(n) void ws_prof_N##n(unsigned long long*, int);
+DG_PDECL(1) DG_PDECL(2) DG_PDECL(3) DG_PDECL(4) DG_PDECL(5) DG_PDECL(6) DG_PDECL(7) DG_PDECL(8) DG_PDECL(9)
+}  // namespace dg
+// profiling builds only (libdg_prof.so): read/reset the WS kernel's cycle counters
+extern "C" __attribute__((visibility("default"))) void dg_debug_ws_profile(int N, unsigned long long* out, int reset) {
+  static void (*const t[9])(unsigned long long*, int) = {dg::ws_prof_N1, dg::ws_prof_N2, dg::ws_prof_N3,
+                                                         dg::ws_prof_N4, dg::ws_prof_N5, dg::ws_prof_N6,
+                                                         dg::ws_prof_N7, dg::ws_prof_N8, dg::ws_prof_N9};
+  if (N >= 1 && N <= 9) t[N - 1](out, reset);
+}
+#endif
+
 extern "C" {
 
 void dg_config_default(dg_config* c) {
@@ -422,7 +452,7 @@ dg_status dg_create(const dg_config* cfg, dg_solver** out) {
   if (cfg->order < 1 || cfg->order > 9) return fail(DG_ERR_ORDER, "order N must be in 1..9");
   if (cfg->precision != 4 && cfg->precision != 8) return fail(DG_ERR_ARG, "precision must be 4 or 8");
   if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return fail(DG_ERR_ARG, "bad rank/nranks");
-  if (cfg->variant < 0 || cfg->variant > 2) return fail(DG_ERR_ARG, "bad variant");
+  if (cfg->variant < 0 || cfg->variant > 3) return fail(DG_ERR_ARG, "bad variant");
   std::unique_ptr<dg_solver> s(new dg_solver());
   s->cfg = *cfg;
   s->N = cfg->order;
@@ -519,19 +549,19 @@ static dg_status upload_common(dg_solver* s, const void* src, bool from_host) {
   if (from_host) {
     CK(cudaMemcpyAsync(s->d_stage64, src, n * sizeof(double), cudaMemcpyHostToDevice, s->stream));
     if (s->fp64)
-      dg::cm_to_tiles<double, double>(s->d_stage64, static_cast<double*>(s->d_u[0]), s->Kl, s->Np, s->ES, s->stream);
+      dg::cm_to_tiles<double, double>(s->d_stage64, static_cast<double*>(s->d_u[0]), s->Kl, s->Np, s->lay, s->stream);
     else
-      dg::cm_to_tiles<double, float>(s->d_stage64, static_cast<float*>(s->d_u[0]), s->Kl, s->Np, s->ES, s->stream);
+      dg::cm_to_tiles<double, float>(s->d_stage64, static_cast<float*>(s->d_u[0]), s->Kl, s->Np, s->lay, s->stream);
   } else {
     if (s->fp64)
       dg::cm_to_tiles<double, double>(static_cast<const double*>(src), static_cast<double*>(s->d_u[0]), s->Kl,
-                                      s->Np, s->ES, s->stream);
+                                      s->Np, s->lay, s->stream);
     else
       dg::cm_to_tiles<float, float>(static_cast<const float*>(src), static_cast<float*>(s->d_u[0]), s->Kl, s->Np,
-                                    s->ES, s->stream);
+                                    s->lay, s->stream);
   }
   CK(cudaGetLastError());
-  CK(cudaMemsetAsync(s->d_res, 0, std::max<int64_t>(s->Kl * s->ES, 1) * s->wsize, s->stream));
+  CK(cudaMemsetAsync(s->d_res, 0, std::max<int64_t>(s->ntiles * s->lay.TS, 1) * s->wsize, s->stream));
   if (from_host) CK(cudaStreamSynchronize(s->stream));
   s->has_fields = true;
   return DG_OK;
@@ -555,18 +585,18 @@ static dg_status download_common(dg_solver* s, void* dst, bool to_host, bool rhs
   }
   if (to_host) {
     if (s->fp64)
-      dg::tiles_to_cm<double, double>(static_cast<const double*>(tiles), s->d_stage64, s->Kl, s->Np, s->ES, s->stream);
+      dg::tiles_to_cm<double, double>(static_cast<const double*>(tiles), s->d_stage64, s->Kl, s->Np, s->lay, s->stream);
     else
-      dg::tiles_to_cm<float, double>(static_cast<const float*>(tiles), s->d_stage64, s->Kl, s->Np, s->ES, s->stream);
+      dg::tiles_to_cm<float, double>(static_cast<const float*>(tiles), s->d_stage64, s->Kl, s->Np, s->lay, s->stream);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(dst, s->d_stage64, n * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));
   } else {
     if (s->fp64)
       dg::tiles_to_cm<double, double>(static_cast<const double*>(tiles), static_cast<double*>(dst), s->Kl, s->Np,
-                                      s->ES, s->stream);
+                                      s->lay, s->stream);
     else
-      dg::tiles_to_cm<float, float>(static_cast<const float*>(tiles), static_cast<float*>(dst), s->Kl, s->Np, s->ES,
+      dg::tiles_to_cm<float, float>(static_cast<const float*>(tiles), static_cast<float*>(dst), s->Kl, s->Np, s->lay,
                                     s->stream);
     CK(cudaGetLastError());
   }

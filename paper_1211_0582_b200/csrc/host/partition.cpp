@@ -66,10 +66,10 @@ std::string build_partition(const MeshData& m, int rank, int nranks, const int32
   return "";
 }
 
-void build_gather_index(const RefElem& ref, const MeshData& m, const Partition& P, int64_t ES,
+void build_gather_index(const RefElem& ref, const MeshData& m, const Partition& P, const TileLayout& L,
                         int64_t ghost_base, std::vector<int32_t>& gidx) {
   const int Nfp = ref.Nfp;
-  gidx.assign(size_t(P.K_local) * 4 * Nfp, -1);
+  gidx.assign(size_t(L.ntiles(P.K_local)) * L.E * 4 * Nfp, -1);
   for (int64_t l = 0; l < P.K_local; ++l) {
     const int64_t k = P.local_ids[l];
     for (int f = 0; f < 4; ++f) {
@@ -84,7 +84,7 @@ void build_gather_index(const RefElem& ref, const MeshData& m, const Partition& 
         if (g >= 0)
           v = ghost_base + g * 6 * Nfp + j;
         else
-          v = P.g2l[k2] * ES + ref.Fmask[f2 * Nfp + j];
+          v = L.off(P.g2l[k2], 0, ref.Fmask[f2 * Nfp + j]);
         gidx[(4 * l + f) * Nfp + i] = int32_t(v);
       }
     }

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "mesh.h"
+#include "../kernels/stage_params.h"
 
 namespace dg {
 
@@ -46,8 +47,9 @@ std::string build_partition(const MeshData& m, int rank, int nranks, const int32
                             Partition& out);
 
 // Gather index of the exterior trace for every local face node (see
-// stage_params.h): k2_local*ES + n2, or ghost_base + g*6*Nfp + j, or -1 (PEC).
-void build_gather_index(const RefElem& ref, const MeshData& m, const Partition& P, int64_t ES,
+// stage_params.h): L.off(k2_local, 0, n2), or ghost_base + g*6*Nfp + j, or -1
+// (PEC).  Rows are padded to ntiles*E elements (padding rows = -1).
+void build_gather_index(const RefElem& ref, const MeshData& m, const Partition& P, const TileLayout& L,
                         int64_t ghost_base, std::vector<int32_t>& gidx);
 
 }  // namespace dg

@@ -6,32 +6,47 @@
 
 #include <cstdint>
 
+#include "stage_params.h"
+
 namespace dg {
 
+// [6][K][Np] (component-major) -> device layout L (padding and absent elements zeroed)
 template <typename S, typename T>
-__global__ void k_cm_to_tiles(const S* __restrict__ src, T* __restrict__ dst, int64_t K, int Np, int64_t ES) {
-  const int64_t total = K * ES;
+__global__ void k_cm_to_tiles(const S* __restrict__ src, T* __restrict__ dst, int64_t K, int Np, TileLayout L) {
+  const int64_t total = L.ntiles(K) * L.TS;
+  const int cols = 6 * L.E;
   for (int64_t w = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; w < total; w += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t k = w / ES;
-    const int r = int(w - k * ES);
+    const int64_t t = w / L.TS;
+    const int64_t r = w - t * L.TS;
+    const int col = int(r / L.LD), n = int(r - int64_t(col) * L.LD);
     T v = T(0);
-    if (r < 6 * Np) {
-      const int c = r / Np, n = r - c * Np;
-      v = T(src[(int64_t(c) * K + k) * Np + n]);
+    if (col < cols && n < Np) {
+      int e, c;
+      if (L.perm) {
+        const int g = col / 24, q = col - 24 * g, nt = q >> 3, rr = q & 7;
+        e = 4 * g + (rr >> 1);
+        c = 2 * nt + (rr & 1);
+      } else {
+        e = col / 6;
+        c = col - 6 * e;
+      }
+      const int64_t k = t * L.E + e;
+      if (k < K) v = T(src[(int64_t(c) * K + k) * Np + n]);
     }
     dst[w] = v;
   }
 }
 
+// device layout L -> [6][K][Np]
 template <typename T, typename D>
-__global__ void k_tiles_to_cm(const T* __restrict__ src, D* __restrict__ dst, int64_t K, int Np, int64_t ES) {
+__global__ void k_tiles_to_cm(const T* __restrict__ src, D* __restrict__ dst, int64_t K, int Np, TileLayout L) {
   const int64_t total = 6 * K * Np;
   for (int64_t w = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; w < total; w += int64_t(gridDim.x) * blockDim.x) {
     const int64_t c = w / (K * Np);
     const int64_t rem = w - c * K * Np;
     const int64_t k = rem / Np;
     const int n = int(rem - k * Np);
-    dst[w] = D(src[k * ES + c * Np + n]);
+    dst[w] = D(src[L.off(k, int(c), n)]);
   }
 }
 
@@ -43,21 +58,21 @@ static unsigned grid_for(int64_t n) {
 }
 
 template <typename S, typename T>
-void cm_to_tiles(const S* src, T* dst, int64_t K, int Np, int64_t ES, void* st) {
-  k_cm_to_tiles<S, T><<<grid_for(K * ES), 256, 0, static_cast<cudaStream_t>(st)>>>(src, dst, K, Np, ES);
+void cm_to_tiles(const S* src, T* dst, int64_t K, int Np, const TileLayout& L, void* st) {
+  k_cm_to_tiles<S, T><<<grid_for(L.ntiles(K) * L.TS), 256, 0, static_cast<cudaStream_t>(st)>>>(src, dst, K, Np, L);
 }
 
 template <typename T, typename D>
-void tiles_to_cm(const T* src, D* dst, int64_t K, int Np, int64_t ES, void* st) {
-  k_tiles_to_cm<T, D><<<grid_for(6 * K * Np), 256, 0, static_cast<cudaStream_t>(st)>>>(src, dst, K, Np, ES);
+void tiles_to_cm(const T* src, D* dst, int64_t K, int Np, const TileLayout& L, void* st) {
+  k_tiles_to_cm<T, D><<<grid_for(6 * K * Np), 256, 0, static_cast<cudaStream_t>(st)>>>(src, dst, K, Np, L);
 }
 
-template void cm_to_tiles<double, double>(const double*, double*, int64_t, int, int64_t, void*);
-template void cm_to_tiles<double, float>(const double*, float*, int64_t, int, int64_t, void*);
-template void cm_to_tiles<float, float>(const float*, float*, int64_t, int, int64_t, void*);
-template void tiles_to_cm<double, double>(const double*, double*, int64_t, int, int64_t, void*);
-template void tiles_to_cm<float, double>(const float*, double*, int64_t, int, int64_t, void*);
-template void tiles_to_cm<float, float>(const float*, float*, int64_t, int, int64_t, void*);
+template void cm_to_tiles<double, double>(const double*, double*, int64_t, int, const TileLayout&, void*);
+template void cm_to_tiles<double, float>(const double*, float*, int64_t, int, const TileLayout&, void*);
+template void cm_to_tiles<float, float>(const float*, float*, int64_t, int, const TileLayout&, void*);
+template void tiles_to_cm<double, double>(const double*, double*, int64_t, int, const TileLayout&, void*);
+template void tiles_to_cm<float, double>(const float*, double*, int64_t, int, const TileLayout&, void*);
+template void tiles_to_cm<float, float>(const float*, float*, int64_t, int, const TileLayout&, void*);
 
 }  // namespace dg
 
@@ -67,22 +82,22 @@ namespace dg {
 // buf[g][c][j] = u[sidx[g][j] + c*Np]  (sender's own face-node order).
 template <typename T>
 __global__ void k_pack_traces(const T* __restrict__ u, T* __restrict__ buf, const int32_t* __restrict__ sidx,
-                              int64_t nfaces, int Np, int Nfp) {
+                              int64_t nfaces, int Nfp, TileLayout L) {
   const int64_t total = nfaces * 6 * Nfp;
   for (int64_t w = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; w < total; w += int64_t(gridDim.x) * blockDim.x) {
     const int64_t g = w / (6 * Nfp);
     const int r = int(w - g * 6 * Nfp);
     const int c = r / Nfp, j = r - c * Nfp;
-    buf[w] = u[sidx[g * Nfp + j] + int64_t(c) * Np];
+    buf[w] = u[sidx[g * Nfp + j] + int64_t(L.coff(c)) * L.LD];
   }
 }
 
 template <typename T>
-void pack_traces(const T* u, T* buf, const int32_t* sidx, int64_t nfaces, int Np, int Nfp, void* st) {
-  k_pack_traces<T><<<grid_for(nfaces * 6 * Nfp), 256, 0, static_cast<cudaStream_t>(st)>>>(u, buf, sidx, nfaces,
-                                                                                          Np, Nfp);
+void pack_traces(const T* u, T* buf, const int32_t* sidx, int64_t nfaces, int Nfp, const TileLayout& L, void* st) {
+  k_pack_traces<T><<<grid_for(nfaces * 6 * Nfp), 256, 0, static_cast<cudaStream_t>(st)>>>(u, buf, sidx, nfaces, Nfp,
+                                                                                          L);
 }
-template void pack_traces<double>(const double*, double*, const int32_t*, int64_t, int, int, void*);
-template void pack_traces<float>(const float*, float*, const int32_t*, int64_t, int, int, void*);
+template void pack_traces<double>(const double*, double*, const int32_t*, int64_t, int, const TileLayout&, void*);
+template void pack_traces<float>(const float*, float*, const int32_t*, int64_t, int, const TileLayout&, void*);
 
 }  // namespace dg

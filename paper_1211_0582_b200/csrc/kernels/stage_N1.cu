@@ -1,13 +1,15 @@
-// Stage-kernel instantiations for order N=1 (stage_basic.cuh, stage_mma.cuh).
-#include "stage_mma.cuh"
+// Stage-kernel instantiations for order N=1 (stage_basic.cuh, stage_mma.cuh, stage_ws.cuh).
+#include "stage_ws.cuh"
 
 namespace dg {
 
 void launch_stage_f64_N1(const StageParams<double>& p, int mode, int variant, void* st) {
-  if (variant == 1)  // DG_VARIANT_BASIC
+  if (variant == 1)       // DG_VARIANT_BASIC
     launch_stage_basic<double, 1>(p, mode, static_cast<cudaStream_t>(st));
-  else               // AUTO / MMA: FP64 tensor-core (DMMA) contractions
+  else if (variant == 2)  // DG_VARIANT_MMA: DMMA, cp.async-pipelined, element-major layout
     launch_stage_mma<1>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
+  else                    // AUTO / DG_VARIANT_MMA_WS: DMMA, warp-specialized TMA pipeline, tiled layout
+    launch_stage_ws<1>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
 }
 
 void launch_stage_f32_N1(const StageParams<float>& p, int mode, int variant, void* st) {
@@ -15,6 +17,15 @@ void launch_stage_f32_N1(const StageParams<float>& p, int mode, int variant, voi
   launch_stage_basic<float, 1>(p, mode, static_cast<cudaStream_t>(st));
 }
 
-size_t ops_pad_doubles_N1() { return MmaCfg<1>::OPS_DOUBLES; }
+TileLayout ws_layout_N1() { return ws_layout<1>(); }
+
+#ifdef DG_WS_PROFILE
+void ws_prof_N1(unsigned long long* out, int reset) {
+  if (reset)
+    ws_prof_reset();
+  else
+    ws_prof_read(out);
+}
+#endif
 
 }  // namespace dg

@@ -5,7 +5,8 @@ namespace dg {
 
 #define DG_DECL(n)                                                                  \
   void launch_stage_f64_N##n(const StageParams<double>&, int, int, void*);          \
-  void launch_stage_f32_N##n(const StageParams<float>&, int, int, void*);
+  void launch_stage_f32_N##n(const StageParams<float>&, int, int, void*);          \
+  TileLayout ws_layout_N##n();
 DG_DECL(1) DG_DECL(2) DG_DECL(3) DG_DECL(4) DG_DECL(5) DG_DECL(6) DG_DECL(7) DG_DECL(8) DG_DECL(9)
 #undef DG_DECL
 
@@ -21,6 +22,12 @@ StageLauncher<float> stage_launcher_f32(int N) {
       launch_stage_f32_N1, launch_stage_f32_N2, launch_stage_f32_N3, launch_stage_f32_N4, launch_stage_f32_N5,
       launch_stage_f32_N6, launch_stage_f32_N7, launch_stage_f32_N8, launch_stage_f32_N9};
   return (N >= 1 && N <= 9) ? t[N - 1] : nullptr;
+}
+
+TileLayout ws_layout_f64(int N) {
+  static TileLayout (*const t[9])() = {ws_layout_N1, ws_layout_N2, ws_layout_N3, ws_layout_N4, ws_layout_N5,
+                                       ws_layout_N6, ws_layout_N7, ws_layout_N8, ws_layout_N9};
+  return (N >= 1 && N <= 9) ? t[N - 1]() : TileLayout{};
 }
 
 }  // namespace dg

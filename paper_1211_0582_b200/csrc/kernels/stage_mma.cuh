@@ -96,7 +96,8 @@ __global__ void __launch_bounds__(MmaCfg<N>::NT)
   using C = MmaCfg<N>;
   constexpr int Np = C::Np, Nfp = C::Nfp, NF = C::NF, M8 = C::M8, KV = C::KV, KL = C::KL;
   constexpr int E = C::E, LDU = C::LDU, LDF = C::LDF, NT = C::NT;
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(16) double smem_mma[];
+  double* smem = smem_mma;
   double* sU0 = smem;
   double* sU1 = sU0 + C::U_SZ;
   double* sR = sU1 + C::U_SZ;                  // residual of the current tile [P][LDU]

@@ -17,9 +17,36 @@
 #pragma once
 #include <cstdint>
 
+#ifdef __CUDACC__
+#define DG_HD __host__ __device__ __forceinline__
+#else
+#define DG_HD inline
+#endif
+
 namespace dg {
 
-constexpr int GEO_W = 25;
+constexpr int GEO_W = 26;  // 25 used (rx..tz, 4 x (n, Fscale)); padded to 16 B for bulk copies
+
+// Field layout in device memory: element k, component c, node n lives at
+//   (k / E) * TS + col(k % E, c) * LD + n.
+// BASIC/MMA kernels: E = 1, LD = Np, TS = ES, col = c        -> k*ES + c*Np + n
+// WS kernel:         E = tile, LD = padded K extent, TS = 6*E*LD, col = the
+//                    MMA column permutation (the tile is the smem image of the
+//                    B operand, so one bulk copy moves it).  Padding is zero.
+struct TileLayout {
+  int E = 1;
+  int LD = 0;
+  int perm = 0;
+  int64_t TS = 0;
+  DG_HD int col(int e, int c) const {
+    return perm ? 24 * (e >> 2) + 8 * (c >> 1) + 2 * (e & 3) + (c & 1) : 6 * e + c;
+  }
+  DG_HD int coff(int c) const { return perm ? 8 * (c >> 1) + (c & 1) : c; }  // col(e,c) - col(e,0)
+  DG_HD int64_t off(int64_t k, int c, int n) const {
+    return (k / E) * TS + int64_t(col(int(k % E), c)) * LD + n;
+  }
+  DG_HD int64_t ntiles(int64_t K) const { return (K + E - 1) / E; }
+};
 
 template <typename T>
 struct StageParams {
@@ -46,6 +73,7 @@ template <typename T>
 using StageLauncher = void (*)(const StageParams<T>&, int mode, int variant, void* stream);
 
 StageLauncher<double> stage_launcher_f64(int N);
+TileLayout ws_layout_f64(int N);  // tiled layout of the WS kernel for order N
 StageLauncher<float> stage_launcher_f32(int N);
 
 }  // namespace dg

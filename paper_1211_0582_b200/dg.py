@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdg.so")
+LIB_PATH = os.environ.get("DG_LIB") or os.path.join(_HERE, "libdg.so")  # DG_LIB: profiling build
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "dg.h")
 
 if not os.path.exists(LIB_PATH):

@@ -52,10 +52,11 @@ def setup(key, VX, E, N):
     return _SETUPS[k]
 
 
-VARIANTS = [(8, 1), (8, 2), (4, 1)]   # (precision, variant): FP64 BASIC, FP64 MMA (DMMA), FP32 BASIC
+VARIANTS = [(8, 1), (8, 2), (8, 3), (4, 1)]   # (precision, variant): FP64 BASIC, MMA, MMA_WS (DMMA), FP32 BASIC
+VIDS = ["f64-basic", "f64-mma", "f64-ws", "f32-basic"]
 
 
-@pytest.mark.parametrize("prec,variant", VARIANTS, ids=["f64-basic", "f64-mma", "f32-basic"])
+@pytest.mark.parametrize("prec,variant", VARIANTS, ids=VIDS)
 @pytest.mark.parametrize("N", range(1, 10))
 def test_rhs_random_fields_shuffled_jittered(N, prec, variant):
     VX, E = mesh(3, 1, 2, 3)                      # K = 162: ragged tail for every tile size
@@ -95,7 +96,7 @@ def test_c1_cavity_100_steps(prec):
     s.close()
 
 
-@pytest.mark.parametrize("prec,variant", VARIANTS, ids=["f64-basic", "f64-mma", "f32-basic"])
+@pytest.mark.parametrize("prec,variant", VARIANTS, ids=VIDS)
 @pytest.mark.parametrize("N", range(1, 10))
 def test_lserk_steps_all_orders(N, prec, variant):
     VX, E = mesh(2, 5, 6, 7)
@@ -170,7 +171,7 @@ def test_bench_mesh_full_size(N, prec):
     s.close()
 
 
-@pytest.mark.parametrize("prec,variant", VARIANTS, ids=["f64-basic", "f64-mma", "f32-basic"])
+@pytest.mark.parametrize("prec,variant", VARIANTS, ids=VIDS)
 @pytest.mark.parametrize("N", range(1, 10))
 def test_many_tiles_per_cta_shuffled(N, prec, variant):
     # K = 10368 on a shuffled/rotated/jittered mesh: the persistent MMA kernel runs
