@@ -77,6 +77,17 @@ def load_peaks():
     return peaks
 
 
+def load_traffic(N, prec, variant):
+    """Per-launch DRAM bytes of the stage kernel from a committed ncu --set full capture, if any."""
+    p = os.path.join(ROOT, "profiles", "r1_traffic.json")
+    try:
+        with open(p) as fh:
+            t = json.load(fh)
+        return t.get(f"{'f64' if prec == 8 else 'f32'}:{variant}:{N}", {}).get("dram_bytes")
+    except Exception:
+        return None
+
+
 def roofline(N, prec, K_total, kernel_ms, peaks, variant=0, traffic=None):
     """Roofline of the fused stage kernel.  FP64 MMA variant (AUTO/MMA): contractions
     on the FP64 tensor pipe (DMMA) -> bound "tensor" against the measured DMMA
@@ -217,7 +228,8 @@ def run_dg(args, N, prec, rank, world, local, dist, stream, flush, nccl_id, peak
     # dominant kernel: the fused stage kernel (5 launches per step, the step's only kernel at 1 GPU)
     kernel_ms = ms_step / 5 if world == 1 else s.time_stage_kernel(10)
     res["stage_kernel_ms"] = round(kernel_ms, 5)
-    res["roofline"] = roofline(N, prec, Kl, kernel_ms, peaks, args.variant)
+    res["roofline"] = roofline(N, prec, Kl, kernel_ms, peaks, args.variant,
+                               traffic=load_traffic(N, prec, args.variant) if world == 1 else None)
     if e2e:
         # end to end through the C ABI with HOST buffers: upload (pinned H2D) + step + download (D2H)
         host_in = torch.from_numpy(np.ascontiguousarray(U0)).pin_memory().numpy()

@@ -53,8 +53,18 @@ struct WsCfg {
   static constexpr int LA = S - 2 < 2 ? S - 2 : 2;  // trace gathers issued LA tiles ahead of the flux
   static constexpr bool OPS_SMEM = N <= 5;
   static constexpr bool RES_SMEM = N <= 4;
-  static constexpr int MW = 8;      // two MMA warps per SMSP: one's epilogue hides under the other's DMMAs
-  static constexpr int PW = 4;      // flux warps (trace gather + flux); plus one dedicated TMA loader warp
+  // warp roles (measured, tools/tune_ws.sh): >= 2 MMA warps per SMSP so one's epilogue hides
+  // under the other's DMMAs; 3 per SMSP when the operators come through L1/L2 (N >= 5)
+#ifdef DG_WS_MW
+  static constexpr int MW = DG_WS_MW;
+#else
+  static constexpr int MW = N >= 5 ? 12 : 8;
+#endif
+#ifdef DG_WS_PW
+  static constexpr int PW = DG_WS_PW;  // flux warps (trace gather + flux); plus one dedicated TMA loader warp
+#else
+  static constexpr int PW = N == 3 ? 6 : 4;
+#endif
   static constexpr int NT = 32 * (MW + 1 + PW);
   static constexpr int PT = 32 * PW;
   static constexpr int G = E / 4;
