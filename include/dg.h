@@ -81,7 +81,9 @@ typedef struct {
   void* stream;         /* cudaStream_t to enqueue on; NULL = solver-owned stream */
   int32_t rank;         /* this process's rank, 0..nranks-1 */
   int32_t nranks;       /* number of ranks (one GPU each); 1 = single GPU */
-  const void* nccl_id;  /* 128-byte ncclUniqueId from rank 0 (nranks > 1), else NULL */
+  const void* nccl_id;  /* 128-byte ncclUniqueId from rank 0 (nranks > 1).  NULL with nranks > 1
+                           makes a loopback partition solver: no NCCL; the ranks live in this
+                           process and are stepped together by dg_group_lserk_step */
   int32_t variant;      /* dg_variant */
 } dg_config;
 
@@ -89,8 +91,8 @@ typedef struct {
 DG_API void dg_config_default(dg_config* cfg);
 
 /* Create a solver.  Builds the reference element of order N on the host (FP64).
- * Errors: DG_ERR_ARG (null, precision not 4/8, nranks < 1, rank out of range,
- * nccl_id NULL with nranks > 1), DG_ERR_ORDER, DG_ERR_CUDA (device unusable). */
+ * Errors: DG_ERR_ARG (null, precision not 4/8, nranks < 1, rank out of range, bad
+ * variant), DG_ERR_ORDER, DG_ERR_CUDA (device unusable), DG_ERR_NCCL. */
 DG_API dg_status dg_create(const dg_config* cfg, dg_solver** out);
 
 /* Upload the (global) mesh: nv vertices VX[nv][3] (FP64), K tets EToV[K][4]
@@ -120,8 +122,20 @@ DG_API dg_status dg_rhs(dg_solver* s, double* rhs);
 DG_API dg_status dg_rhs_device(dg_solver* s, void* rhs_dev);
 
 /* Advance nsteps >= 0 LSERK4 steps of size dt (5 stages each; asynchronous,
- * graph-launched).  With nranks > 1 each stage exchanges partition-face traces. */
+ * graph-launched).  With nranks > 1 each stage exchanges partition-face traces
+ * through NCCL.  Loopback solvers return DG_ERR_STATE (use dg_group_lserk_step). */
 DG_API dg_status dg_lserk_step(dg_solver* s, double dt, int32_t nsteps);
+
+/* Advance a group of loopback partition solvers (same mesh, order, precision and
+ * variant; group[i] may be given in any order but must cover ranks 0..n-1 once)
+ * by nsteps LSERK4 steps in lockstep.  Per stage each rank packs its partition-
+ * face traces, the records are copied device-to-device into the peers' ghost
+ * regions (the NCCL path's data movement, without NCCL), and
+ * every rank runs its interior range concurrently with the copies, then its
+ * partition-boundary range.  Results are bitwise identical to one solver on the
+ * whole mesh (reading R15).  Asynchronous.  Errors: DG_ERR_ARG,
+ * DG_ERR_STATE (missing fields), DG_ERR_CUDA. */
+DG_API dg_status dg_group_lserk_step(dg_solver* const* group, int32_t n, double dt, int32_t nsteps);
 
 /* Copy the current fields out: host FP64 [6][K_local][Np] (synchronises) or
  * device memory in the solver precision (asynchronous). */

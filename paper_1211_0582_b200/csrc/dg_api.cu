@@ -107,6 +107,8 @@ struct dg_solver {
   cudaStream_t stream = nullptr, comm = nullptr;
   bool own_stream = false;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+  cudaEvent_t ev_packed = nullptr, ev_copied = nullptr;  // loopback transport
+  bool loopback = false;  // nranks > 1 without NCCL: stepped only by dg_group_lserk_step
   ncclComm_t ncomm = nullptr;
   int cur = 0;
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
@@ -233,6 +235,68 @@ dg_status enqueue_stage(dg_solver* s, int stage, double dt, int cur) {
     launch_stage<T>(s, p, 1, 0, s->Kl, s->stream);
   }
   CK(cudaGetLastError());
+  return DG_OK;
+}
+
+template <typename T>
+dg::StageParams<T> stage_params(dg_solver* s, int stage, double dt, int cur) {
+  dg::StageParams<T> p = base_params<T>(s);
+  p.u_in = static_cast<T*>(s->d_u[cur]);
+  p.u_out = static_cast<T*>(s->d_u[cur ^ 1]);
+  p.res = static_cast<T*>(s->d_res);
+  p.rk_a = T(kRkA[stage]);
+  p.rk_b = T(kRkB[stage]);
+  p.dt = T(dt);
+  p.first_stage = stage == 0 ? 1 : 0;
+  return p;
+}
+
+// Loopback transport: one LSERK stage for a group of same-process solvers that
+// partition one mesh.  Identical to the NCCL path except that each partition's
+// ghost records are copied device-to-device from its peers' send buffers.
+template <typename T>
+dg_status group_stage(dg_solver* const* g, int n, int stage, double dt, int cur) {
+  const size_t rec = size_t(6) * g[0]->Nfp;
+  for (int i = 0; i < n; ++i) {  // pack (after my previous stage, after peers finished reading my send buffer)
+    dg_solver* s = g[i];
+    if (s->part.n_ghost_faces == 0) continue;
+    CK(cudaEventRecord(s->ev_fork, s->stream));
+    CK(cudaStreamWaitEvent(s->comm, s->ev_fork, 0));
+    for (const auto& pp : s->part.peers) CK(cudaStreamWaitEvent(s->comm, g[pp.rank]->ev_copied, 0));
+    dg::pack_traces<T>(static_cast<T*>(s->d_u[cur]), static_cast<T*>(s->d_send), s->d_sidx, s->part.n_ghost_faces,
+                       s->Nfp, s->lay, s->comm);
+    CK(cudaEventRecord(s->ev_packed, s->comm));
+  }
+  for (int q = 0; q < n; ++q) {  // receive: copy peers' records into my ghost region
+    dg_solver* s = g[q];
+    if (s->part.n_ghost_faces == 0) continue;
+    for (const auto& pp : s->part.peers) {
+      dg_solver* r = g[pp.rank];
+      const dg::PeerPlan* back = nullptr;
+      for (const auto& rp : r->part.peers)
+        if (rp.rank == q) back = &rp;
+      if (!back || back->nfaces != pp.nfaces) return fail(DG_ERR_STATE, "inconsistent partition plans in group");
+      CK(cudaStreamWaitEvent(s->comm, r->ev_packed, 0));
+      T* dst = static_cast<T*>(s->d_u[cur]) + s->ghost_base + pp.recv_off * rec;
+      const T* src = static_cast<const T*>(r->d_send) + back->send_off * rec;
+      CK(cudaMemcpyAsync(dst, src, pp.nfaces * rec * sizeof(T), cudaMemcpyDeviceToDevice, s->comm));
+    }
+    CK(cudaEventRecord(s->ev_copied, s->comm));
+    CK(cudaEventRecord(s->ev_join, s->comm));
+  }
+  for (int i = 0; i < n; ++i) {  // compute: interior range, then (after the ghosts landed) the rest
+    dg_solver* s = g[i];
+    dg::StageParams<T> p = stage_params<T>(s, stage, dt, cur);
+    if (s->part.n_ghost_faces > 0) {
+      const int64_t split = (s->part.K_interior / s->lay.E) * s->lay.E;
+      launch_stage<T>(s, p, 1, 0, split, s->stream);
+      CK(cudaStreamWaitEvent(s->stream, s->ev_join, 0));
+      launch_stage<T>(s, p, 1, split, s->Kl, s->stream);
+    } else {
+      launch_stage<T>(s, p, 1, 0, s->Kl, s->stream);
+    }
+    CK(cudaGetLastError());
+  }
   return DG_OK;
 }
 
@@ -468,7 +532,7 @@ dg_status dg_create(const dg_config* cfg, dg_solver** out) {
   s->Np = s->ref.Np;
   s->Nfp = s->ref.Nfp;
   if (!s->host_only) {
-    if (cfg->nranks > 1 && !cfg->nccl_id) return fail(DG_ERR_ARG, "nccl_id required with nranks > 1");
+    s->loopback = cfg->nranks > 1 && !cfg->nccl_id;  // in-process partitions (dg_group_lserk_step)
     CK(cudaSetDevice(cfg->device));
     if (cfg->stream) {
       s->stream = static_cast<cudaStream_t>(cfg->stream);
@@ -481,7 +545,9 @@ dg_status dg_create(const dg_config* cfg, dg_solver** out) {
     CK(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
     CK(cudaEventCreate(&s->ev_t0));
     CK(cudaEventCreate(&s->ev_t1));
-    if (cfg->nranks > 1) {
+    CK(cudaEventCreateWithFlags(&s->ev_packed, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&s->ev_copied, cudaEventDisableTiming));
+    if (cfg->nranks > 1 && !s->loopback) {
       NcclApi& n = nccl();
       if (!n.ok) return fail(DG_ERR_NCCL, n.err);
       ncclUniqueId id;
@@ -573,6 +639,7 @@ dg_status dg_fields_upload_device(dg_solver* s, const void* f) { g_err.clear(); 
 static dg_status download_common(dg_solver* s, void* dst, bool to_host, bool rhs) {
   dg_status st = need_device(s);
   if (st != DG_OK) return st;
+  if (rhs && s->loopback) return fail(DG_ERR_STATE, "loopback partition solver: rhs needs its peers (use one solver)");
   if (!s->has_fields) return fail(DG_ERR_STATE, "no fields uploaded");
   if (!dst) return fail(DG_ERR_ARG, "null output pointer");
   const int64_t n = 6 * s->Kl * s->Np;
@@ -614,7 +681,38 @@ dg_status dg_lserk_step(dg_solver* s, double dt, int32_t nsteps) {
   if (st != DG_OK) return st;
   if (!s->has_fields) return fail(DG_ERR_STATE, "no fields uploaded");
   if (nsteps < 0) return fail(DG_ERR_ARG, "nsteps < 0");
+  if (s->loopback) return fail(DG_ERR_STATE, "loopback partition solver: step it with dg_group_lserk_step");
   return s->fp64 ? lserk_steps<double>(s, dt, nsteps) : lserk_steps<float>(s, dt, nsteps);
+}
+
+dg_status dg_group_lserk_step(dg_solver* const* group, int32_t n, double dt, int32_t nsteps) {
+  g_err.clear();
+  if (!group || n < 1 || nsteps < 0) return fail(DG_ERR_ARG, "bad group arguments");
+  std::vector<dg_solver*> g(n, nullptr);
+  for (int i = 0; i < n; ++i) {
+    dg_solver* s = group[i];
+    dg_status st = need_device(s);
+    if (st != DG_OK) return st;
+    if (!s->has_fields) return fail(DG_ERR_STATE, "group member without fields");
+    if (s->cfg.nranks != n || s->cfg.rank < 0 || s->cfg.rank >= n || g[s->cfg.rank])
+      return fail(DG_ERR_ARG, "group must hold ranks 0..n-1 of one partition, once each");
+    if (n > 1 && !s->loopback) return fail(DG_ERR_ARG, "group members must be loopback solvers (nccl_id NULL)");
+    g[s->cfg.rank] = s;
+  }
+  for (int i = 1; i < n; ++i)
+    if (g[i]->N != g[0]->N || g[i]->fp64 != g[0]->fp64 || g[i]->cur != g[0]->cur || g[i]->mesh.K != g[0]->mesh.K ||
+        g[i]->lay.E != g[0]->lay.E || g[i]->lay.perm != g[0]->lay.perm)
+      return fail(DG_ERR_ARG, "group members differ in order, precision, variant, mesh or step parity");
+  for (int step = 0; step < nsteps; ++step) {
+    for (int stage = 0; stage < 5; ++stage) {
+      const int cur = g[0]->cur;
+      dg_status st = g[0]->fp64 ? group_stage<double>(g.data(), n, stage, dt, cur)
+                                : group_stage<float>(g.data(), n, stage, dt, cur);
+      if (st != DG_OK) return st;
+      for (int i = 0; i < n; ++i) g[i]->cur ^= 1;
+    }
+  }
+  return DG_OK;
 }
 
 dg_status dg_synchronize(dg_solver* s) {
@@ -708,6 +806,8 @@ void dg_destroy(dg_solver* s) {
     if (s->ev_join) cudaEventDestroy(s->ev_join);
     if (s->ev_t0) cudaEventDestroy(s->ev_t0);
     if (s->ev_t1) cudaEventDestroy(s->ev_t1);
+    if (s->ev_packed) cudaEventDestroy(s->ev_packed);
+    if (s->ev_copied) cudaEventDestroy(s->ev_copied);
     if (s->comm) cudaStreamDestroy(s->comm);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
   }

@@ -22,7 +22,7 @@ if not os.path.exists(LIB_PATH):
 lib = C.CDLL(LIB_PATH)
 
 DG_OK, DG_ERR_ARG, DG_ERR_ORDER, DG_ERR_MESH, DG_ERR_STATE, DG_ERR_CUDA, DG_ERR_NCCL, DG_ERR_OOM = range(8)
-DG_VARIANT_AUTO, DG_VARIANT_BASIC, DG_VARIANT_MMA = 0, 1, 2
+DG_VARIANT_AUTO, DG_VARIANT_BASIC, DG_VARIANT_MMA, DG_VARIANT_MMA_WS = 0, 1, 2, 3
 STATUS_NAMES = {0: "DG_OK", 1: "DG_ERR_ARG", 2: "DG_ERR_ORDER", 3: "DG_ERR_MESH", 4: "DG_ERR_STATE",
                 5: "DG_ERR_CUDA", 6: "DG_ERR_NCCL", 7: "DG_ERR_OOM"}
 
@@ -50,6 +50,7 @@ _SIGS = {
     "dg_rhs": (C.c_int, [_P, _D]),
     "dg_rhs_device": (C.c_int, [_P, _P]),
     "dg_lserk_step": (C.c_int, [_P, C.c_double, C.c_int32]),
+    "dg_group_lserk_step": (C.c_int, [C.POINTER(_P), C.c_int32, C.c_double, C.c_int32]),
     "dg_fields_download": (C.c_int, [_P, _D]),
     "dg_fields_download_device": (C.c_int, [_P, _P]),
     "dg_synchronize": (C.c_int, [_P]),
@@ -86,6 +87,12 @@ def check(status, where=""):
 
 def _ptr(a, t):
     return a.ctypes.data_as(t) if a is not None else None
+
+
+def group_lserk_step(solvers, dt, nsteps=1):
+    """dg_group_lserk_step over loopback partition solvers (one per rank, same mesh)."""
+    arr = (_P * len(solvers))(*[sv.h for sv in solvers])
+    check(dg_group_lserk_step(arr, len(solvers), float(dt), int(nsteps)), "dg_group_lserk_step")
 
 
 class Solver:
