@@ -67,14 +67,27 @@ def load_peaks():
         peaks["fp64_tflops"] = float(ap["fp64_dfma_tflops"])
         peaks["fp32_tflops"] = float(ap["fp32_ffma_tflops"])
         peaks["dmma_tflops"] = float(ap["fp64_dmma_tflops"])
-        peaks["alu_src"] = "measured (profiles/alu_peaks.json, tools/alu_peaks.cu)"
+        peaks["tf32x3_tflops"] = float(ap.get("tf32_mma_sync_tflops", 301.3)) / 3.0
+        peaks["alu_src"] = "measured (profiles/alu_peaks.json, tools/alu_peaks.cu, tools/tf32_mma.cu)"
     else:
         # unit counts x max clock: 148 SMs x 64 DFMA (128 FFMA) lanes x 2 flop x 1.965 GHz
         peaks["fp64_tflops"] = 148 * 64 * 2 * 1.965e9 / 1e12
         peaks["fp32_tflops"] = 148 * 128 * 2 * 1.965e9 / 1e12
         peaks["dmma_tflops"] = peaks["fp64_tflops"]
+        peaks["tf32x3_tflops"] = peaks["fp32_tflops"]
         peaks["alu_src"] = "derived from unit counts and clocks (not measured)"
     return peaks
+
+
+def ws_kind(N, prec, variant):
+    """Which kernel the library runs for (N, precision, variant) — mirrors dg_api.cu auto_variant()."""
+    if variant == 1:
+        return "basic"
+    if variant == 2:
+        return "mma" if prec == 8 else "basic"
+    if variant == 3:
+        return "ws"
+    return "basic" if (prec == 4 and N == 1) else "ws"
 
 
 def load_traffic(N, prec, variant):
@@ -89,14 +102,19 @@ def load_traffic(N, prec, variant):
 
 
 def roofline(N, prec, K_total, kernel_ms, peaks, variant=0, traffic=None):
-    """Roofline of the fused stage kernel.  FP64 MMA variant (AUTO/MMA): contractions
-    on the FP64 tensor pipe (DMMA) -> bound "tensor" against the measured DMMA
-    peak; BASIC FP64 / FP32: "alu" against the measured DFMA / FFMA peak."""
+    """Roofline of the fused stage kernel.  FP64 MMA/WS variants: contractions on the
+    FP64 tensor pipe (DMMA) -> bound "tensor" against the measured DMMA peak.  FP32
+    WS variant: 3xTF32 on HMMA -> "tensor" against the measured TF32 mma.sync peak / 3
+    (algorithmic flops counted once).  BASIC: "alu" against measured DFMA / FFMA."""
     w = 8 if prec == 8 else 4
     F = flops_per_elem_stage(N) * K_total
     B = bytes_per_elem_stage(N, w) * K_total
-    tensor = prec == 8 and variant != 1
-    pipe = (peaks["dmma_tflops"] if tensor else peaks["fp64_tflops"]) if prec == 8 else peaks["fp32_tflops"]
+    kind = ws_kind(N, prec, variant)
+    tensor = kind != "basic"
+    if prec == 8:
+        pipe = peaks["dmma_tflops"] if tensor else peaks["fp64_tflops"]
+    else:
+        pipe = peaks["tf32x3_tflops"] if tensor else peaks["fp32_tflops"]
     ridge = pipe * 1e12 / (peaks["hbm_gbs"] * 1e9)
     ai = F / B
     if ai < ridge:
@@ -356,7 +374,7 @@ def main():
                     "config": {"workload": workload, "K_total": head["K_total"], "order": N,
                                "precision": head["precision"], "parallelism": f"mesh z-slabs x{world}, NCCL halo",
                                "l2": "flushed before every timed step (256 MiB write, not timed)",
-                               "variant": args.variant},
+                               "variant": args.variant, "kernel": ws_kind(N, prec, args.variant)},
                     "roofline": head["roofline"], "e2e": head["e2e"],
                     "gpu_launches": head["launches_per_step"] * args.steps,
                     "stage_kernel_ms": head["stage_kernel_ms"],

@@ -67,10 +67,12 @@ typedef enum {
 } dg_status;
 
 typedef enum {
-  DG_VARIANT_AUTO = 0,   /* library picks per (N, precision): FP64 -> MMA_WS, FP32 -> BASIC */
+  DG_VARIANT_AUTO = 0,   /* measured best per (precision, N): MMA_WS, except FP32 N=1 -> BASIC */
   DG_VARIANT_BASIC = 1,  /* one fused element-tile kernel per stage, FMA contractions */
-  DG_VARIANT_MMA = 2,    /* FP64: DMMA contractions, cp.async-pipelined persistent kernel */
-  DG_VARIANT_MMA_WS = 3  /* FP64: DMMA contractions, warp-specialized TMA/mbarrier pipeline */
+  DG_VARIANT_MMA = 2,    /* FP64: DMMA contractions, cp.async-pipelined persistent kernel
+                            (FP32: same as BASIC) */
+  DG_VARIANT_MMA_WS = 3  /* warp-specialized TMA/mbarrier pipeline; contractions on tensor
+                            cores: FP64 DMMA, FP32 3xTF32 HMMA */
 } dg_variant;
 
 typedef struct {

@@ -151,6 +151,14 @@ void release_device(dg_solver* s) {
   p = s->d_sidx; free_dev(p); s->d_sidx = nullptr;
 }
 
+// DG_VARIANT_AUTO: the measured-best kernel per (precision, order) on the bench
+// config (bench.py sweep): FP64 -> MMA_WS for all N; FP32 -> BASIC at N = 1
+// (HBM-bound, smallest tiles win), MMA_WS (3xTF32) otherwise.
+int auto_variant(bool fp64, int N) {
+  if (!fp64 && N == 1) return DG_VARIANT_BASIC;
+  return DG_VARIANT_MMA_WS;
+}
+
 dg_status need_device(dg_solver* s) {
   if (!s) return fail(DG_ERR_ARG, "null solver");
   if (s->host_only) return fail(DG_ERR_STATE, "compute call on a host-only solver (device = -1)");
@@ -326,8 +334,11 @@ dg_status upload_setup(dg_solver* s) {
   const int Np = s->Np, Nfp = s->Nfp, NF = 4 * Nfp;
   const int64_t Kl = P.K_local;
   s->Kl = Kl;
-  if (sizeof(T) == 8 && (s->variant == DG_VARIANT_AUTO || s->variant == DG_VARIANT_MMA_WS)) {
+  const bool ws = s->variant == DG_VARIANT_AUTO || s->variant == DG_VARIANT_MMA_WS;
+  if (sizeof(T) == 8 && ws) {
     s->lay = dg::ws_layout_f64(s->N);
+  } else if (sizeof(T) == 4 && ws) {
+    s->lay = dg::ws32_layout_f32(s->N);
   } else {
     s->lay = dg::TileLayout();
     s->lay.E = 1;
@@ -392,6 +403,13 @@ dg_status upload_setup(dg_solver* s) {
       for (int j = 0; j < NF; ++j) pad[size_t(3) * M8 * KV + size_t(i) * NF + j] = T(s->ref.LIFT(i, j));
     CK(cudaMalloc(&s->d_ops_pad, pad.size() * wb));
     CK(cudaMemcpy(s->d_ops_pad, pad.data(), pad.size() * wb, cudaMemcpyHostToDevice));
+  } else {
+    // FP32 3xTF32: hi/lo split operators, zero-padded (stage_ws32.cuh)
+    std::vector<float> pad(dg::ws32_ops_count(s->N));
+    dg::ws32_ops_build(s->N, s->ref.Dr.a.data(), s->ref.Ds.a.data(), s->ref.Dt.a.data(), s->ref.LIFT.a.data(),
+                       pad.data());
+    CK(cudaMalloc(&s->d_ops_pad, pad.size() * sizeof(float)));
+    CK(cudaMemcpy(s->d_ops_pad, pad.data(), pad.size() * sizeof(float), cudaMemcpyHostToDevice));
   }
   std::vector<int16_t> fm(NF);
   for (int i = 0; i < NF; ++i) fm[i] = int16_t(s->ref.Fmask[i]);
@@ -522,7 +540,7 @@ dg_status dg_create(const dg_config* cfg, dg_solver** out) {
   s->N = cfg->order;
   s->fp64 = cfg->precision == 8;
   s->wsize = s->fp64 ? 8 : 4;
-  s->variant = cfg->variant;
+  s->variant = cfg->variant == DG_VARIANT_AUTO ? auto_variant(cfg->precision == 8, cfg->order) : cfg->variant;
   s->host_only = cfg->device < 0;
   try {
     s->ref = dg::build_ref_elem(s->N);

@@ -6,7 +6,10 @@ namespace dg {
 #define DG_DECL(n)                                                                  \
   void launch_stage_f64_N##n(const StageParams<double>&, int, int, void*);          \
   void launch_stage_f32_N##n(const StageParams<float>&, int, int, void*);          \
-  TileLayout ws_layout_N##n();
+  TileLayout ws_layout_N##n();                                                      \
+  TileLayout ws32_layout_N##n();                                                    \
+  size_t ws32_ops_count_N##n();                                                     \
+  void ws32_ops_N##n(const double*, const double*, const double*, const double*, float*);
 DG_DECL(1) DG_DECL(2) DG_DECL(3) DG_DECL(4) DG_DECL(5) DG_DECL(6) DG_DECL(7) DG_DECL(8) DG_DECL(9)
 #undef DG_DECL
 
@@ -28,6 +31,26 @@ TileLayout ws_layout_f64(int N) {
   static TileLayout (*const t[9])() = {ws_layout_N1, ws_layout_N2, ws_layout_N3, ws_layout_N4, ws_layout_N5,
                                        ws_layout_N6, ws_layout_N7, ws_layout_N8, ws_layout_N9};
   return (N >= 1 && N <= 9) ? t[N - 1]() : TileLayout{};
+}
+
+TileLayout ws32_layout_f32(int N) {
+  static TileLayout (*const t[9])() = {ws32_layout_N1, ws32_layout_N2, ws32_layout_N3, ws32_layout_N4, ws32_layout_N5,
+                                       ws32_layout_N6, ws32_layout_N7, ws32_layout_N8, ws32_layout_N9};
+  return (N >= 1 && N <= 9) ? t[N - 1]() : TileLayout{};
+}
+
+size_t ws32_ops_count(int N) {
+  static size_t (*const t[9])() = {ws32_ops_count_N1, ws32_ops_count_N2, ws32_ops_count_N3,
+                                   ws32_ops_count_N4, ws32_ops_count_N5, ws32_ops_count_N6,
+                                   ws32_ops_count_N7, ws32_ops_count_N8, ws32_ops_count_N9};
+  return (N >= 1 && N <= 9) ? t[N - 1]() : 0;
+}
+
+void ws32_ops_build(int N, const double* Dr, const double* Ds, const double* Dt, const double* L, float* out) {
+  static void (*const t[9])(const double*, const double*, const double*, const double*, float*) = {
+      ws32_ops_N1, ws32_ops_N2, ws32_ops_N3, ws32_ops_N4, ws32_ops_N5,
+      ws32_ops_N6, ws32_ops_N7, ws32_ops_N8, ws32_ops_N9};
+  if (N >= 1 && N <= 9) t[N - 1](Dr, Ds, Dt, L, out);
 }
 
 }  // namespace dg

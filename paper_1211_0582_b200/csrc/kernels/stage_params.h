@@ -73,7 +73,10 @@ template <typename T>
 using StageLauncher = void (*)(const StageParams<T>&, int mode, int variant, void* stream);
 
 StageLauncher<double> stage_launcher_f64(int N);
-TileLayout ws_layout_f64(int N);  // tiled layout of the WS kernel for order N
+TileLayout ws_layout_f64(int N);   // tiled layout of the FP64 WS kernel for order N
+TileLayout ws32_layout_f32(int N); // tiled layout of the FP32 (3xTF32) WS kernel
+size_t ws32_ops_count(int N);      // floats in its split hi/lo operator buffer
+void ws32_ops_build(int N, const double* Dr, const double* Ds, const double* Dt, const double* LIFT, float* out);
 StageLauncher<float> stage_launcher_f32(int N);
 
 }  // namespace dg

@@ -1,0 +1,464 @@
+// WS variant, FP32: the warp-specialized TMA/mbarrier stage kernel of
+// stage_ws.cuh with the two contractions on the tensor cores as 3xTF32
+// (mma.sync.m16n8k8.tf32 -> SASS HMMA.1688.F32.TF32):
+//     A.B ~= A_hi.B_hi + A_hi.B_lo + A_lo.B_hi      (x_hi = tf32(x), x_lo = tf32(x - x_hi))
+// which keeps FP32-level accuracy (plain TF32 fails the 1e-4 FP32 tolerance:
+// SURVEY.md §7 hard part 2).  A_hi/A_lo are split once on the host; B (element
+// tile, face buffer) is split in registers as fragments are loaded.  The flux,
+// chain rule, curl and LSERK update stay on the FFMA pipe, which runs
+// concurrently with HMMA (tools/tf32_mma.cu: 518 TF32 FMA/clk/SM ~ 300 TFLOP/s,
+// while FFMA warps keep 104 FMA/clk/SM alongside).
+//
+// m16n8k8 fragments: A a0=(g,t) a1=(g+8,t) a2=(g,t+4) a3=(g+8,t+4); B b0=(k=t,n=g)
+// b1=(k=t+4,n=g); C c0=(g,2t) c1=(g,2t+1) c2=(g+8,2t) c3=(g+8,2t+1) with g = lane/4,
+// t = lane%4.  Columns 2t+v per n-tile, as for DMMA, so the same column
+// permutation gives each thread all six components of element 4g+t — here for
+// two node rows (g and g+8 of the 16-row m-tile).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstring>
+
+#include "stage_ws.cuh"
+
+namespace dg {
+
+__host__ __device__ constexpr int ldx8(int x) {  // >= x, = 4 (mod 8): conflict-free 8x4 TF32 fragments
+  return (x % 8 == 4) ? x : ldx8(x + 4);
+}
+
+template <int N>
+struct Ws32Cfg {
+  static constexpr int Np = Order<N>::Np, Nfp = Order<N>::Nfp, NF = Order<N>::NF;
+  static constexpr int M16 = (Np + 15) / 16 * 16;
+  static constexpr int MT = M16 / 16;
+  static constexpr int KV = (Np + 7) / 8 * 8;
+  static constexpr int KL = (NF + 7) / 8 * 8;
+  static constexpr int LD = ldx8(KV);
+  static constexpr int LDF = ldx8(KL);
+  static constexpr int LDA = ldx8(KV);
+  static constexpr int LDL = ldx8(KL);
+  static constexpr int E = N == 1 ? 32 : N == 2 ? 16 : N == 3 ? 8 : 4;
+  static constexpr int S = N <= 6 ? 5 : N <= 8 ? 4 : 3;
+  static constexpr int LA = S - 2 < 2 ? S - 2 : 2;
+  static constexpr bool OPS_SMEM = N <= 4;
+  static constexpr bool RES_SMEM = N <= 6;
+  static constexpr int MW = 8;  // 12 spills at the 544-thread register budget
+  static constexpr int PW = 4;
+  static constexpr int NT = 32 * (MW + 1 + PW);
+  static constexpr int PT = 32 * PW;
+  static constexpr int G = E / 4;
+  static constexpr int T = MT * G;
+  static constexpr int TS = 6 * E * LD;  // floats per tile
+  static constexpr int GEOT = E * GEO_W;
+  static constexpr int IDXT = E * NF;
+  static constexpr int OFF_U = 0;
+  static constexpr int OFF_R = OFF_U + r16(TS * 4);
+  static constexpr int OFF_G = OFF_R + (RES_SMEM ? r16(TS * 4) : 0);
+  static constexpr int OFF_I = OFF_G + r16(GEOT * 4);
+  static constexpr int OFF_F = OFF_I + r16(IDXT * 4);
+  static constexpr int SLOT = OFF_F + r16(6 * E * LDF * 4);
+  // operators: hi and lo copies of [3][M16][LDA] + [M16][LDL]
+  static constexpr int A_ONE = 3 * M16 * LDA + M16 * LDL;
+  static constexpr int A_BYTES = OPS_SMEM ? r16(2 * A_ONE * 4) : 0;
+  static constexpr int FM_BYTES = r16(NF * 2);
+  static constexpr int BAR_BYTES = 4 * S * 8;
+  static constexpr size_t SMEM_BYTES = size_t(S) * SLOT + A_BYTES + FM_BYTES + BAR_BYTES;
+  static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+  // global operator buffer (floats): hi [3][M16][KV] + [M16][KL], then lo (same shape)
+  static constexpr size_t OPS_ONE = size_t(3) * M16 * KV + size_t(M16) * KL;
+};
+
+__device__ __forceinline__ unsigned tf32_rna(float x) {
+  unsigned r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+// split x into tf32 hi + tf32 lo
+__device__ __forceinline__ void tf32_split(float x, unsigned& hi, unsigned& lo) {
+  hi = tf32_rna(x);
+  lo = tf32_rna(x - __uint_as_float(hi));
+}
+__device__ __forceinline__ void hmma_tf32(float (&c)[4], const unsigned (&a)[4], unsigned b0, unsigned b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// 3xTF32: c += Ahi.Bhi + Ahi.Blo + Alo.Bhi
+__device__ __forceinline__ void mma3(float (&c)[4], const unsigned (&ah)[4], const unsigned (&al)[4], unsigned bh0,
+                                     unsigned bh1, unsigned bl0, unsigned bl1) {
+  hmma_tf32(c, al, bh0, bh1);
+  hmma_tf32(c, ah, bl0, bl1);
+  hmma_tf32(c, ah, bh0, bh1);
+}
+
+template <int N, bool UPDATE>
+__global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
+    dg_stage_ws32(const StageParams<float> p, const float* __restrict__ opsA, int64_t t_begin, int64_t t_count) {
+  using C = Ws32Cfg<N>;
+  constexpr int Np = C::Np, Nfp = C::Nfp, NF = C::NF, M16 = C::M16, KV = C::KV, KL = C::KL;
+  constexpr int E = C::E, LD = C::LD, LDF = C::LDF, S = C::S, TS = C::TS;
+  extern __shared__ __align__(128) unsigned char smem_ws32[];
+  unsigned char* smem = smem_ws32;
+  float* sA = reinterpret_cast<float*>(smem + size_t(S) * C::SLOT);  // hi then lo
+  int16_t* sFm = reinterpret_cast<int16_t*>(smem + size_t(S) * C::SLOT + C::A_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(S) * C::SLOT + C::A_BYTES + C::FM_BYTES);
+  uint64_t* bar_load = bars;
+  uint64_t* bar_tr = bars + S;
+  uint64_t* bar_full = bars + 2 * S;
+  uint64_t* bar_empty = bars + 3 * S;
+  auto sU = [&](int s) { return reinterpret_cast<float*>(smem + size_t(s) * C::SLOT + C::OFF_U); };
+  auto sR = [&](int s) { return reinterpret_cast<float*>(smem + size_t(s) * C::SLOT + C::OFF_R); };
+  auto sG = [&](int s) { return reinterpret_cast<float*>(smem + size_t(s) * C::SLOT + C::OFF_G); };
+  auto sI = [&](int s) { return reinterpret_cast<int32_t*>(smem + size_t(s) * C::SLOT + C::OFF_I); };
+  auto sF = [&](int s) { return reinterpret_cast<float*>(smem + size_t(s) * C::SLOT + C::OFF_F); };
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool res_in = UPDATE && !p.first_stage;
+  const int64_t J = t_count > blockIdx.x ? (t_count - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int64_t kend = p.k_begin + p.K;
+  auto tile_of = [&](int64_t j) { return t_begin + blockIdx.x + j * gridDim.x; };
+  auto count_of = [&](int64_t tile) {
+    const int64_t k0 = tile * E;
+    return int(kend - k0 < E ? kend - k0 : E);
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(bar_load + s, 1);
+      mbar_init(bar_tr + s, C::PT);
+      mbar_init(bar_full + s, C::PT);
+      mbar_init(bar_empty + s, C::MW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int m = tid; m < NF; m += C::NT) sFm[m] = p.fmask[m];
+  if constexpr (C::OPS_SMEM) {
+    for (int h = 0; h < 2; ++h) {
+      const float* src = opsA + size_t(h) * C::OPS_ONE;
+      float* dst = sA + h * C::A_ONE;
+      for (int w = tid; w < 3 * M16 * KV; w += C::NT) {
+        const int r = w / KV, k = w - r * KV;
+        dst[r * C::LDA + k] = src[w];
+      }
+      for (int w = tid; w < M16 * KL; w += C::NT) {
+        const int r = w / KL, k = w - r * KL;
+        dst[3 * M16 * C::LDA + r * C::LDL + k] = src[3 * M16 * KV + w];
+      }
+    }
+  }
+  __syncthreads();
+
+  if (warp == C::MW) {
+    // ===================== TMA loader warp (one lane) =====================
+    if (lane == 0) {
+      for (int64_t j = 0; j < J; ++j) {
+        const int s = int(j % S);
+        mbar_wait(bar_empty + s, (unsigned(j / S) & 1) ^ 1);
+        const int64_t tile = tile_of(j);
+        unsigned bytes = TS * 4 + C::GEOT * 4 + C::IDXT * 4;
+        if (C::RES_SMEM && res_in) bytes += TS * 4;
+        mbar_arrive_tx(bar_load + s, bytes);
+        bulk_g2s(sU(s), p.u_in + tile * TS, TS * 4, bar_load + s);
+        if (C::RES_SMEM && res_in) bulk_g2s(sR(s), p.res + tile * TS, TS * 4, bar_load + s);
+        bulk_g2s(sG(s), p.geo + tile * C::GEOT, C::GEOT * 4, bar_load + s);
+        bulk_g2s(sI(s), p.gidx + tile * C::IDXT, C::IDXT * 4, bar_load + s);
+      }
+    }
+  } else if (warp > C::MW) {
+    // ============================ flux warps ============================
+    const int ptid = tid - 32 * (C::MW + 1);
+    auto traces = [&](int64_t j) {
+      const int s = int(j % S);
+      mbar_wait(bar_load + s, unsigned(j / S) & 1);
+      const int32_t* I = sI(s);
+      float* F = sF(s);
+      for (int w = ptid; w < E * NF; w += C::PT) {
+        const int32_t gi = I[w];
+        if (gi >= 0) {
+          const int e = w / NF, m = w - e * NF;
+          const bool ghost = gi >= p.ghost_base;
+          const float* src = p.u_in + gi;
+          const int cb = 24 * (e >> 2) + 2 * (e & 3);
+#pragma unroll
+          for (int c = 0; c < 6; ++c) {
+            const int co = 8 * (c >> 1) + (c & 1);
+            cp_async4(F + (cb + co) * LDF + m, src + (ghost ? c * Nfp : co * LD));
+          }
+        }
+      }
+      cp_async_mbar_arrive(bar_tr + s);
+    };
+    auto flux = [&](int64_t j) {
+      const int s = int(j % S);
+      mbar_wait(bar_tr + s, unsigned(j / S) & 1);
+      const int ne = count_of(tile_of(j));
+      const float* U = sU(s);
+      const float* Gm = sG(s);
+      const int32_t* I = sI(s);
+      float* F = sF(s);
+      for (int w = ptid; w < E * NF; w += C::PT) {
+        const int e = w / NF, m = w - e * NF, f = m / Nfp;
+        const int cb = 24 * (e >> 2) + 2 * (e & 3);
+        float fl[6] = {0, 0, 0, 0, 0, 0};
+        if (e < ne) {
+          const float* g = Gm + e * GEO_W + 9 + 4 * f;
+          const float nx = g[0], ny = g[1], nz = g[2], fs = g[3];
+          const int nM = sFm[m];
+          float uM[6], dE[3], dH[3];
+#pragma unroll
+          for (int c = 0; c < 6; ++c) uM[c] = U[(cb + 8 * (c >> 1) + (c & 1)) * LD + nM];
+          if (I[w] >= 0) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              dE[c] = F[(cb + 8 * (c >> 1) + (c & 1)) * LDF + m] - uM[c];
+              dH[c] = F[(cb + 8 * ((c + 3) >> 1) + ((c + 3) & 1)) * LDF + m] - uM[c + 3];
+            }
+          } else {  // PEC wall: E+ = -E-, H+ = H-
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              dE[c] = -2.0f * uM[c];
+              dH[c] = 0.0f;
+            }
+          }
+          maxwell_flux<float>(nx, ny, nz, p.alpha, dE, dH, fl);
+          const float sc = fs * 0.5f;
+#pragma unroll
+          for (int c = 0; c < 6; ++c) fl[c] *= sc;
+        }
+#pragma unroll
+        for (int c = 0; c < 6; ++c) F[(cb + 8 * (c >> 1) + (c & 1)) * LDF + m] = fl[c];
+      }
+      // zero the K padding of the face buffer (lift K = KL >= NF)
+      if constexpr (KL > NF) {
+        for (int w = ptid; w < 6 * E * (KL - NF); w += C::PT) {
+          const int col = w / (KL - NF), k = NF + (w - col * (KL - NF));
+          F[col * LDF + k] = 0.0f;
+        }
+      }
+      mbar_arrive(bar_full + s);
+    };
+    for (int64_t t = 0; t < C::LA && t < J; ++t) traces(t);
+    for (int64_t j = 0; j < J; ++j) {
+      if (C::LA == 0) {
+        traces(j);
+        flux(j);
+      } else {
+        flux(j);
+        if (j + C::LA < J) traces(j + C::LA);
+      }
+    }
+  } else {
+    // ============================= MMA warps =============================
+    const int gid = lane >> 2, tig = lane & 3;
+    const int64_t total = J * C::T;
+    int64_t released = 0, waited = -1;
+    auto release = [&](int64_t jj) {
+      if (waited < jj) {
+        mbar_wait(bar_full + int(jj % S), unsigned(jj / S) & 1);
+        waited = jj;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_empty + int(jj % S));
+    };
+    const float* Ahi = C::OPS_SMEM ? sA : opsA;
+    const float* Alo = C::OPS_SMEM ? sA + C::A_ONE : opsA + C::OPS_ONE;
+    constexpr int lda = C::OPS_SMEM ? C::LDA : KV;
+    constexpr int ldl = C::OPS_SMEM ? C::LDL : KL;
+    constexpr int l0 = 3 * M16 * lda;  // LIFT offset within an operator copy
+    auto ldA = [&](const float* base, int idx) -> float {
+      if constexpr (C::OPS_SMEM)
+        return base[idx];
+      else
+        return __ldg(base + idx);
+    };
+    for (int64_t q = warp; q < total; q += C::MW) {
+      const int64_t j = q / C::T;
+      const int task = int(q - j * C::T);
+      while (released < j) release(released++);
+      const int s = int(j % S);
+      if (waited < j) {
+        mbar_wait(bar_full + s, unsigned(j / S) & 1);
+        waited = j;
+      }
+      const int64_t tile = tile_of(j);
+      const int ne = count_of(tile);
+      const int t = task % C::MT, g = task / C::MT;
+      const int r0 = 16 * t + gid;  // rows r0 and r0 + 8
+      const float* U = sU(s);
+      const float* F = sF(s);
+      float acc[3][3][4];
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int nt = 0; nt < 3; ++nt) acc[b][nt][0] = acc[b][nt][1] = acc[b][nt][2] = acc[b][nt][3] = 0.0f;
+      const float* bp = U + (24 * g + gid) * LD + tig;
+#pragma unroll 2
+      for (int kk = 0; kk < KV; kk += 8) {
+        unsigned bh[3][2], bl[3][2];
+#pragma unroll
+        for (int nt = 0; nt < 3; ++nt) {
+          tf32_split(bp[nt * 8 * LD + kk], bh[nt][0], bl[nt][0]);
+          tf32_split(bp[nt * 8 * LD + kk + 4], bh[nt][1], bl[nt][1]);
+        }
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          const int rb = b * M16 + r0;
+          unsigned ah[4], al[4];
+          ah[0] = __float_as_uint(ldA(Ahi, rb * lda + kk + tig));
+          ah[1] = __float_as_uint(ldA(Ahi, (rb + 8) * lda + kk + tig));
+          ah[2] = __float_as_uint(ldA(Ahi, rb * lda + kk + tig + 4));
+          ah[3] = __float_as_uint(ldA(Ahi, (rb + 8) * lda + kk + tig + 4));
+          al[0] = __float_as_uint(ldA(Alo, rb * lda + kk + tig));
+          al[1] = __float_as_uint(ldA(Alo, (rb + 8) * lda + kk + tig));
+          al[2] = __float_as_uint(ldA(Alo, rb * lda + kk + tig + 4));
+          al[3] = __float_as_uint(ldA(Alo, (rb + 8) * lda + kk + tig + 4));
+#pragma unroll
+          for (int nt = 0; nt < 3; ++nt) mma3(acc[b][nt], ah, al, bh[nt][0], bh[nt][1], bl[nt][0], bl[nt][1]);
+        }
+      }
+      // chain rule + curl for rows r0 (h=0) and r0+8 (h=1), element 4g+tig
+      float r[3][4];
+      {
+        const float* Gm = sG(s) + (4 * g + tig) * GEO_W;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float dx[6], dy[6], dz[6];
+#pragma unroll
+          for (int c = 0; c < 6; ++c) {
+            const int i = 2 * h + (c & 1);
+            const float ur = acc[0][c >> 1][i], us = acc[1][c >> 1][i], ut = acc[2][c >> 1][i];
+            dx[c] = Gm[0] * ur + Gm[3] * us + Gm[6] * ut;
+            dy[c] = Gm[1] * ur + Gm[4] * us + Gm[7] * ut;
+            dz[c] = Gm[2] * ur + Gm[5] * us + Gm[8] * ut;
+          }
+          r[0][2 * h + 0] = dy[5] - dz[4];
+          r[0][2 * h + 1] = dz[3] - dx[5];
+          r[1][2 * h + 0] = dx[4] - dy[3];
+          r[1][2 * h + 1] = -(dy[2] - dz[1]);
+          r[2][2 * h + 0] = -(dz[0] - dx[2]);
+          r[2][2 * h + 1] = -(dx[1] - dy[0]);
+        }
+      }
+      // lift: r += LIFT . Flux  (3xTF32)
+      const float* fp = F + (24 * g + gid) * LDF + tig;
+#pragma unroll 2
+      for (int kk = 0; kk < KL; kk += 8) {
+        unsigned ah[4], al[4];
+        ah[0] = __float_as_uint(ldA(Ahi, l0 + r0 * ldl + kk + tig));
+        ah[1] = __float_as_uint(ldA(Ahi, l0 + (r0 + 8) * ldl + kk + tig));
+        ah[2] = __float_as_uint(ldA(Ahi, l0 + r0 * ldl + kk + tig + 4));
+        ah[3] = __float_as_uint(ldA(Ahi, l0 + (r0 + 8) * ldl + kk + tig + 4));
+        al[0] = __float_as_uint(ldA(Alo, l0 + r0 * ldl + kk + tig));
+        al[1] = __float_as_uint(ldA(Alo, l0 + (r0 + 8) * ldl + kk + tig));
+        al[2] = __float_as_uint(ldA(Alo, l0 + r0 * ldl + kk + tig + 4));
+        al[3] = __float_as_uint(ldA(Alo, l0 + (r0 + 8) * ldl + kk + tig + 4));
+#pragma unroll
+        for (int nt = 0; nt < 3; ++nt) {
+          unsigned bh0, bl0, bh1, bl1;
+          tf32_split(fp[nt * 8 * LDF + kk], bh0, bl0);
+          tf32_split(fp[nt * 8 * LDF + kk + 4], bh1, bl1);
+          mma3(r[nt], ah, al, bh0, bh1, bl0, bl1);
+        }
+      }
+      // LSERK update / RHS store (tiled layout), rows r0 and r0+8
+      const int e = 4 * g + tig;
+      if (e < ne) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int row = r0 + 8 * h;
+          if (row < Np) {
+            const int64_t tb = tile * TS + row;
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+              const int col = 24 * g + 8 * (c >> 1) + 2 * tig + (c & 1);
+              const int64_t idx = tb + int64_t(col) * LD;
+              const float rhs = r[c >> 1][2 * h + (c & 1)];
+              if (UPDATE) {
+                float rold = 0.0f;
+                if (res_in) rold = C::RES_SMEM ? sR(s)[col * LD + row] : p.res[idx];
+                const float rr = p.rk_a * rold + p.dt * rhs;
+                p.res[idx] = rr;
+                p.u_out[idx] = U[col * LD + row] + p.rk_b * rr;
+              } else {
+                p.rhs_out[idx] = rhs;
+              }
+            }
+          }
+        }
+      }
+    }
+    while (released < J) release(released++);
+  }
+}
+
+template <int N>
+void launch_stage_ws32(const StageParams<float>& p, const float* opsA, int mode, cudaStream_t st) {
+  using C = Ws32Cfg<N>;
+  static int sms = 0;
+  if (!sms) {
+    cudaFuncSetAttribute(dg_stage_ws32<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+    cudaFuncSetAttribute(dg_stage_ws32<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if (p.K <= 0) return;
+  const int64_t t0 = p.k_begin / C::E;
+  const int64_t tc = (p.k_begin + p.K + C::E - 1) / C::E - t0;
+  const unsigned grid = unsigned(tc < sms ? tc : sms);
+  if (mode == 1)
+    dg_stage_ws32<N, true><<<grid, C::NT, C::SMEM_BYTES, st>>>(p, opsA, t0, tc);
+  else
+    dg_stage_ws32<N, false><<<grid, C::NT, C::SMEM_BYTES, st>>>(p, opsA, t0, tc);
+}
+
+template <int N>
+TileLayout ws32_layout() {
+  using C = Ws32Cfg<N>;
+  TileLayout L;
+  L.E = C::E;
+  L.LD = C::LD;
+  L.perm = 1;
+  L.TS = C::TS;
+  return L;
+}
+
+// host: padded 3xTF32 operator buffer (hi then lo), from row-major FP64 Dr|Ds|Dt ([Np][Np]) and LIFT ([Np][4Nfp])
+template <int N>
+void ws32_ops(const double* Dr, const double* Ds, const double* Dt, const double* LIFT, float* out) {
+  using C = Ws32Cfg<N>;
+  constexpr int Np = C::Np, NF = C::NF, M16 = C::M16, KV = C::KV, KL = C::KL;
+  auto tf32 = [](double v) -> float {  // round-to-nearest into 10 explicit mantissa bits (matches cvt.rna)
+    float f = float(v);
+    unsigned u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7f800000u) != 0x7f800000u) {
+      u += 0x1000u;
+      u &= 0xffffe000u;
+    }
+    float r;
+    std::memcpy(&r, &u, 4);
+    return r;
+  };
+  for (size_t i = 0; i < 2 * C::OPS_ONE; ++i) out[i] = 0.0f;
+  const double* D[3] = {Dr, Ds, Dt};
+  for (int b = 0; b < 3; ++b)
+    for (int i = 0; i < Np; ++i)
+      for (int k = 0; k < Np; ++k) {
+        const double v = D[b][i * Np + k];
+        const float hi = tf32(v);
+        out[(size_t(b) * M16 + i) * KV + k] = hi;
+        out[C::OPS_ONE + (size_t(b) * M16 + i) * KV + k] = tf32(v - double(hi));
+      }
+  for (int i = 0; i < Np; ++i)
+    for (int k = 0; k < NF; ++k) {
+      const double v = LIFT[i * NF + k];
+      const float hi = tf32(v);
+      out[size_t(3) * M16 * KV + size_t(i) * KL + k] = hi;
+      out[C::OPS_ONE + size_t(3) * M16 * KV + size_t(i) * KL + k] = tf32(v - double(hi));
+    }
+}
+
+}  // namespace dg

@@ -52,8 +52,8 @@ def setup(key, VX, E, N):
     return _SETUPS[k]
 
 
-VARIANTS = [(8, 1), (8, 2), (8, 3), (4, 1)]   # (precision, variant): FP64 BASIC, MMA, MMA_WS (DMMA), FP32 BASIC
-VIDS = ["f64-basic", "f64-mma", "f64-ws", "f32-basic"]
+VARIANTS = [(8, 1), (8, 2), (8, 3), (4, 1), (4, 3)]  # FP64 BASIC, MMA, MMA_WS (DMMA); FP32 BASIC, MMA_WS (3xTF32)
+VIDS = ["f64-basic", "f64-mma", "f64-ws", "f32-basic", "f32-ws"]
 
 
 @pytest.mark.parametrize("prec,variant", VARIANTS, ids=VIDS)
