@@ -71,8 +71,10 @@ typedef enum {
   DG_VARIANT_BASIC = 1,  /* one fused element-tile kernel per stage, FMA contractions */
   DG_VARIANT_MMA = 2,    /* FP64: DMMA contractions, cp.async-pipelined persistent kernel
                             (FP32: same as BASIC) */
-  DG_VARIANT_MMA_WS = 3  /* warp-specialized TMA/mbarrier pipeline; contractions on tensor
+  DG_VARIANT_MMA_WS = 3, /* warp-specialized TMA/mbarrier pipeline; contractions on tensor
                             cores: FP64 DMMA, FP32 3xTF32 HMMA */
+  DG_VARIANT_TC = 4      /* FP32, N <= 4: tcgen05.mma kind::tf32 (3xTF32) with TMEM
+                            accumulators (5th-generation tensor cores) */
 } dg_variant;
 
 typedef struct {

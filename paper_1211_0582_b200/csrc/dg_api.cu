@@ -335,10 +335,14 @@ dg_status upload_setup(dg_solver* s) {
   const int64_t Kl = P.K_local;
   s->Kl = Kl;
   const bool ws = s->variant == DG_VARIANT_AUTO || s->variant == DG_VARIANT_MMA_WS;
+  const bool tc = sizeof(T) == 4 && s->variant == DG_VARIANT_TC;
   if (sizeof(T) == 8 && ws) {
     s->lay = dg::ws_layout_f64(s->N);
   } else if (sizeof(T) == 4 && ws) {
     s->lay = dg::ws32_layout_f32(s->N);
+  } else if (tc) {
+    s->lay = dg::tc_layout_f32(s->N);
+    if (Kl >= (int64_t(1) << 22)) return fail(DG_ERR_ARG, "TC variant: more than 2^22 local elements");
   } else {
     s->lay = dg::TileLayout();
     s->lay.E = 1;
@@ -404,10 +408,15 @@ dg_status upload_setup(dg_solver* s) {
     CK(cudaMalloc(&s->d_ops_pad, pad.size() * wb));
     CK(cudaMemcpy(s->d_ops_pad, pad.data(), pad.size() * wb, cudaMemcpyHostToDevice));
   } else {
-    // FP32 3xTF32: hi/lo split operators, zero-padded (stage_ws32.cuh)
-    std::vector<float> pad(dg::ws32_ops_count(s->N));
-    dg::ws32_ops_build(s->N, s->ref.Dr.a.data(), s->ref.Ds.a.data(), s->ref.Dt.a.data(), s->ref.LIFT.a.data(),
+    // FP32 3xTF32: hi/lo split operators, zero-padded (stage_ws32.cuh / stage_tc.cuh)
+    const bool tcv = s->lay.perm == 2;
+    std::vector<float> pad(tcv ? dg::tc_ops_count(s->N) : dg::ws32_ops_count(s->N));
+    if (tcv)
+      dg::tc_ops_build(s->N, s->ref.Dr.a.data(), s->ref.Ds.a.data(), s->ref.Dt.a.data(), s->ref.LIFT.a.data(),
                        pad.data());
+    else
+      dg::ws32_ops_build(s->N, s->ref.Dr.a.data(), s->ref.Ds.a.data(), s->ref.Dt.a.data(), s->ref.LIFT.a.data(),
+                         pad.data());
     CK(cudaMalloc(&s->d_ops_pad, pad.size() * sizeof(float)));
     CK(cudaMemcpy(s->d_ops_pad, pad.data(), pad.size() * sizeof(float), cudaMemcpyHostToDevice));
   }
@@ -420,7 +429,9 @@ dg_status upload_setup(dg_solver* s) {
     std::vector<int32_t> sidx(size_t(P.n_ghost_faces) * Nfp);
     for (int64_t g = 0; g < P.n_ghost_faces; ++g)
       for (int j = 0; j < Nfp; ++j)
-        sidx[g * Nfp + j] = int32_t(s->lay.off(P.send_elem[g], 0, s->ref.Fmask[P.send_face[g] * Nfp + j]));
+        sidx[g * Nfp + j] = s->lay.perm == 2
+                                ? int32_t((P.send_elem[g] << 8) | s->ref.Fmask[P.send_face[g] * Nfp + j])
+                                : int32_t(s->lay.off(P.send_elem[g], 0, s->ref.Fmask[P.send_face[g] * Nfp + j]));
     CK(cudaMalloc((void**)&s->d_sidx, sidx.size() * sizeof(int32_t)));
     CK(cudaMemcpy(s->d_sidx, sidx.data(), sidx.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   }
@@ -534,7 +545,9 @@ dg_status dg_create(const dg_config* cfg, dg_solver** out) {
   if (cfg->order < 1 || cfg->order > 9) return fail(DG_ERR_ORDER, "order N must be in 1..9");
   if (cfg->precision != 4 && cfg->precision != 8) return fail(DG_ERR_ARG, "precision must be 4 or 8");
   if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return fail(DG_ERR_ARG, "bad rank/nranks");
-  if (cfg->variant < 0 || cfg->variant > 3) return fail(DG_ERR_ARG, "bad variant");
+  if (cfg->variant < 0 || cfg->variant > 4) return fail(DG_ERR_ARG, "bad variant");
+  if (cfg->variant == DG_VARIANT_TC && (cfg->precision != 4 || cfg->order > 4))
+    return fail(DG_ERR_ARG, "DG_VARIANT_TC is the FP32 tcgen05 kernel for N <= 4");
   std::unique_ptr<dg_solver> s(new dg_solver());
   s->cfg = *cfg;
   s->N = cfg->order;

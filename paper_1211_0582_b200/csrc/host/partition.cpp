@@ -81,7 +81,10 @@ void build_gather_index(const RefElem& ref, const MeshData& m, const Partition& 
       for (int i = 0; i < Nfp; ++i) {
         const int j = m.fperm[code * Nfp + i];  // neighbour face-node position
         int64_t v;
-        if (g >= 0)
+        if (L.perm == 2)
+          v = g >= 0 ? (TileLayout::GHOST_FLAG | (g * 6 * Nfp + j))
+                     : ((P.g2l[k2] << 8) | ref.Fmask[f2 * Nfp + j]);
+        else if (g >= 0)
           v = ghost_base + g * 6 * Nfp + j;
         else
           v = L.off(P.g2l[k2], 0, ref.Fmask[f2 * Nfp + j]);

@@ -18,11 +18,19 @@ __global__ void k_cm_to_tiles(const S* __restrict__ src, T* __restrict__ dst, in
   for (int64_t w = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; w < total; w += int64_t(gridDim.x) * blockDim.x) {
     const int64_t t = w / L.TS;
     const int64_t r = w - t * L.TS;
-    const int col = int(r / L.LD), n = int(r - int64_t(col) * L.LD);
+    int col, n;
+    if (L.perm == 2) {  // inverse of the core-matrix placement
+      const int chunk = int(r >> 5), q = int(r & 31), kc = L.LD >> 2;
+      col = (chunk / kc) * 8 + (q >> 2);
+      n = (chunk % kc) * 4 + (q & 3);
+    } else {
+      col = int(r / L.LD);
+      n = int(r - int64_t(col) * L.LD);
+    }
     T v = T(0);
     if (col < cols && n < Np) {
       int e, c;
-      if (L.perm) {
+      if (L.perm == 1) {
         const int g = col / 24, q = col - 24 * g, nt = q >> 3, rr = q & 7;
         e = 4 * g + (rr >> 1);
         c = 2 * nt + (rr & 1);
@@ -88,7 +96,8 @@ __global__ void k_pack_traces(const T* __restrict__ u, T* __restrict__ buf, cons
     const int64_t g = w / (6 * Nfp);
     const int r = int(w - g * 6 * Nfp);
     const int c = r / Nfp, j = r - c * Nfp;
-    buf[w] = u[sidx[g * Nfp + j] + int64_t(L.coff(c)) * L.LD];
+    const int32_t si = sidx[g * Nfp + j];
+    buf[w] = L.perm == 2 ? u[L.off(si >> 8, c, si & 255)] : u[si + int64_t(L.coff(c)) * L.LD];
   }
 }
 

@@ -20,6 +20,9 @@ void launch_stage_f32_N5(const StageParams<float>& p, int mode, int variant, voi
 }
 
 TileLayout ws32_layout_N5() { return ws32_layout<5>(); }
+TileLayout tc_layout_N5() { return TileLayout{}; }  // TC covers N <= 4
+size_t tc_ops_count_N5() { return 0; }
+void tc_ops_N5(const double*, const double*, const double*, const double*, float*) {}
 size_t ws32_ops_count_N5() { return 2 * Ws32Cfg<5>::OPS_ONE; }
 void ws32_ops_N5(const double* Dr, const double* Ds, const double* Dt, const double* L, float* out) {
   ws32_ops<5>(Dr, Ds, Dt, L, out);

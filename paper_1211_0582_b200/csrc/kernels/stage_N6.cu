@@ -20,6 +20,9 @@ void launch_stage_f32_N6(const StageParams<float>& p, int mode, int variant, voi
 }
 
 TileLayout ws32_layout_N6() { return ws32_layout<6>(); }
+TileLayout tc_layout_N6() { return TileLayout{}; }  // TC covers N <= 4
+size_t tc_ops_count_N6() { return 0; }
+void tc_ops_N6(const double*, const double*, const double*, const double*, float*) {}
 size_t ws32_ops_count_N6() { return 2 * Ws32Cfg<6>::OPS_ONE; }
 void ws32_ops_N6(const double* Dr, const double* Ds, const double* Dt, const double* L, float* out) {
   ws32_ops<6>(Dr, Ds, Dt, L, out);

@@ -20,6 +20,9 @@ void launch_stage_f32_N7(const StageParams<float>& p, int mode, int variant, voi
 }
 
 TileLayout ws32_layout_N7() { return ws32_layout<7>(); }
+TileLayout tc_layout_N7() { return TileLayout{}; }  // TC covers N <= 4
+size_t tc_ops_count_N7() { return 0; }
+void tc_ops_N7(const double*, const double*, const double*, const double*, float*) {}
 size_t ws32_ops_count_N7() { return 2 * Ws32Cfg<7>::OPS_ONE; }
 void ws32_ops_N7(const double* Dr, const double* Ds, const double* Dt, const double* L, float* out) {
   ws32_ops<7>(Dr, Ds, Dt, L, out);

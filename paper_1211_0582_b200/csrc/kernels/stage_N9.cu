@@ -20,6 +20,9 @@ void launch_stage_f32_N9(const StageParams<float>& p, int mode, int variant, voi
 }
 
 TileLayout ws32_layout_N9() { return ws32_layout<9>(); }
+TileLayout tc_layout_N9() { return TileLayout{}; }  // TC covers N <= 4
+size_t tc_ops_count_N9() { return 0; }
+void tc_ops_N9(const double*, const double*, const double*, const double*, float*) {}
 size_t ws32_ops_count_N9() { return 2 * Ws32Cfg<9>::OPS_ONE; }
 void ws32_ops_N9(const double* Dr, const double* Ds, const double* Dt, const double* L, float* out) {
   ws32_ops<9>(Dr, Ds, Dt, L, out);

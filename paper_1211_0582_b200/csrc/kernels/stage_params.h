@@ -30,22 +30,33 @@ constexpr int GEO_W = 26;  // 25 used (rx..tz, 4 x (n, Fscale)); padded to 16 B 
 // Field layout in device memory: element k, component c, node n lives at
 //   (k / E) * TS + col(k % E, c) * LD + n.
 // BASIC/MMA kernels: E = 1, LD = Np, TS = ES, col = c        -> k*ES + c*Np + n
-// WS kernel:         E = tile, LD = padded K extent, TS = 6*E*LD, col = the
-//                    MMA column permutation (the tile is the smem image of the
-//                    B operand, so one bulk copy moves it).  Padding is zero.
+// WS kernels:        perm = 1: E = tile, LD = padded K extent, TS = 6*E*LD,
+//                    col = the MMA column permutation (the tile is the smem image
+//                    of the mma.sync B operand, so one bulk copy moves it).
+// TC kernel:         perm = 2: the tile is the tcgen05 K-major SWIZZLE_NONE
+//                    canonical image of the B operand: column col = 6e + c, node n
+//                    in core matrix (col/8, n/4) of 8 rows x 4 words:
+//                    ((col/8)*(LD/4) + n/4)*32 + (col%8)*4 + n%4.
+// Padding (rows n >= Np, absent elements) is zero in every layout.
 struct TileLayout {
   int E = 1;
   int LD = 0;
   int perm = 0;
   int64_t TS = 0;
   DG_HD int col(int e, int c) const {
-    return perm ? 24 * (e >> 2) + 8 * (c >> 1) + 2 * (e & 3) + (c & 1) : 6 * e + c;
+    return perm == 1 ? 24 * (e >> 2) + 8 * (c >> 1) + 2 * (e & 3) + (c & 1) : 6 * e + c;
   }
-  DG_HD int coff(int c) const { return perm ? 8 * (c >> 1) + (c & 1) : c; }  // col(e,c) - col(e,0)
-  DG_HD int64_t off(int64_t k, int c, int n) const {
-    return (k / E) * TS + int64_t(col(int(k % E), c)) * LD + n;
+  DG_HD int coff(int c) const { return perm == 1 ? 8 * (c >> 1) + (c & 1) : c; }  // perm 0/1: col(e,c) - col(e,0)
+  DG_HD int64_t inner(int cl, int n) const {  // word offset of (column, node) inside a tile
+    return perm == 2 ? int64_t(((cl >> 3) * (LD >> 2) + (n >> 2)) * 32 + (cl & 7) * 4 + (n & 3))
+                     : int64_t(cl) * LD + n;
   }
+  DG_HD int64_t off(int64_t k, int c, int n) const { return (k / E) * TS + inner(col(int(k % E), c), n); }
   DG_HD int64_t ntiles(int64_t K) const { return (K + E - 1) / E; }
+  // gather-index encoding: perm 0/1 store off(k2, 0, n2) (+ coff(c)*LD per component);
+  // perm 2 stores (k2 << 8) | n2 and the kernel evaluates off() per component.
+  // Ghost records are ghost_base + rec (perm 0/1) or GHOST_FLAG | rec (perm 2).
+  static constexpr int32_t GHOST_FLAG = int32_t(1) << 30;
 };
 
 template <typename T>
@@ -77,6 +88,9 @@ TileLayout ws_layout_f64(int N);   // tiled layout of the FP64 WS kernel for ord
 TileLayout ws32_layout_f32(int N); // tiled layout of the FP32 (3xTF32) WS kernel
 size_t ws32_ops_count(int N);      // floats in its split hi/lo operator buffer
 void ws32_ops_build(int N, const double* Dr, const double* Ds, const double* Dt, const double* LIFT, float* out);
+TileLayout tc_layout_f32(int N);   // tcgen05 (TC) kernel layout, N <= 4 (E = 0 otherwise)
+size_t tc_ops_count(int N);
+void tc_ops_build(int N, const double* Dr, const double* Ds, const double* Dt, const double* LIFT, float* out);
 StageLauncher<float> stage_launcher_f32(int N);
 
 }  // namespace dg

@@ -52,13 +52,19 @@ def setup(key, VX, E, N):
     return _SETUPS[k]
 
 
-VARIANTS = [(8, 1), (8, 2), (8, 3), (4, 1), (4, 3)]  # FP64 BASIC, MMA, MMA_WS (DMMA); FP32 BASIC, MMA_WS (3xTF32)
-VIDS = ["f64-basic", "f64-mma", "f64-ws", "f32-basic", "f32-ws"]
+VARIANTS = [(8, 1), (8, 2), (8, 3), (4, 1), (4, 3), (4, 4)]  # FP64 BASIC, MMA, MMA_WS (DMMA); FP32 BASIC, MMA_WS (3xTF32 HMMA), TC (tcgen05)
+VIDS = ["f64-basic", "f64-mma", "f64-ws", "f32-basic", "f32-ws", "f32-tc"]
+
+
+def supported(N, prec, variant):
+    if variant == 4 and N > 4:
+        pytest.skip("the tcgen05 TC kernel covers N <= 4")
 
 
 @pytest.mark.parametrize("prec,variant", VARIANTS, ids=VIDS)
 @pytest.mark.parametrize("N", range(1, 10))
 def test_rhs_random_fields_shuffled_jittered(N, prec, variant):
+    supported(N, prec, variant)
     VX, E = mesh(3, 1, 2, 3)                      # K = 162: ragged tail for every tile size
     st = setup("m3", VX, E, N)
     U = di.random_fields(st.K, N, seed=0)
@@ -99,6 +105,7 @@ def test_c1_cavity_100_steps(prec):
 @pytest.mark.parametrize("prec,variant", VARIANTS, ids=VIDS)
 @pytest.mark.parametrize("N", range(1, 10))
 def test_lserk_steps_all_orders(N, prec, variant):
+    supported(N, prec, variant)
     VX, E = mesh(2, 5, 6, 7)
     st = setup("m2", VX, E, N)
     U0 = di.random_fields(st.K, N, seed=1)
@@ -174,6 +181,7 @@ def test_bench_mesh_full_size(N, prec):
 @pytest.mark.parametrize("prec,variant", VARIANTS, ids=VIDS)
 @pytest.mark.parametrize("N", range(1, 10))
 def test_many_tiles_per_cta_shuffled(N, prec, variant):
+    supported(N, prec, variant)
     # K = 10368 on a shuffled/rotated/jittered mesh: the persistent MMA kernel runs
     # several element tiles per CTA (exercises its cp.async double buffering)
     VX, E = mesh(12, 21, 22, 23)

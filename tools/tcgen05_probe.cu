@@ -12,7 +12,7 @@
 #include <cstring>
 #include <vector>
 
-constexpr int M = 128;
+constexpr int M = 128;  // rows of the A buffers (the M=64 probe uses the first 64)
 
 __device__ __forceinline__ unsigned su32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 
@@ -39,7 +39,7 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int m, int n) {
          | (uint32_t(m >> 4) << 24);// M / 16
 }
 
-template <int N, int K, int PASSES>
+template <int N, int K, int PASSES, int MM = 128>
 __global__ void probe(const float* A, const float* Alo, const float* B, const float* Blo, float* D) {
   extern __shared__ __align__(1024) unsigned char sm[];
   float* sA = reinterpret_cast<float*>(sm);
@@ -73,7 +73,7 @@ __global__ void probe(const float* A, const float* Alo, const float* B, const fl
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base;
   if (tid == 0) {
-    const uint32_t idesc = idesc_tf32(M, N);
+    const uint32_t idesc = idesc_tf32(MM, N);
     for (int pass = 0; pass < PASSES; ++pass) {
       const float* a = pass == 1 ? sAl : sA;  // pass 0: A.B, 1: Alo.B, 2: A.Blo
       const float* b = pass == 2 ? sBl : sB;
@@ -179,7 +179,44 @@ void run() {
   cudaFree(dA); cudaFree(dB); cudaFree(dAl); cudaFree(dBl); cudaFree(dD);
 }
 
+// M=64: which TMEM lanes hold which rows?  Reads all 128 lanes and matches them to rows.
+void run_m64() {
+  constexpr int N = 48, K = 40;
+  std::vector<float> A(M * K), B(N * K), Z(M * K, 0.0f), D(M * N);
+  unsigned s = 777;
+  auto rnd = [&]() { s = s * 1664525u + 1013904223u; return (float((s >> 8) & 0xffff) / 65536.0f) * 2.0f - 1.0f; };
+  for (auto& x : A) x = rnd();
+  for (auto& x : B) x = rnd();
+  float *dA, *dB, *dZ, *dD;
+  cudaMalloc(&dA, A.size() * 4); cudaMalloc(&dB, B.size() * 4); cudaMalloc(&dZ, Z.size() * 4); cudaMalloc(&dD, D.size() * 4);
+  cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(dZ, Z.data(), Z.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemset(dD, 0, D.size() * 4);
+  const int smem = (2 * M * K + 2 * N * K) * 4;
+  cudaFuncSetAttribute(probe<N, K, 1, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  probe<N, K, 1, 64><<<1, 128, smem>>>(dA, dZ, dB, dZ, dD);
+  cudaError_t e = cudaDeviceSynchronize();
+  cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost);
+  printf("{\"M\": 64, \"err\": \"%s\", \"lane_to_row\": [", cudaGetErrorString(e));
+  for (int lane = 0; lane < 128; ++lane) {
+    int match = -1;
+    for (int m = 0; m < 64 && match < 0; ++m) {
+      double md = 0;
+      for (int n = 0; n < N; ++n) {
+        double r = 0;
+        for (int k = 0; k < K; ++k) r += double(trunc_tf32(A[m * K + k])) * trunc_tf32(B[n * K + k]);
+        md = std::fmax(md, std::fabs(r - D[lane * N + n]));
+      }
+      if (md < 1e-4) match = m;
+    }
+    printf("%s%d", lane ? "," : "", match);
+  }
+  printf("]}\n");
+}
+
 int main() {
+  run_m64();
   run<96, 40>();
   run<144, 40>();
   run<256, 64>();
