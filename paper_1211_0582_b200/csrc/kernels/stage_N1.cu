@@ -36,10 +36,13 @@ TileLayout ws_layout_N1() { return ws_layout<1>(); }
 
 #ifdef DG_WS_PROFILE
 void ws_prof_N1(unsigned long long* out, int reset) {
-  if (reset)
+  if (reset) {
     ws_prof_reset();
-  else
+    tc_prof_reset();
+  } else {
     ws_prof_read(out);
+    tc_prof_read(out + 16);  // TC-kernel counters follow the WS ones
+  }
 }
 #endif
 

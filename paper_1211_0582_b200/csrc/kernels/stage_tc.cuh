@@ -40,12 +40,14 @@ struct TcCfg {
   static constexpr int ML = 64;
   static constexpr int E = N <= 2 ? 16 : 8;       // 6E % 16 == 0
   static constexpr int COLS = 6 * E;
-  static constexpr int S = 2;                      // ring slots
-  static constexpr int LA = 0;                     // trace lookahead (S - 2)
-  static constexpr int PW = 4;                     // flux warps
+  static constexpr int S = N <= 3 ? 3 : 2;        // ring slots (smem budget)
+  static constexpr int LA = S - 2;                 // trace lookahead
+  static constexpr int PW = 8;                     // flux warps
+  static constexpr int EW = 8;                     // epilogue warps (two per TMEM lane quarter)
   static constexpr int W_LOAD = 0, W_FLUX0 = 1, W_MMA = 1 + PW, W_EPI0 = 2 + PW;
-  static constexpr int NT = 32 * (W_EPI0 + 4);
+  static constexpr int NT = 32 * (W_EPI0 + EW);
   static constexpr int PT = 32 * PW;
+  static constexpr int ET = 32 * EW;
   static constexpr int TS = COLS * KV;             // floats per field tile (B image)
   static constexpr int FS = COLS * KL;             // floats per face-buffer tile
   static constexpr int GEOT = E * GEO_W;
@@ -97,12 +99,29 @@ __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t da, uint64_t
 }
 __device__ __forceinline__ float tf32_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 
+#ifdef DG_WS_PROFILE
+// 0 load wait empty | 1 flux wait load | 2 flux traces issue | 3 flux wait traces | 4 flux compute | 5 flux lo-split
+// 6 mma wait full | 7 mma wait acc_empty | 8 mma issue | 9 epi wait acc_full | 10 epi pass1 | 11 epi pass2
+// 12 epi store+release | 13 tiles (lane-0 of epilogue warp 0)
+__device__ unsigned long long g_tc_prof[16];
+#define TC_T(v) long long v = clock64()
+#define TC_A(i, t0) \
+  do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_tc_prof[i], (unsigned long long)(clock64() - (t0))); } while (0)
+#else
+#define TC_T(v) \
+  do {          \
+  } while (0)
+#define TC_A(i, t0) \
+  do {              \
+  } while (0)
+#endif
+
 template <int N, bool UPDATE>
 __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
     dg_stage_tc(const StageParams<float> p, const float* __restrict__ opsA, int64_t t_begin, int64_t t_count) {
   using C = TcCfg<N>;
   constexpr int Np = C::Np, Nfp = C::Nfp, NF = C::NF, KV = C::KV, KL = C::KL, E = C::E, COLS = C::COLS;
-  constexpr int S = C::S, TS = C::TS, FS = C::FS;
+  constexpr int S = C::S, TS = C::TS;
   extern __shared__ __align__(1024) unsigned char smem_tc[];
   unsigned char* smem = smem_tc;
   auto sU = [&](int s) { return reinterpret_cast<float*>(smem + size_t(s) * C::SLOT + C::OFF_U); };
@@ -141,11 +160,11 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
       mbar_init(bar_load + s, 1);
       mbar_init(bar_tr + s, C::PT);
       mbar_init(bar_full + s, C::PT);
-      mbar_init(bar_empty + s, 4);  // epilogue warps
+      mbar_init(bar_empty + s, C::EW);  // epilogue warps
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(acc_full + a, 1);   // tcgen05.commit
-      mbar_init(acc_empty + a, 4);  // epilogue warps
+      mbar_init(acc_empty + a, C::EW);  // epilogue warps
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -169,7 +188,9 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
     if (lane == 0) {
       for (int64_t j = 0; j < J; ++j) {
         const int s = int(j % S);
+        TC_T(t0);
         mbar_wait(bar_empty + s, (unsigned(j / S) & 1) ^ 1);
+        TC_A(0, t0);
         const int64_t tile = tile_of(j);
         unsigned bytes = TS * 4 + C::GEOT * 4 + C::IDXT * 4;
         if (res_in) bytes += TS * 4;
@@ -185,13 +206,16 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
     const int ptid = tid - 32 * C::W_FLUX0;
     auto traces = [&](int64_t j) {
       const int s = int(j % S);
+      TC_T(t0);
       mbar_wait(bar_load + s, unsigned(j / S) & 1);
+      TC_A(1, t0);
+      TC_T(t1);
       const int32_t* I = sI(s);
       float* F = sF(s);
-      for (int w = ptid; w < E * NF; w += C::PT) {
-        const int32_t gi = I[w];
+      for (int w = ptid; w < E * NF; w += C::PT) {  // element-fastest: <= 2-way bank conflicts
+        const int m = w / E, e = w - m * E;
+        const int32_t gi = I[e * NF + m];
         if (gi >= 0) {
-          const int e = w / NF, m = w - e * NF;
           if (gi & TileLayout::GHOST_FLAG) {
             const float* src = p.u_in + p.ghost_base + (gi & ~TileLayout::GHOST_FLAG);
 #pragma unroll
@@ -206,17 +230,25 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
         }
       }
       cp_async_mbar_arrive(bar_tr + s);
+      // B_lo split of the element tile for 3xTF32 (padding is zero, so is its split)
+      const float* U = sU(s);
+      float* UL = sUL(s);
+      for (int w = ptid; w < TS; w += C::PT) UL[w] = tf32_lo(U[w]);
+      TC_A(2, t1);
     };
     auto flux = [&](int64_t j) {
       const int s = int(j % S);
+      TC_T(t0);
       mbar_wait(bar_tr + s, unsigned(j / S) & 1);
+      TC_A(3, t0);
+      TC_T(t1);
       const int ne = count_of(tile_of(j));
       const float* U = sU(s);
       const float* Gm = sG(s);
       const int32_t* I = sI(s);
       float* F = sF(s);
-      for (int w = ptid; w < E * NF; w += C::PT) {
-        const int e = w / NF, m = w - e * NF, f = m / Nfp;
+      for (int w = ptid; w < E * NF; w += C::PT) {  // element-fastest
+        const int m = w / E, e = w - m * E, f = m / Nfp;
         float fl[6] = {0, 0, 0, 0, 0, 0};
         if (e < ne) {
           const float* g = Gm + e * GEO_W + 9 + 4 * f;
@@ -225,7 +257,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
           float uM[6], dE[3], dH[3];
 #pragma unroll
           for (int c = 0; c < 6; ++c) uM[c] = U[cm_off(6 * e + c, nM, KV)];
-          if (I[w] >= 0) {
+          if (I[e * NF + m] >= 0) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
               dE[c] = F[cm_off(6 * e + c, m, KL)] - uM[c];
@@ -243,27 +275,37 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
 #pragma unroll
           for (int c = 0; c < 6; ++c) fl[c] *= sc;
         }
+        float* FL = sFL(s);
 #pragma unroll
-        for (int c = 0; c < 6; ++c) F[cm_off(6 * e + c, m, KL)] = fl[c];
+        for (int c = 0; c < 6; ++c) {
+          const int o = cm_off(6 * e + c, m, KL);
+          F[o] = fl[c];
+          FL[o] = tf32_lo(fl[c]);  // B_lo split for 3xTF32
+        }
       }
-      if constexpr (KL > NF) {  // zero the lift K padding
+      if constexpr (KL > NF) {  // zero the lift K padding (and its split)
+        float* FL = sFL(s);
         for (int w = ptid; w < COLS * (KL - NF); w += C::PT) {
           const int cl = w / (KL - NF), k = NF + (w - cl * (KL - NF));
           F[cm_off(cl, k, KL)] = 0.0f;
+          FL[cm_off(cl, k, KL)] = 0.0f;
         }
       }
-      asm volatile("bar.sync 1, %0;" ::"n"(C::PT) : "memory");  // flux warps: face buffer complete
-      // B_lo splits for 3xTF32 (U padding is zero, so its split is zero too)
-      float* FL = sFL(s);
-      float* UL = sUL(s);
-      for (int w = ptid; w < FS; w += C::PT) FL[w] = tf32_lo(F[w]);
-      for (int w = ptid; w < TS; w += C::PT) UL[w] = tf32_lo(U[w]);
+      TC_A(4, t1);
+      TC_T(t2);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tcgen05.mma operands
+      TC_A(5, t2);
       mbar_arrive(bar_full + s);
     };
+    for (int64_t t = 0; t < C::LA && t < J; ++t) traces(t);
     for (int64_t j = 0; j < J; ++j) {
-      traces(j);
-      flux(j);
+      if (C::LA == 0) {
+        traces(j);
+        flux(j);
+      } else {
+        flux(j);
+        if (j + C::LA < J) traces(j + C::LA);
+      }
     }
   } else if (warp == C::W_MMA) {
     // ========================= MMA issuer =========================
@@ -271,8 +313,13 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
       constexpr uint32_t idv = idesc_tf32_f32(C::MV, COLS), idl = idesc_tf32_f32(C::ML, COLS);
       for (int64_t j = 0; j < J; ++j) {
         const int s = int(j % S), a = int(j & 1);
+        TC_T(t0);
         mbar_wait(bar_full + s, unsigned(j / S) & 1);
+        TC_A(6, t0);
+        TC_T(t1);
         mbar_wait(acc_empty + a, (unsigned(j >> 1) & 1) ^ 1);
+        TC_A(7, t1);
+        TC_T(t2);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t dV = tmem + uint32_t(a * 2 * COLS), dL = dV + COLS;
         const float* U = sU(s);
@@ -298,24 +345,29 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                          smem_u32(acc_full + a))
                      : "memory");
+        TC_A(8, t2);
       }
     }
   } else {
     // =========================== epilogue ===========================
     const int q = warp & 3;           // TMEM lane quarter of this warp
+    const int half = (warp - C::W_EPI0) >> 2;  // which of the two warps of this quarter
     const int et = tid - 32 * C::W_EPI0;
     for (int64_t j = 0; j < J; ++j) {
       const int s = int(j % S), a = int(j & 1);
       const int64_t tile = tile_of(j);
       const int ne = count_of(tile);
+      TC_T(t0);
       mbar_wait(acc_full + a, unsigned(j >> 1) & 1);
+      TC_A(9, t0);
+      TC_T(t1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       // pass 1: TMEM rows -> shared staging (M=128: row = lane; M=64: row = 16*q + lane, lane < 16)
       const uint32_t colV = uint32_t(a * 2 * COLS), colL = colV + COLS;
       const int rowV = C::MV == 128 ? 32 * q + lane : (lane < 16 ? 16 * q + lane : -1);
       const int rowL = lane < 16 ? 16 * q + lane : -1;
 #pragma unroll 1
-      for (int c0 = 0; c0 < COLS; c0 += 8) {
+      for (int c0 = 8 * half; c0 < COLS; c0 += 8 * (C::EW / 4)) {
         uint32_t v[8], l[8];
         const uint32_t base = tmem + (uint32_t(32 * q) << 16);
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -335,14 +387,17 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty + a);
-      asm volatile("bar.sync 2, 128;" ::: "memory");  // staging complete
-      // pass 2: per (node i, element e): chain rule + curl (eq. 4, 6) + lift + LSERK update
-      const float* U = sU(s);
-      const float* R = sR(s);
+      asm volatile("bar.sync 2, %0;" ::"n"(C::ET) : "memory");  // staging complete
+      TC_A(10, t1);
+      TC_T(t2);
+      // pass 2: per (node i, element e): chain rule + curl (eq. 4, 6) + lift + LSERK update.
+      // Results overwrite the slot's tile images (u_out into U, res/rhs into R), which
+      // are then written back with one bulk copy each.
+      float* U = sU(s);
+      float* R = sR(s);
       const float* Gm = sG(s);
-      for (int pr = et; pr < Np * E; pr += 128) {
-        const int e = pr / Np, i = pr - e * Np;
-        if (e >= ne) continue;
+      for (int pr = et; pr < Np * E; pr += C::ET) {  // element-fastest: <= 2-way bank conflicts
+        const int i = pr / E, e = pr - i * E;
         const float* g = Gm + e * GEO_W;
         float dx[6], dy[6], dz[6];
 #pragma unroll
@@ -366,19 +421,43 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
           const int col = 6 * e + c;
           const float r = rhs[c] + YL[i * (COLS + 1) + col];
           const int o = cm_off(col, i, KV);
-          const int64_t idx = tile * TS + o;
           if (UPDATE) {
             const float rold = res_in ? R[o] : 0.0f;
             const float rr = p.rk_a * rold + p.dt * r;
-            p.res[idx] = rr;
-            p.u_out[idx] = U[o] + p.rk_b * rr;
+            R[o] = rr;
+            U[o] = U[o] + p.rk_b * rr;
           } else {
-            p.rhs_out[idx] = r;
+            R[o] = r;
           }
         }
       }
-      asm volatile("bar.sync 2, 128;" ::: "memory");  // staging and slot reads done
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> bulk-store reads
+      asm volatile("bar.sync 2, %0;" ::"n"(C::ET) : "memory");     // staging and slot tile images done
+      TC_A(11, t2);
+      TC_T(t3);
+      if (et == 0) {
+        // absent elements of a partial tile hold zero fields -> zero results; padding rows stay zero
+        if (UPDATE) {
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(p.u_out + tile * TS),
+                       "r"(smem_u32(U)), "r"(unsigned(TS * 4))
+                       : "memory");
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(p.res + tile * TS),
+                       "r"(smem_u32(R)), "r"(unsigned(TS * 4))
+                       : "memory");
+        } else {
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(p.rhs_out + tile * TS),
+                       "r"(smem_u32(R)), "r"(unsigned(TS * 4))
+                       : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem may be reused after this
+      }
+      asm volatile("bar.sync 2, %0;" ::"n"(C::ET) : "memory");
       if (lane == 0) mbar_arrive(bar_empty + s);
+      TC_A(12, t3);
+#ifdef DG_WS_PROFILE
+      if (et == 0) atomicAdd(&g_tc_prof[13], 1ull);
+#endif
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -388,6 +467,14 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
   }
 }
+
+#ifdef DG_WS_PROFILE
+inline void tc_prof_read(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_tc_prof, sizeof(g_tc_prof)); }
+inline void tc_prof_reset() {
+  static unsigned long long z[16] = {0};
+  cudaMemcpyToSymbol(g_tc_prof, z, sizeof(z));
+}
+#endif
 
 template <int N>
 void launch_stage_tc(const StageParams<float>& p, const float* opsA, int mode, cudaStream_t st) {
