@@ -81,7 +81,10 @@ void build_gather_index(const RefElem& ref, const MeshData& m, const Partition& 
       for (int i = 0; i < Nfp; ++i) {
         const int j = m.fperm[code * Nfp + i];  // neighbour face-node position
         int64_t v;
-        if (L.perm == 2)
+        const int64_t l2 = g >= 0 ? -1 : P.g2l[k2];
+        if (L.perm >= 1 && l2 >= 0 && l2 / L.E == l / L.E)
+          v = TileLayout::INTRA_FLAG | ((l2 % L.E) << 8) | ref.Fmask[f2 * Nfp + j];
+        else if (L.perm == 2)
           v = g >= 0 ? (TileLayout::GHOST_FLAG | (g * 6 * Nfp + j))
                      : ((P.g2l[k2] << 8) | ref.Fmask[f2 * Nfp + j]);
         else if (g >= 0)

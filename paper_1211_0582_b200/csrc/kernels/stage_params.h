@@ -57,6 +57,10 @@ struct TileLayout {
   // perm 2 stores (k2 << 8) | n2 and the kernel evaluates off() per component.
   // Ghost records are ghost_base + rec (perm 0/1) or GHOST_FLAG | rec (perm 2).
   static constexpr int32_t GHOST_FLAG = int32_t(1) << 30;
+  // tiled layouts (perm 1/2): a face whose neighbour sits in the SAME tile is encoded as
+  // INTRA_FLAG | (e2 << 8) | n2 — the kernel reads u+ from the tile already in shared
+  // memory instead of gathering it (the paper's flux-gather granularity).
+  static constexpr int32_t INTRA_FLAG = int32_t(1) << 29;
 };
 
 template <typename T>

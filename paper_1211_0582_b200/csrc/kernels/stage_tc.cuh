@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
       for (int w = ptid; w < E * NF; w += C::PT) {  // element-fastest: <= 2-way bank conflicts
         const int m = w / E, e = w - m * E;
         const int32_t gi = I[e * NF + m];
-        if (gi >= 0) {
+        if (gi >= 0 && !(gi & TileLayout::INTRA_FLAG)) {  // intra-tile faces need no gather
           if (gi & TileLayout::GHOST_FLAG) {
             const float* src = p.u_in + p.ghost_base + (gi & ~TileLayout::GHOST_FLAG);
 #pragma unroll
@@ -257,7 +257,15 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
           float uM[6], dE[3], dH[3];
 #pragma unroll
           for (int c = 0; c < 6; ++c) uM[c] = U[cm_off(6 * e + c, nM, KV)];
-          if (I[e * NF + m] >= 0) {
+          const int32_t gi = I[e * NF + m];
+          if (gi >= 0 && (gi & TileLayout::INTRA_FLAG)) {  // neighbour in this tile: u+ from shared memory
+            const int e2 = (gi >> 8) & 255, n2 = gi & 255;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              dE[c] = U[cm_off(6 * e2 + c, n2, KV)] - uM[c];
+              dH[c] = U[cm_off(6 * e2 + c + 3, n2, KV)] - uM[c + 3];
+            }
+          } else if (gi >= 0) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
               dE[c] = F[cm_off(6 * e + c, m, KL)] - uM[c];

@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
       float* F = sF(s);
       for (int w = ptid; w < E * NF; w += C::PT) {
         const int32_t gi = I[w];
-        if (gi >= 0) {
+        if (gi >= 0 && !(gi & TileLayout::INTRA_FLAG)) {  // intra-tile faces need no gather
           const int e = w / NF, m = w - e * NF;
           const bool ghost = gi >= p.ghost_base;
           const float* src = p.u_in + gi;
@@ -209,7 +209,16 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
           float uM[6], dE[3], dH[3];
 #pragma unroll
           for (int c = 0; c < 6; ++c) uM[c] = U[(cb + 8 * (c >> 1) + (c & 1)) * LD + nM];
-          if (I[w] >= 0) {
+          const int32_t gi = I[w];
+          if (gi >= 0 && (gi & TileLayout::INTRA_FLAG)) {  // neighbour in this tile: u+ from shared memory
+            const int e2 = (gi >> 8) & 255, n2 = gi & 255;
+            const int cb2 = 24 * (e2 >> 2) + 2 * (e2 & 3);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              dE[c] = U[(cb2 + 8 * (c >> 1) + (c & 1)) * LD + n2] - uM[c];
+              dH[c] = U[(cb2 + 8 * ((c + 3) >> 1) + ((c + 3) & 1)) * LD + n2] - uM[c + 3];
+            }
+          } else if (gi >= 0) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
               dE[c] = F[(cb + 8 * (c >> 1) + (c & 1)) * LDF + m] - uM[c];
