@@ -90,13 +90,14 @@ def ws_kind(N, prec, variant):
     return "basic" if (prec == 4 and N == 1) else "ws"
 
 
-def load_traffic(N, prec, variant):
-    """Per-launch DRAM bytes of the stage kernel from a committed ncu --set full capture, if any."""
+def load_traffic(N, prec, variant, K):
+    """Per-launch DRAM bytes of the stage kernel from a committed ncu --set full capture of
+    the same (precision, variant, order, mesh size), if any."""
     p = os.path.join(ROOT, "profiles", "r1_traffic.json")
     try:
         with open(p) as fh:
             t = json.load(fh)
-        return t.get(f"{'f64' if prec == 8 else 'f32'}:{variant}:{N}", {}).get("dram_bytes")
+        return t.get(f"{'f64' if prec == 8 else 'f32'}:{variant}:{N}:K{K}", {}).get("dram_bytes")
     except Exception:
         return None
 
@@ -205,9 +206,11 @@ def run_dg(args, N, prec, rank, world, local, dist, stream, flush, nccl_id, peak
 
     n = args.mesh_n
     VX, E = di.kuhn_box(n, nz=n * world)
+    if args.shuffle_seed is not None:
+        E, _ = di.shuffle_elements(E, args.shuffle_seed)
     K_total = E.shape[0]
     s = Solver(N, precision=prec, device=local, stream=stream.cuda_stream, rank=rank, nranks=world,
-               nccl_id=nccl_id, variant=args.variant)
+               nccl_id=nccl_id, variant=args.variant, reorder=args.reorder)
     s.mesh_upload(VX, E)
     Kl = s.K_local
     U0 = di.random_fields(K_total, N, seed=0)[:, s.local_elements()]
@@ -247,7 +250,7 @@ def run_dg(args, N, prec, rank, world, local, dist, stream, flush, nccl_id, peak
     kernel_ms = ms_step / 5 if world == 1 else s.time_stage_kernel(10)
     res["stage_kernel_ms"] = round(kernel_ms, 5)
     res["roofline"] = roofline(N, prec, Kl, kernel_ms, peaks, args.variant,
-                               traffic=load_traffic(N, prec, args.variant) if world == 1 else None)
+                               traffic=load_traffic(N, prec, args.variant, Kl) if world == 1 else None)
     if e2e:
         # end to end through the C ABI with HOST buffers: upload (pinned H2D) + step + download (D2H)
         host_in = torch.from_numpy(np.ascontiguousarray(U0)).pin_memory().numpy()
@@ -312,6 +315,9 @@ def main():
     ap.add_argument("--mesh-n", type=int, default=15)
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-large", action="store_true", help="skip the HBM-resident C4 line (K = 1.05M)")
+    ap.add_argument("--shuffle-seed", type=int, default=None, help="random element numbering (unstructured-like)")
+    ap.add_argument("--reorder", action="store_true", help="library Morton renumbering of the elements")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
@@ -360,6 +366,15 @@ def main():
                 for n_ in range(1, 10):
                     r = run_dg(args, n_, p, rank, world, local, dist, stream, flush, nccl_id, peaks)
                     sweep.append({k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()})
+        large = None
+        if not args.no_large and world == 1:
+            # configs[3] at one GPU: Kuhn n=56, K = 1 053 696 (state 1.8 GB >> 126 MB L2), N=4 FP64
+            import copy
+            a2 = copy.copy(args)
+            a2.mesh_n, a2.steps, a2.warmup = 56, max(3, min(args.steps, 10)), 3
+            r = run_dg(a2, 4, 8, rank, world, local, dist, stream, flush, nccl_id, peaks)
+            large = {k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()}
+            large["workload"] = "C4 (configs[3]) at 1 GPU: Kuhn n=56, K=1053696, N=4, FP64; HBM-resident"
     clocks = clk.summary()
 
     cpu = None
@@ -374,13 +389,16 @@ def main():
                     "config": {"workload": workload, "K_total": head["K_total"], "order": N,
                                "precision": head["precision"], "parallelism": f"mesh z-slabs x{world}, NCCL halo",
                                "l2": "flushed before every timed step (256 MiB write, not timed)",
-                               "variant": args.variant, "kernel": ws_kind(N, prec, args.variant)},
+                               "variant": args.variant, "kernel": ws_kind(N, prec, args.variant),
+                               "element_order": ("shuffled(seed %d)" % args.shuffle_seed
+                                                 if args.shuffle_seed is not None else "natural")
+                                                + (" + Morton reorder" if args.reorder else "")},
                     "roofline": head["roofline"], "e2e": head["e2e"],
                     "gpu_launches": head["launches_per_step"] * args.steps,
                     "stage_kernel_ms": head["stage_kernel_ms"],
                     "clocks": clocks, "cpu_baseline": cpu,
                     "peaks": {k: v for k, v in peaks.items()},
-                    "sweep": sweep})
+                    "sweep": sweep, "large": large})
         print(json.dumps(out), flush=True)
     if dist:
         dist.barrier()

@@ -132,10 +132,11 @@ def jitter_interior(VX, n: int, seed: int, L: float = 1.0, amp: float = 0.1):
     return VX
 
 
-def random_fields(K: int, N: int, seed: int = 0):
-    """U(-1,1) fields, shape [6][K][Np], float64 (C-ABI host layout)."""
+def random_fields(K: int, N: int, seed: int = 0, nfields: int = 6):
+    """U(-1,1) fields, shape [nfields][K][Np], float64 (C-ABI host layout); nfields = 6
+    for Maxwell (Ex..Hz), 4 for acoustics (p, vx, vy, vz)."""
     rng = np.random.default_rng(seed)
-    return rng.uniform(-1.0, 1.0, size=(6, K, np_of(N)))
+    return rng.uniform(-1.0, 1.0, size=(nfields, K, np_of(N)))
 
 
 def cavity_mode_101(x, y, z, t=0.0):
@@ -177,6 +178,25 @@ def cavity_mode_111(x, y, z, t=0.0, A=1.0, B=-0.5, C=-0.5):
     Hy = -(cEy / w) * st
     Hz = -(cEz / w) * st
     return np.stack([Ex, Ey, Ez, Hx, Hy, Hz])
+
+
+def acoustic_mode(x, y, z, t=0.0, lmn=(1, 1, 1)):
+    """Exact rigid-wall (v.n = 0) eigenmode of linear acoustics (rho0 = c = 1) in the unit
+    cube: p = cos(l pi x) cos(m pi y) cos(n pi z) cos(w t), v = -(sin(w t)/w) grad p0,
+    w = pi sqrt(l^2 + m^2 + n^2).  Returns [4][...] ordered (p, vx, vy, vz)."""
+    x = np.asarray(x, dtype=np.float64); y = np.asarray(y, dtype=np.float64); z = np.asarray(z, dtype=np.float64)
+    l, m, n = lmn
+    pi = math.pi
+    w = pi * math.sqrt(l * l + m * m + n * n)
+    cx, sx = np.cos(l * pi * x), np.sin(l * pi * x)
+    cy, sy = np.cos(m * pi * y), np.sin(m * pi * y)
+    cz, sz = np.cos(n * pi * z), np.sin(n * pi * z)
+    st = math.sin(w * t) / w
+    p = cx * cy * cz * math.cos(w * t)
+    vx = l * pi * sx * cy * cz * st
+    vy = m * pi * cx * sy * cz * st
+    vz = n * pi * cx * cy * sz * st
+    return np.stack([p, vx, vy, vz])
 
 
 def dt_rule(VX, EToV, N: int, C: float = 0.25):

@@ -89,6 +89,10 @@ typedef struct {
                            makes a loopback partition solver: no NCCL; the ranks live in this
                            process and are stepped together by dg_group_lserk_step */
   int32_t variant;      /* dg_variant */
+  int32_t reorder;      /* 1: renumber this rank's elements along a Morton curve of their
+                           centroids (within the interior and partition-boundary groups) for
+                           gather locality and intra-tile faces; dg_local_elements reports the
+                           storage order.  0 (default): ascending global id within each group */
 } dg_config;
 
 /* Fill *cfg with defaults: N=3, FP64, alpha=1, device 0, own stream, 1 rank, AUTO. */

@@ -19,6 +19,8 @@ Modules
            coordinate matching
   maxwell  Maxwell RHS with upwind flux + PEC walls, LSERK4, energy
            (PAPER.md:157-169, 231-255, 1083-1092, 1179-1181)
+  acoustics  second linear system: linear acoustics with upwind
+           flux + rigid walls through the same four stages
 
 Parity pins: every function is pinned by a `-m "not gpu"` test in
 tests/test_oracle_*.py against closed forms, invariants, brute force or
@@ -26,7 +28,7 @@ golden values (see DESIGN.md §"Oracle and its pins").  Functions whose result i
 pinned only by invariants (the interior warp&blend node positions for N >= 4)
 say so in their docstring: "parity unpinned beyond invariants".
 """
-from . import refelem, mesh, maxwell  # noqa: F401
+from . import refelem, mesh, maxwell, acoustics  # noqa: F401
 from .refelem import RefElement, build_reference  # noqa: F401
 from .mesh import Setup  # noqa: F401
 from .maxwell import rhs, lserk4, lserk4_coefficients, energy  # noqa: F401

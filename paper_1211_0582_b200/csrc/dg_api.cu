@@ -530,6 +530,7 @@ void dg_config_default(dg_config* c) {
   c->nranks = 1;
   c->nccl_id = nullptr;
   c->variant = DG_VARIANT_AUTO;
+  c->reorder = 0;
 }
 
 const char* dg_last_error(void) { return g_err.c_str(); }
@@ -599,7 +600,8 @@ dg_status dg_mesh_upload(dg_solver* s, int64_t nv, const double* VX, int64_t K, 
   std::string err;
   try {
     err = dg::build_mesh(s->ref, nv, VX, K, EToV, s->mesh);
-    if (err.empty()) err = dg::build_partition(s->mesh, s->cfg.rank, s->cfg.nranks, part, s->part);
+    if (err.empty())
+      err = dg::build_partition(s->mesh, s->cfg.rank, s->cfg.nranks, part, s->part, s->cfg.reorder != 0);
   } catch (const std::exception& e) {
     err = e.what();
   }

@@ -6,8 +6,46 @@
 
 namespace dg {
 
+namespace {
+uint64_t spread3(uint64_t v) {  // 21-bit -> every third bit
+  v &= 0x1fffff;
+  v = (v | v << 32) & 0x1f00000000ffffULL;
+  v = (v | v << 16) & 0x1f0000ff0000ffULL;
+  v = (v | v << 8) & 0x100f00f00f00f00fULL;
+  v = (v | v << 4) & 0x10c30c30c30c30c3ULL;
+  v = (v | v << 2) & 0x1249249249249249ULL;
+  return v;
+}
+// sort [b, e) of ids by the Morton code of the element centroids (bounding box of all elements)
+void morton_sort(const MeshData& m, std::vector<int64_t>& ids, size_t b, size_t e) {
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int64_t v = 0; v < m.nv; ++v)
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = std::min(lo[d], m.VX[3 * v + d]);
+      hi[d] = std::max(hi[d], m.VX[3 * v + d]);
+    }
+  std::vector<std::pair<uint64_t, int64_t>> key;
+  key.reserve(e - b);
+  for (size_t i = b; i < e; ++i) {
+    const int64_t k = ids[i];
+    uint64_t code = 0;
+    for (int d = 0; d < 3; ++d) {
+      double c = 0;
+      for (int q = 0; q < 4; ++q) c += m.VX[3 * m.EToV[4 * k + q] + d];
+      c *= 0.25;
+      const double t = (c - lo[d]) / std::max(hi[d] - lo[d], 1e-300);
+      const uint64_t g = uint64_t(std::min(std::max(t, 0.0), 1.0) * double((1 << 21) - 1));
+      code |= spread3(g) << d;
+    }
+    key.push_back({code, k});
+  }
+  std::sort(key.begin(), key.end());
+  for (size_t i = b; i < e; ++i) ids[i] = key[i - b].second;
+}
+}  // namespace
+
 std::string build_partition(const MeshData& m, int rank, int nranks, const int32_t* owner,
-                            Partition& P) {
+                            Partition& P, bool reorder) {
   const int64_t K = m.K;
   P = Partition();
   P.rank = rank;
@@ -40,6 +78,10 @@ std::string build_partition(const MeshData& m, int rank, int nranks, const int32
   for (int64_t k = 0; k < K; ++k)
     if (own[k] == rank && is_bnd[k]) P.local_ids.push_back(k);
   P.K_local = int64_t(P.local_ids.size());
+  if (reorder) {
+    morton_sort(m, P.local_ids, 0, size_t(P.K_interior));
+    morton_sort(m, P.local_ids, size_t(P.K_interior), size_t(P.K_local));
+  }
   P.g2l.assign(K, -1);
   for (int64_t l = 0; l < P.K_local; ++l) P.g2l[P.local_ids[l]] = l;
   P.ghost_of.assign(4 * P.K_local, -1);

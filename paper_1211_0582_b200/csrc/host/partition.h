@@ -42,9 +42,10 @@ struct Partition {
   std::vector<int64_t> ghost_of;    // [K_local][4]
 };
 
-// owner: [K] rank per element, or empty -> contiguous ranges.  Returns "" or an error.
+// owner: [K] rank per element, or empty -> contiguous ranges.  reorder: sort each group
+// (interior, boundary) by the Morton code of the element centroids.  Returns "" or an error.
 std::string build_partition(const MeshData& m, int rank, int nranks, const int32_t* owner,
-                            Partition& out);
+                            Partition& out, bool reorder = false);
 
 // Gather index of the exterior trace for every local face node (see
 // stage_params.h): L.off(k2_local, 0, n2), or ghost_base + g*6*Nfp + j, or -1

@@ -30,7 +30,8 @@ STATUS_NAMES = {0: "DG_OK", 1: "DG_ERR_ARG", 2: "DG_ERR_ORDER", 3: "DG_ERR_MESH"
 class dg_config(C.Structure):
     _fields_ = [("order", C.c_int32), ("precision", C.c_int32), ("alpha", C.c_double),
                 ("device", C.c_int32), ("stream", C.c_void_p), ("rank", C.c_int32),
-                ("nranks", C.c_int32), ("nccl_id", C.c_void_p), ("variant", C.c_int32)]
+                ("nranks", C.c_int32), ("nccl_id", C.c_void_p), ("variant", C.c_int32),
+                ("reorder", C.c_int32)]
 
 
 _P = C.c_void_p
@@ -100,12 +101,12 @@ class Solver:
     C-ABI layout [6][K_local][Np]; device arrays are torch tensors (data_ptr)."""
 
     def __init__(self, order, precision=8, alpha=1.0, device=0, stream=None, rank=0, nranks=1,
-                 nccl_id=None, variant=DG_VARIANT_AUTO):
+                 nccl_id=None, variant=DG_VARIANT_AUTO, reorder=False):
         cfg = dg_config()
         dg_config_default(C.byref(cfg))
         cfg.order, cfg.precision, cfg.alpha, cfg.device = order, precision, alpha, device
         cfg.stream = stream
-        cfg.rank, cfg.nranks, cfg.variant = rank, nranks, variant
+        cfg.rank, cfg.nranks, cfg.variant, cfg.reorder = rank, nranks, variant, int(bool(reorder))
         self._id_buf = None
         if nccl_id is not None:
             self._id_buf = C.create_string_buffer(bytes(nccl_id), 128)

@@ -154,3 +154,28 @@ def test_partition_local_order_and_ids():
         # contiguous default owner: k*P//K
         assert set(ids.tolist()) == {k for k in range(K) if (k * 2) // K == r}
     assert sorted(np.concatenate(seen).tolist()) == list(range(K))
+
+
+def test_morton_reorder_is_local_permutation():
+    # reorder=1: a permutation of this rank's elements (interior group first, then the
+    # partition-boundary group), with far better centroid locality than a shuffled input
+    VX, E = di.kuhn_box(6)
+    E, _ = di.shuffle_elements(E, 4)
+    cen = VX[E].mean(axis=1)
+
+    def hop(ids):
+        return float(np.linalg.norm(np.diff(cen[ids], axis=0), axis=1).mean())
+
+    s = Solver(3, device=-1, reorder=True)
+    s.mesh_upload(VX, E)
+    ids = s.local_elements()
+    assert np.array_equal(np.sort(ids), np.arange(E.shape[0]))
+    assert hop(ids) < 0.25 * hop(np.arange(E.shape[0]))
+    st = oracle.Setup(VX, E, 3)
+    EToE, EToF, vM, vP = s.get_maps()                 # maps stay in global numbering
+    assert (EToE == st.EToE).all() and (vP == st.vmapP).all()
+    for r in range(2):
+        s = Solver(2, device=-1, rank=r, nranks=2, reorder=True)
+        s.mesh_upload(VX, E)
+        ids = s.local_elements()
+        assert set(ids.tolist()) == {k for k in range(E.shape[0]) if (k * 2) // E.shape[0] == r}

@@ -161,6 +161,57 @@ def test_central_flux_alpha0():
 
 
 @pytest.mark.parametrize("prec", [8, 4])
+def test_central_flux_energy_conserved_on_gpu(prec):
+    # NEXT-2: alpha = 0 with PEC walls is a skew operator in the M_g inner
+    # product, so the discrete energy is conserved up to the O(dt^6) LSERK4 defect
+    # (oracle pin: tests/test_oracle_operator.py::test_central_flux_energy_drift_small);
+    # the upwind flux (alpha = 1) must dissipate.
+    N = 4
+    VX, E = mesh(2, 7, 8, None)
+    st = oracle.Setup(VX, E, N)
+    U0 = di.random_fields(st.K, N, seed=11)
+    dt = di.dt_rule(VX, E, N)
+    e0 = oracle.energy(st, U0)
+    out = {}
+    for alpha in (0.0, 1.0):
+        s = Solver(N, precision=prec, alpha=alpha)
+        s.mesh_upload(VX, E)
+        s.fields_upload(U0)
+        s.lserk_step(dt, 50)
+        out[alpha] = s.fields_download()
+        s.close()
+    # random fields load the top of the spectrum, where the LSERK4 defect |R(iy)| - 1
+    # ~ -y^6/72 gives an oracle drift of -2.25e-6 over 50 steps (upwind: -39%)
+    assert abs(oracle.energy(st, out[0.0]) - e0) / e0 < (1e-5 if prec == 8 else 1e-4)
+    assert oracle.energy(st, out[1.0]) < 0.7 * e0
+    if prec == 8:
+        ref = oracle.lserk4(st, U0, dt, 50, alpha=0.0)
+        assert relerr(out[0.0], ref) < 1e-11
+        assert abs(oracle.energy(st, out[0.0]) - oracle.energy(st, ref)) < 1e-12 * e0
+
+
+@pytest.mark.parametrize("prec,variant", VARIANTS, ids=VIDS)
+@pytest.mark.parametrize("N", [1, 3, 4, 7])
+def test_morton_reorder(N, prec, variant):
+    # reorder=1: the library renumbers elements along a Morton curve; fields are in the
+    # storage order dg_local_elements reports, results must equal the oracle's permuted
+    supported(N, prec, variant)
+    VX, E = mesh(6, 31, 32, 33)
+    st = setup("m6", VX, E, N)
+    U0 = di.random_fields(st.K, N, seed=9)
+    s = Solver(N, precision=prec, variant=variant, reorder=True)
+    s.mesh_upload(VX, E)
+    ids = s.local_elements()
+    assert np.array_equal(np.sort(ids), np.arange(st.K)) and not np.array_equal(ids, np.arange(st.K))
+    s.fields_upload(np.ascontiguousarray(U0[:, ids]))
+    assert relerr(s.rhs(), oracle.rhs(st, U0)[:, ids]) < TOL_RHS[prec]
+    dt = di.dt_rule(VX, E, N)
+    s.lserk_step(dt, 2)
+    assert relerr(s.fields_download(), oracle.lserk4(st, U0, dt, 2)[:, ids]) < TOL_STEP[prec]
+    s.close()
+
+
+@pytest.mark.parametrize("prec", [8, 4])
 @pytest.mark.parametrize("N", [1, 4, 9])
 def test_bench_mesh_full_size(N, prec):
     # the bench workload (config C2: Kuhn n=15, K=20250), full-size comparison

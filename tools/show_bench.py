@@ -13,3 +13,6 @@ for r in d.get("sweep", []):
     rf = r["roofline"]
     print(f'{r["precision"]} N={r["N"]} {r["ms_per_step"]:9.4f} ms  {r["dof_updates_per_s"]:.3g} DOF/s  '
           f'{r["gflops"]:8.0f} GF/s  {rf["bound"]} {rf["frac"]:.3f} of {rf["peak"]}')
+if d.get("large"):
+    r = d["large"]
+    print("large", r.get("workload"), r["ms_per_step"], "ms", f'{r["dof_updates_per_s"]:.3g}', "DOF/s", r["roofline"])
