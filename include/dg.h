@@ -28,7 +28,8 @@
  *     A call out of order returns DG_ERR_STATE.
  *   - Fields on the host are FP64, component-major [6][K_local][Np] in the
  *     order (Ex, Ey, Ez, Hx, Hy, Hz), node index fastest (HW's Np x K per
- *     component).  Node n of element k is the n-th warp&blend node mapped
+ *     component).  With dg_config.system = DG_SYSTEM_ACOUSTICS every "[6]" below
+ *     reads "[4]", components (p, vx, vy, vz).  Node n of element k is the n-th warp&blend node mapped
  *     affinely (dg_get_nodes).  FP32 solvers round on upload and widen exactly
  *     on download.
  *   - Work is enqueued on the solver's stream (dg_config.stream, or a
@@ -77,6 +78,16 @@ typedef enum {
                             accumulators (5th-generation tensor cores) */
 } dg_variant;
 
+/* The linear hyperbolic system u_t + div F(u) = 0 the operator is
+ * built for.  Both go through the same four stages (volume, flux gather, lift, update). */
+typedef enum {
+  DG_SYSTEM_MAXWELL = 0,   /* 6 fields (E, H): the north_star path; every variant */
+  DG_SYSTEM_ACOUSTICS = 1  /* 4 fields (p, v), rho0 = c = 1: p_t + div v = 0, v_t + grad p = 0;
+                              upwind flux (-A_n + alpha |A_n|)[[u]]; rigid walls v.n = 0
+                              (mirror p+ = p-, v+ = v- - 2 (n.v-) n); R16/R17.
+                              BASIC kernel only (AUTO selects it; MMA/MMA_WS/TC -> DG_ERR_ARG) */
+} dg_system;
+
 typedef struct {
   int32_t order;        /* polynomial order N, 1..9 */
   int32_t precision;    /* 8 = FP64, 4 = FP32 arithmetic and storage on the device */
@@ -93,9 +104,11 @@ typedef struct {
                            centroids (within the interior and partition-boundary groups) for
                            gather locality and intra-tile faces; dg_local_elements reports the
                            storage order.  0 (default): ascending global id within each group */
+  int32_t system;       /* dg_system (default DG_SYSTEM_MAXWELL) */
 } dg_config;
 
-/* Fill *cfg with defaults: N=3, FP64, alpha=1, device 0, own stream, 1 rank, AUTO. */
+/* Fill *cfg with defaults: N=3, FP64, alpha=1, device 0, own stream, 1 rank, AUTO,
+ * no reorder, Maxwell. */
 DG_API void dg_config_default(dg_config* cfg);
 
 /* Create a solver.  Builds the reference element of order N on the host (FP64).

@@ -83,6 +83,7 @@ const double kRkB[5] = {1432997174477.0 / 9575080441755.0, 5161836677717.0 / 136
 struct dg_solver {
   dg_config cfg{};
   int N = 0, Np = 0, Nfp = 0;
+  int nc = 6;  // fields per element (dg_system)
   bool host_only = false;
   bool fp64 = true;
   size_t wsize = 8;
@@ -96,13 +97,13 @@ struct dg_solver {
   void* d_u[2] = {nullptr, nullptr};
   void* d_res = nullptr;
   void* d_scratch = nullptr;   // [Kl][ES] (solver precision)
-  double* d_stage64 = nullptr; // [6][Kl][Np] FP64 host-layout staging
+  double* d_stage64 = nullptr; // [nc][Kl][Np] FP64 host-layout staging
   void* d_geo = nullptr;
   int32_t* d_gidx = nullptr;
   void* d_ops = nullptr;
   void* d_ops_pad = nullptr;   // FP64 MMA variant operators, zero-padded
   int16_t* d_fmask = nullptr;
-  void* d_send = nullptr;      // [n_ghost][6][Nfp]
+  void* d_send = nullptr;      // [n_ghost][nc][Nfp]
   int32_t* d_sidx = nullptr;   // [n_ghost][Nfp] element-node offsets for packing
   cudaStream_t stream = nullptr, comm = nullptr;
   bool own_stream = false;
@@ -178,6 +179,7 @@ dg::StageParams<T> base_params(dg_solver* s) {
   p.ES = s->ES;
   p.ghost_base = s->ghost_base;
   p.alpha = T(s->cfg.alpha);
+  p.system = s->cfg.system;
   p.K = s->Kl;
   p.k_begin = 0;
   return p;
@@ -203,7 +205,7 @@ dg_status enqueue_exchange(dg_solver* s, T* u) {
   if (P.n_ghost_faces == 0) return DG_OK;
   dg::pack_traces<T>(u, static_cast<T*>(s->d_send), s->d_sidx, P.n_ghost_faces, s->Nfp, s->lay, s->comm);
   NcclApi& n = nccl();
-  const size_t rec = size_t(6) * s->Nfp;
+  const size_t rec = size_t(s->nc) * s->Nfp;
   const int dtype = sizeof(T) == 8 ? ncclFloat64_ : ncclFloat32_;
   if (n.GroupStart() != 0) return fail(DG_ERR_NCCL, "ncclGroupStart failed");
   for (const auto& pp : P.peers) {
@@ -264,7 +266,7 @@ dg::StageParams<T> stage_params(dg_solver* s, int stage, double dt, int cur) {
 // ghost records are copied device-to-device from its peers' send buffers.
 template <typename T>
 dg_status group_stage(dg_solver* const* g, int n, int stage, double dt, int cur) {
-  const size_t rec = size_t(6) * g[0]->Nfp;
+  const size_t rec = size_t(g[0]->nc) * g[0]->Nfp;
   for (int i = 0; i < n; ++i) {  // pack (after my previous stage, after peers finished reading my send buffer)
     dg_solver* s = g[i];
     if (s->part.n_ghost_faces == 0) continue;
@@ -345,17 +347,18 @@ dg_status upload_setup(dg_solver* s) {
     if (Kl >= (int64_t(1) << 22)) return fail(DG_ERR_ARG, "TC variant: more than 2^22 local elements");
   } else {
     s->lay = dg::TileLayout();
+    s->lay.nc = s->nc;
     s->lay.E = 1;
     s->lay.LD = Np;
     s->lay.perm = 0;
-    s->lay.TS = sizeof(T) == 8 ? 6 * Np : ((6 * Np + 3) / 4) * 4;
+    s->lay.TS = sizeof(T) == 8 ? s->nc * Np : ((s->nc * Np + 3) / 4) * 4;
   }
   s->ES = s->lay.TS;
   s->ntiles = s->lay.ntiles(Kl);
   const int64_t Kpad = s->ntiles * s->lay.E;
   const int64_t twords = s->ntiles * s->lay.TS;
   s->ghost_base = twords;
-  s->ghost_words = P.n_ghost_faces * 6 * Nfp;
+  s->ghost_words = P.n_ghost_faces * s->nc * Nfp;
   const int64_t uwords = s->ghost_base + s->ghost_words;
   if (uwords >= (int64_t(1) << (s->lay.perm >= 1 ? 29 : 31)))
     return fail(DG_ERR_ARG, "local problem too large for 32-bit gather indices on one rank (partition further)");
@@ -368,7 +371,7 @@ dg_status upload_setup(dg_solver* s) {
   CK(cudaMemsetAsync(s->d_res, 0, std::max<int64_t>(twords, 1) * wb, s->stream));
   CK(cudaMalloc(&s->d_scratch, std::max<int64_t>(twords, 1) * wb));
   CK(cudaMemsetAsync(s->d_scratch, 0, std::max<int64_t>(twords, 1) * wb, s->stream));
-  CK(cudaMalloc((void**)&s->d_stage64, std::max<int64_t>(6 * Kl * Np, 1) * sizeof(double)));
+  CK(cudaMalloc((void**)&s->d_stage64, std::max<int64_t>(s->nc * Kl * Np, 1) * sizeof(double)));
   // geometry [Kpad][GEO_W] (padding elements zero)
   std::vector<T> geo(size_t(std::max<int64_t>(Kpad, 1)) * dg::GEO_W, T(0));
   for (int64_t l = 0; l < Kl; ++l) {
@@ -425,7 +428,7 @@ dg_status upload_setup(dg_solver* s) {
   CK(cudaMalloc((void**)&s->d_fmask, NF * sizeof(int16_t)));
   CK(cudaMemcpy(s->d_fmask, fm.data(), NF * sizeof(int16_t), cudaMemcpyHostToDevice));
   if (P.n_ghost_faces > 0) {
-    CK(cudaMalloc(&s->d_send, P.n_ghost_faces * 6 * Nfp * wb));
+    CK(cudaMalloc(&s->d_send, P.n_ghost_faces * s->nc * Nfp * wb));
     std::vector<int32_t> sidx(size_t(P.n_ghost_faces) * Nfp);
     for (int64_t g = 0; g < P.n_ghost_faces; ++g)
       for (int j = 0; j < Nfp; ++j)
@@ -531,6 +534,7 @@ void dg_config_default(dg_config* c) {
   c->nccl_id = nullptr;
   c->variant = DG_VARIANT_AUTO;
   c->reorder = 0;
+  c->system = DG_SYSTEM_MAXWELL;
 }
 
 const char* dg_last_error(void) { return g_err.c_str(); }
@@ -549,12 +553,18 @@ dg_status dg_create(const dg_config* cfg, dg_solver** out) {
   if (cfg->variant < 0 || cfg->variant > 4) return fail(DG_ERR_ARG, "bad variant");
   if (cfg->variant == DG_VARIANT_TC && (cfg->precision != 4 || cfg->order > 4))
     return fail(DG_ERR_ARG, "DG_VARIANT_TC is the FP32 tcgen05 kernel for N <= 4");
+  if (cfg->system != DG_SYSTEM_MAXWELL && cfg->system != DG_SYSTEM_ACOUSTICS) return fail(DG_ERR_ARG, "bad system");
+  if (cfg->system == DG_SYSTEM_ACOUSTICS && cfg->variant != DG_VARIANT_AUTO && cfg->variant != DG_VARIANT_BASIC)
+    return fail(DG_ERR_ARG, "DG_SYSTEM_ACOUSTICS runs on the BASIC kernel only");
   std::unique_ptr<dg_solver> s(new dg_solver());
   s->cfg = *cfg;
   s->N = cfg->order;
   s->fp64 = cfg->precision == 8;
   s->wsize = s->fp64 ? 8 : 4;
-  s->variant = cfg->variant == DG_VARIANT_AUTO ? auto_variant(cfg->precision == 8, cfg->order) : cfg->variant;
+  s->nc = cfg->system == DG_SYSTEM_ACOUSTICS ? 4 : 6;
+  s->variant = cfg->system == DG_SYSTEM_ACOUSTICS ? DG_VARIANT_BASIC
+               : cfg->variant == DG_VARIANT_AUTO  ? auto_variant(cfg->precision == 8, cfg->order)
+                                                  : cfg->variant;
   s->host_only = cfg->device < 0;
   try {
     s->ref = dg::build_ref_elem(s->N);
@@ -643,7 +653,7 @@ static dg_status upload_common(dg_solver* s, const void* src, bool from_host) {
   if (st != DG_OK) return st;
   if (!s->has_mesh) return fail(DG_ERR_STATE, "no mesh uploaded");
   if (!src) return fail(DG_ERR_ARG, "null field pointer");
-  const int64_t n = 6 * s->Kl * s->Np;
+  const int64_t n = s->nc * s->Kl * s->Np;
   s->cur = 0;
   if (from_host) {
     CK(cudaMemcpyAsync(s->d_stage64, src, n * sizeof(double), cudaMemcpyHostToDevice, s->stream));
@@ -675,7 +685,7 @@ static dg_status download_common(dg_solver* s, void* dst, bool to_host, bool rhs
   if (rhs && s->loopback) return fail(DG_ERR_STATE, "loopback partition solver: rhs needs its peers (use one solver)");
   if (!s->has_fields) return fail(DG_ERR_STATE, "no fields uploaded");
   if (!dst) return fail(DG_ERR_ARG, "null output pointer");
-  const int64_t n = 6 * s->Kl * s->Np;
+  const int64_t n = s->nc * s->Kl * s->Np;
   const void* tiles = s->d_u[s->cur];
   if (rhs) {
     st = s->fp64 ? enqueue_rhs<double>(s, static_cast<double*>(s->d_scratch))
@@ -734,7 +744,7 @@ dg_status dg_group_lserk_step(dg_solver* const* group, int32_t n, double dt, int
   }
   for (int i = 1; i < n; ++i)
     if (g[i]->N != g[0]->N || g[i]->fp64 != g[0]->fp64 || g[i]->cur != g[0]->cur || g[i]->mesh.K != g[0]->mesh.K ||
-        g[i]->lay.E != g[0]->lay.E || g[i]->lay.perm != g[0]->lay.perm)
+        g[i]->lay.E != g[0]->lay.E || g[i]->lay.perm != g[0]->lay.perm || g[i]->nc != g[0]->nc)
       return fail(DG_ERR_ARG, "group members differ in order, precision, variant, mesh or step parity");
   for (int step = 0; step < nsteps; ++step) {
     for (int stage = 0; stage < 5; ++stage) {

@@ -127,10 +127,10 @@ void build_gather_index(const RefElem& ref, const MeshData& m, const Partition& 
         if (L.perm >= 1 && l2 >= 0 && l2 / L.E == l / L.E)
           v = TileLayout::INTRA_FLAG | ((l2 % L.E) << 8) | ref.Fmask[f2 * Nfp + j];
         else if (L.perm == 2)
-          v = g >= 0 ? (TileLayout::GHOST_FLAG | (g * 6 * Nfp + j))
+          v = g >= 0 ? (TileLayout::GHOST_FLAG | (g * L.nc * Nfp + j))
                      : ((P.g2l[k2] << 8) | ref.Fmask[f2 * Nfp + j]);
         else if (g >= 0)
-          v = ghost_base + g * 6 * Nfp + j;
+          v = ghost_base + g * L.nc * Nfp + j;
         else
           v = L.off(P.g2l[k2], 0, ref.Fmask[f2 * Nfp + j]);
         gidx[(4 * l + f) * Nfp + i] = int32_t(v);

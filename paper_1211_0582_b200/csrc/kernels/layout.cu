@@ -1,4 +1,4 @@
-// Layout conversion between the C-ABI field layout [6][K][Np] (component-major,
+// Layout conversion between the C-ABI field layout [nc][K][Np] (nc = L.nc) (component-major,
 // HW's Np x K per component) and the device element-tile layout [K][ES]
 // (element-major, see stage_params.h).  Not on the timed device path; they run
 // inside dg_fields_upload/download and dg_rhs.
@@ -14,7 +14,7 @@ namespace dg {
 template <typename S, typename T>
 __global__ void k_cm_to_tiles(const S* __restrict__ src, T* __restrict__ dst, int64_t K, int Np, TileLayout L) {
   const int64_t total = L.ntiles(K) * L.TS;
-  const int cols = 6 * L.E;
+  const int cols = L.nc * L.E;
   for (int64_t w = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; w < total; w += int64_t(gridDim.x) * blockDim.x) {
     const int64_t t = w / L.TS;
     const int64_t r = w - t * L.TS;
@@ -35,8 +35,8 @@ __global__ void k_cm_to_tiles(const S* __restrict__ src, T* __restrict__ dst, in
         e = 4 * g + (rr >> 1);
         c = 2 * nt + (rr & 1);
       } else {
-        e = col / 6;
-        c = col - 6 * e;
+        e = col / L.nc;
+        c = col - L.nc * e;
       }
       const int64_t k = t * L.E + e;
       if (k < K) v = T(src[(int64_t(c) * K + k) * Np + n]);
@@ -48,7 +48,7 @@ __global__ void k_cm_to_tiles(const S* __restrict__ src, T* __restrict__ dst, in
 // device layout L -> [6][K][Np]
 template <typename T, typename D>
 __global__ void k_tiles_to_cm(const T* __restrict__ src, D* __restrict__ dst, int64_t K, int Np, TileLayout L) {
-  const int64_t total = 6 * K * Np;
+  const int64_t total = L.nc * K * Np;
   for (int64_t w = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; w < total; w += int64_t(gridDim.x) * blockDim.x) {
     const int64_t c = w / (K * Np);
     const int64_t rem = w - c * K * Np;
@@ -72,7 +72,7 @@ void cm_to_tiles(const S* src, T* dst, int64_t K, int Np, const TileLayout& L, v
 
 template <typename T, typename D>
 void tiles_to_cm(const T* src, D* dst, int64_t K, int Np, const TileLayout& L, void* st) {
-  k_tiles_to_cm<T, D><<<grid_for(6 * K * Np), 256, 0, static_cast<cudaStream_t>(st)>>>(src, dst, K, Np, L);
+  k_tiles_to_cm<T, D><<<grid_for(L.nc * K * Np), 256, 0, static_cast<cudaStream_t>(st)>>>(src, dst, K, Np, L);
 }
 
 template void cm_to_tiles<double, double>(const double*, double*, int64_t, int, const TileLayout&, void*);
@@ -91,10 +91,10 @@ namespace dg {
 template <typename T>
 __global__ void k_pack_traces(const T* __restrict__ u, T* __restrict__ buf, const int32_t* __restrict__ sidx,
                               int64_t nfaces, int Nfp, TileLayout L) {
-  const int64_t total = nfaces * 6 * Nfp;
+  const int64_t total = nfaces * L.nc * Nfp;
   for (int64_t w = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; w < total; w += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t g = w / (6 * Nfp);
-    const int r = int(w - g * 6 * Nfp);
+    const int64_t g = w / (L.nc * Nfp);
+    const int r = int(w - g * L.nc * Nfp);
     const int c = r / Nfp, j = r - c * Nfp;
     const int32_t si = sidx[g * Nfp + j];
     buf[w] = L.perm == 2 ? u[L.off(si >> 8, c, si & 255)] : u[si + int64_t(L.coff(c)) * L.LD];
@@ -103,7 +103,7 @@ __global__ void k_pack_traces(const T* __restrict__ u, T* __restrict__ buf, cons
 
 template <typename T>
 void pack_traces(const T* u, T* buf, const int32_t* sidx, int64_t nfaces, int Nfp, const TileLayout& L, void* st) {
-  k_pack_traces<T><<<grid_for(nfaces * 6 * Nfp), 256, 0, static_cast<cudaStream_t>(st)>>>(u, buf, sidx, nfaces, Nfp,
+  k_pack_traces<T><<<grid_for(nfaces * L.nc * Nfp), 256, 0, static_cast<cudaStream_t>(st)>>>(u, buf, sidx, nfaces, Nfp,
                                                                                           L);
 }
 template void pack_traces<double>(const double*, double*, const int32_t*, int64_t, int, const TileLayout&, void*);

@@ -39,12 +39,13 @@ constexpr int GEO_W = 26;  // 25 used (rx..tz, 4 x (n, Fscale)); padded to 16 B 
 //                    ((col/8)*(LD/4) + n/4)*32 + (col%8)*4 + n%4.
 // Padding (rows n >= Np, absent elements) is zero in every layout.
 struct TileLayout {
+  int nc = 6;  // fields per element (6 Maxwell; 4 acoustics, perm 0 only)
   int E = 1;
   int LD = 0;
   int perm = 0;
   int64_t TS = 0;
   DG_HD int col(int e, int c) const {
-    return perm == 1 ? 24 * (e >> 2) + 8 * (c >> 1) + 2 * (e & 3) + (c & 1) : 6 * e + c;
+    return perm == 1 ? 24 * (e >> 2) + 8 * (c >> 1) + 2 * (e & 3) + (c & 1) : nc * e + c;
   }
   DG_HD int coff(int c) const { return perm == 1 ? 8 * (c >> 1) + (c & 1) : c; }  // perm 0/1: col(e,c) - col(e,0)
   DG_HD int64_t inner(int cl, int n) const {  // word offset of (column, node) inside a tile
@@ -80,6 +81,7 @@ struct StageParams {
   int64_t ghost_base;  // offset of the ghost-trace region
   T rk_a, rk_b, dt, alpha;
   int first_stage;     // 1: a_s == 0, do not read res
+  int system;          // dg_system: 0 Maxwell, 1 acoustics (BASIC kernel)
 };
 
 // Launchers, one per (order, precision), defined in stage_N*.cu.

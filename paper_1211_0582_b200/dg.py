@@ -22,7 +22,8 @@ if not os.path.exists(LIB_PATH):
 lib = C.CDLL(LIB_PATH)
 
 DG_OK, DG_ERR_ARG, DG_ERR_ORDER, DG_ERR_MESH, DG_ERR_STATE, DG_ERR_CUDA, DG_ERR_NCCL, DG_ERR_OOM = range(8)
-DG_VARIANT_AUTO, DG_VARIANT_BASIC, DG_VARIANT_MMA, DG_VARIANT_MMA_WS = 0, 1, 2, 3
+DG_VARIANT_AUTO, DG_VARIANT_BASIC, DG_VARIANT_MMA, DG_VARIANT_MMA_WS, DG_VARIANT_TC = 0, 1, 2, 3, 4
+DG_SYSTEM_MAXWELL, DG_SYSTEM_ACOUSTICS = 0, 1
 STATUS_NAMES = {0: "DG_OK", 1: "DG_ERR_ARG", 2: "DG_ERR_ORDER", 3: "DG_ERR_MESH", 4: "DG_ERR_STATE",
                 5: "DG_ERR_CUDA", 6: "DG_ERR_NCCL", 7: "DG_ERR_OOM"}
 
@@ -31,7 +32,7 @@ class dg_config(C.Structure):
     _fields_ = [("order", C.c_int32), ("precision", C.c_int32), ("alpha", C.c_double),
                 ("device", C.c_int32), ("stream", C.c_void_p), ("rank", C.c_int32),
                 ("nranks", C.c_int32), ("nccl_id", C.c_void_p), ("variant", C.c_int32),
-                ("reorder", C.c_int32)]
+                ("reorder", C.c_int32), ("system", C.c_int32)]
 
 
 _P = C.c_void_p
@@ -98,15 +99,18 @@ def group_lserk_step(solvers, dt, nsteps=1):
 
 class Solver:
     """Convenience wrapper: one dg_solver.  Host arrays are numpy FP64 in the
-    C-ABI layout [6][K_local][Np]; device arrays are torch tensors (data_ptr)."""
+    C-ABI layout [nfields][K_local][Np] (6 Maxwell, 4 acoustics); device arrays are
+    torch tensors (data_ptr)."""
 
     def __init__(self, order, precision=8, alpha=1.0, device=0, stream=None, rank=0, nranks=1,
-                 nccl_id=None, variant=DG_VARIANT_AUTO, reorder=False):
+                 nccl_id=None, variant=DG_VARIANT_AUTO, reorder=False, system=DG_SYSTEM_MAXWELL):
         cfg = dg_config()
         dg_config_default(C.byref(cfg))
         cfg.order, cfg.precision, cfg.alpha, cfg.device = order, precision, alpha, device
         cfg.stream = stream
         cfg.rank, cfg.nranks, cfg.variant, cfg.reorder = rank, nranks, variant, int(bool(reorder))
+        cfg.system = system
+        self.nfields = 4 if system == DG_SYSTEM_ACOUSTICS else 6
         self._id_buf = None
         if nccl_id is not None:
             self._id_buf = C.create_string_buffer(bytes(nccl_id), 128)
@@ -149,14 +153,14 @@ class Solver:
 
     def fields_upload(self, f):
         f = np.ascontiguousarray(f, dtype=np.float64)
-        assert f.shape == (6, self.K_local, self.Np), f.shape
+        assert f.shape == (self.nfields, self.K_local, self.Np), f.shape
         check(dg_fields_upload(self.h, _ptr(f, _D)), "dg_fields_upload")
 
     def fields_upload_device(self, t):
         check(dg_fields_upload_device(self.h, C.c_void_p(t.data_ptr())), "dg_fields_upload_device")
 
     def fields_download(self, out=None):
-        out = np.empty((6, self.K_local, self.Np)) if out is None else out
+        out = np.empty((self.nfields, self.K_local, self.Np)) if out is None else out
         check(dg_fields_download(self.h, _ptr(out, _D)), "dg_fields_download")
         return out
 
@@ -164,7 +168,7 @@ class Solver:
         check(dg_fields_download_device(self.h, C.c_void_p(t.data_ptr())), "dg_fields_download_device")
 
     def rhs(self):
-        out = np.empty((6, self.K_local, self.Np))
+        out = np.empty((self.nfields, self.K_local, self.Np))
         check(dg_rhs(self.h, _ptr(out, _D)), "dg_rhs")
         return out
 

@@ -49,6 +49,15 @@ def test_argument_errors():
     with pytest.raises(DGError) as e:
         Solver(3, device=-1, rank=2, nranks=2)
     assert e.value.status == dg.DG_ERR_ARG
+    with pytest.raises(DGError) as e:
+        Solver(3, device=-1, system=2)
+    assert e.value.status == dg.DG_ERR_ARG
+    for v in (2, 3, 4):                      # acoustics: BASIC kernel only
+        with pytest.raises(DGError) as e:
+            Solver(3, precision=4, device=-1, variant=v, system=dg.DG_SYSTEM_ACOUSTICS)
+        assert e.value.status == dg.DG_ERR_ARG
+    s = Solver(3, device=-1, system=dg.DG_SYSTEM_ACOUSTICS)
+    assert s.nfields == 4
 
 
 def test_host_only_solver_refuses_compute():

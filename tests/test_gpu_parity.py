@@ -369,3 +369,88 @@ def test_convergence_study_c3(N, ns):
     assert rates[-1] >= N + 0.5, (e64, rates)
     for a, b in zip(e32, e64):
         assert abs(a - b) <= max(3e-6, 1e-3 * b), (e32, e64)
+
+
+# ------------------------------------------------------------------ NEXT-3: acoustics
+from oracle import acoustics as oac  # noqa: E402
+from paper_1211_0582_b200.dg import DG_SYSTEM_ACOUSTICS  # noqa: E402
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+@pytest.mark.parametrize("N", range(1, 10))
+def test_acoustics_rhs_and_steps(N, prec):
+    # the second linear system through the same BASIC stage kernel (dg_system = 1):
+    # RHS and 2 LSERK4 steps vs the acoustics oracle on a shuffled/rotated/jittered mesh
+    VX, E = mesh(3, 1, 2, 3)
+    st = setup("m3", VX, E, N)
+    U = di.random_fields(st.K, N, seed=2, nfields=4)
+    s = Solver(N, precision=prec, system=DG_SYSTEM_ACOUSTICS)
+    s.mesh_upload(VX, E)
+    s.fields_upload(U)
+    assert relerr(s.rhs(), oac.rhs(st, U)) < TOL_RHS[prec]
+    dt = di.dt_rule(VX, E, N)
+    s.lserk_step(dt, 2)
+    assert relerr(s.fields_download(), oac.lserk4(st, U, dt, 2)) < TOL_STEP[prec]
+    s.close()
+
+
+def test_acoustics_alpha0_energy_and_partitions():
+    N = 3
+    VX, E = mesh(4, 41, 42, 43)
+    st = setup("m4", VX, E, N)
+    K = st.K
+    U0 = di.random_fields(K, N, seed=8, nfields=4)
+    dt = di.dt_rule(VX, E, N)
+    s = Solver(N, alpha=0.0, system=DG_SYSTEM_ACOUSTICS)
+    s.mesh_upload(VX, E)
+    s.fields_upload(U0)
+    assert relerr(s.rhs(), oac.rhs(st, U0, alpha=0.0)) < 1e-12
+    s.lserk_step(dt, 20)
+    U = s.fields_download()
+    s.close()
+    e0 = oac.energy(st, U0)
+    assert abs(oac.energy(st, U) - e0) / e0 < 1e-5
+    assert relerr(U, oac.lserk4(st, U0, dt, 20, alpha=0.0)) < 1e-11
+    # 3 loopback partitions (4-field ghost records): bitwise equal to one solver
+    ref = Solver(N, system=DG_SYSTEM_ACOUSTICS)
+    ref.mesh_upload(VX, E)
+    ref.fields_upload(U0)
+    ref.lserk_step(dt, 3)
+    Uref = ref.fields_download()
+    ref.close()
+    part = np.random.default_rng(3).integers(0, 3, K).astype(np.int32)
+    solvers, ids = [], []
+    for r in range(3):
+        sv = Solver(N, rank=r, nranks=3, system=DG_SYSTEM_ACOUSTICS)
+        sv.mesh_upload(VX, E, part)
+        ids.append(sv.local_elements())
+        sv.fields_upload(U0[:, ids[-1]])
+        solvers.append(sv)
+    group_lserk_step(solvers, dt, 3)
+    Up = np.empty_like(U0)
+    for sv, ix in zip(solvers, ids):
+        Up[:, ix] = sv.fields_download()
+        sv.close()
+    assert np.array_equal(Up, Uref)
+
+
+@pytest.mark.parametrize("N", [2, 4])
+def test_acoustics_convergence_rigid_wall_mode(N):
+    import math
+    T = 0.25
+    errs = []
+    for n in (2, 4, 8):
+        VX, E = di.kuhn_box(n)
+        s = Solver(N, system=DG_SYSTEM_ACOUSTICS)
+        s.mesh_upload(VX, E)
+        x, y, z = s.get_nodes()
+        dt0 = di.dt_rule(VX, E, N)
+        steps = int(math.ceil(T / dt0))
+        s.fields_upload(di.acoustic_mode(x, y, z))
+        s.lserk_step(T / steps, steps)
+        D = s.fields_download() - di.acoustic_mode(x, y, z, t=T)
+        s.close()
+        st = setup(f"cavity{n}", VX, E, N)
+        errs.append(math.sqrt(2 * oac.energy(st, D)))
+    rates = [math.log2(errs[i] / errs[i + 1]) for i in range(len(errs) - 1)]
+    assert rates[-1] >= N + 0.5, (errs, rates)
