@@ -46,10 +46,17 @@ def flops_per_elem_stage(N):
     return 36 * Np * Np + 48 * Np * Nfp + 102 * Np + 256 * Nfp
 
 
-def bytes_per_elem_stage(N, w):
+def flops_per_elem_stage_acoustics(N):
+    """Acoustics (NEXT-3) analogue of F(N): volume 3 x 4 fields x 2Np^2, lift 4 fields x
+    2 Np 4Nfp, chain rule + div/grad 32Np, update 16Np, flux 20 per face node."""
+    Np, Nfp = di.np_of(N), di.nfp_of(N)
+    return 24 * Np * Np + 32 * Np * Nfp + 48 * Np + 80 * Nfp
+
+
+def bytes_per_elem_stage(N, w, nfields=6):
     """B(N): fused-stage algorithmic HBM bytes per element:
     u in, res in, res out, u out (24 Np words) + 25 geometry words + 20 B connectivity."""
-    return w * (24 * di.np_of(N) + 25) + 20
+    return w * (4 * nfields * di.np_of(N) + 25) + 20
 
 
 def load_peaks():
@@ -87,6 +94,8 @@ def ws_kind(N, prec, variant):
         return "mma" if prec == 8 else "basic"
     if variant == 3:
         return "ws"
+    if prec == 8 and N in (1, 6):
+        return "mma"
     return "basic" if (prec == 4 and N == 1) else "ws"
 
 
@@ -102,14 +111,14 @@ def load_traffic(N, prec, variant, K):
         return None
 
 
-def roofline(N, prec, K_total, kernel_ms, peaks, variant=0, traffic=None):
+def roofline(N, prec, K_total, kernel_ms, peaks, variant=0, traffic=None, fpe=None, bpe=None):
     """Roofline of the fused stage kernel.  FP64 MMA/WS variants: contractions on the
     FP64 tensor pipe (DMMA) -> bound "tensor" against the measured DMMA peak.  FP32
     WS variant: 3xTF32 on HMMA -> "tensor" against the measured TF32 mma.sync peak / 3
     (algorithmic flops counted once).  BASIC: "alu" against measured DFMA / FFMA."""
     w = 8 if prec == 8 else 4
-    F = flops_per_elem_stage(N) * K_total
-    B = bytes_per_elem_stage(N, w) * K_total
+    F = (fpe or flops_per_elem_stage(N)) * K_total
+    B = (bpe or bytes_per_elem_stage(N, w)) * K_total
     kind = ws_kind(N, prec, variant)
     tensor = kind != "basic"
     if prec == 8:
@@ -209,11 +218,13 @@ def run_dg(args, N, prec, rank, world, local, dist, stream, flush, nccl_id, peak
     if args.shuffle_seed is not None:
         E, _ = di.shuffle_elements(E, args.shuffle_seed)
     K_total = E.shape[0]
+    system = getattr(args, "system", 0)
+    nf = 4 if system == 1 else 6
     s = Solver(N, precision=prec, device=local, stream=stream.cuda_stream, rank=rank, nranks=world,
-               nccl_id=nccl_id, variant=args.variant, reorder=args.reorder)
+               nccl_id=nccl_id, variant=args.variant, reorder=args.reorder, system=system)
     s.mesh_upload(VX, E)
     Kl = s.K_local
-    U0 = di.random_fields(K_total, N, seed=0)[:, s.local_elements()]
+    U0 = di.random_fields(K_total, N, seed=0, nfields=nf)[:, s.local_elements()]
     s.fields_upload(U0)
     dt = di.dt_rule(VX, E, N)
     with torch.cuda.stream(stream):
@@ -241,20 +252,27 @@ def run_dg(args, N, prec, rank, world, local, dist, stream, flush, nccl_id, peak
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
     Np = di.np_of(N)
-    dofs = 6 * Np * K_total
+    dofs = nf * Np * K_total
+    fpe = flops_per_elem_stage_acoustics(N) if system == 1 else flops_per_elem_stage(N)
     res = {"N": N, "precision": "f64" if prec == 8 else "f32", "K_total": K_total, "K_local": Kl,
            "ms_per_step": round(ms_step, 5), "dof_updates_per_s": dofs / (ms_step * 1e-3),
-           "gflops": 5 * K_total * flops_per_elem_stage(N) / (ms_step * 1e-3) / 1e9,
+           "gflops": 5 * K_total * fpe / (ms_step * 1e-3) / 1e9,
            "launches_per_step": s.launches_per_step()}
     # dominant kernel: the fused stage kernel (5 launches per step, the step's only kernel at 1 GPU)
     kernel_ms = ms_step / 5 if world == 1 else s.time_stage_kernel(10)
     res["stage_kernel_ms"] = round(kernel_ms, 5)
-    res["roofline"] = roofline(N, prec, Kl, kernel_ms, peaks, args.variant,
-                               traffic=load_traffic(N, prec, args.variant, Kl) if world == 1 else None)
+    if system == 1:
+        # acoustics runs on the BASIC kernel (FMA contractions): alu or hbm by its own F/B
+        res["system"] = "acoustics"
+        res["roofline"] = roofline(N, prec, Kl, kernel_ms, peaks, 1, None, fpe,
+                                   bytes_per_elem_stage(N, 8 if prec == 8 else 4, 4))
+    else:
+        res["roofline"] = roofline(N, prec, Kl, kernel_ms, peaks, args.variant,
+                                   traffic=load_traffic(N, prec, args.variant, Kl) if world == 1 else None)
     if e2e:
         # end to end through the C ABI with HOST buffers: upload (pinned H2D) + step + download (D2H)
         host_in = torch.from_numpy(np.ascontiguousarray(U0)).pin_memory().numpy()
-        host_out = torch.empty((6, Kl, Np), dtype=torch.float64).pin_memory().numpy()
+        host_out = torch.empty((nf, Kl, Np), dtype=torch.float64).pin_memory().numpy()
         s.fields_upload(host_in)
         s.lserk_step(dt, 1)
         s.fields_download(host_out)
@@ -366,6 +384,15 @@ def main():
                 for n_ in range(1, 10):
                     r = run_dg(args, n_, p, rank, world, local, dist, stream, flush, nccl_id, peaks)
                     sweep.append({k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()})
+        acoustics = []
+        if not args.no_sweep:
+            # NEXT-3: the second linear system on the same C2 mesh (BASIC kernel, 4 fields)
+            import copy
+            a3 = copy.copy(args)
+            a3.system, a3.variant = 1, 0
+            for p in (8, 4):
+                r = run_dg(a3, 4, p, rank, world, local, dist, stream, flush, nccl_id, peaks)
+                acoustics.append({k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()})
         large = None
         if not args.no_large and world == 1:
             # configs[3] at one GPU: Kuhn n=56, K = 1 053 696 (state 1.8 GB >> 126 MB L2), N=4 FP64
@@ -398,7 +425,7 @@ def main():
                     "stage_kernel_ms": head["stage_kernel_ms"],
                     "clocks": clocks, "cpu_baseline": cpu,
                     "peaks": {k: v for k, v in peaks.items()},
-                    "sweep": sweep, "large": large})
+                    "sweep": sweep, "acoustics": acoustics, "large": large})
         print(json.dumps(out), flush=True)
     if dist:
         dist.barrier()

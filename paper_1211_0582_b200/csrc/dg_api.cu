@@ -153,10 +153,12 @@ void release_device(dg_solver* s) {
 }
 
 // DG_VARIANT_AUTO: the measured-best kernel per (precision, order) on the bench
-// config (bench.py sweep): FP64 -> MMA_WS for all N; FP32 -> BASIC at N = 1
-// (HBM-bound, smallest tiles win), MMA_WS (3xTF32) otherwise.
+// config (NEXT-4 sweep, tools/variant_sweep.py, profiles/r1_pdl_sweep.jsonl):
+// FP64 -> MMA at N = 1 and 6, MMA_WS otherwise; FP32 -> BASIC at N = 1 (HBM-bound,
+// smallest tiles win), MMA_WS (3xTF32) otherwise.
 int auto_variant(bool fp64, int N) {
   if (!fp64 && N == 1) return DG_VARIANT_BASIC;
+  if (fp64 && (N == 1 || N == 6)) return DG_VARIANT_MMA;
   return DG_VARIANT_MMA_WS;
 }
 

@@ -30,6 +30,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include "pdl.cuh"
 #include "stage_basic.cuh"
 
 namespace dg {
@@ -98,6 +99,7 @@ __global__ void __launch_bounds__(MmaCfg<N>::NT)
   constexpr int E = C::E, LDU = C::LDU, LDF = C::LDF, NT = C::NT;
   extern __shared__ __align__(16) double smem_mma[];
   double* smem = smem_mma;
+  pdl_trigger();
   double* sU0 = smem;
   double* sU1 = sU0 + C::U_SZ;
   double* sR = sU1 + C::U_SZ;                  // residual of the current tile [P][LDU]
@@ -195,6 +197,7 @@ __global__ void __launch_bounds__(MmaCfg<N>::NT)
     }
   }
 
+  pdl_wait();  // the previous stage's fields are complete from here on
   int64_t tile = blockIdx.x;
   if (tile < ntiles) {
     issue_tile(tile, sU0, sG0, sI0);
@@ -402,9 +405,9 @@ void launch_stage_mma(const StageParams<double>& p, const double* opsA, int mode
   const int64_t ntiles = (p.K + C::E - 1) / C::E;
   const unsigned grid = unsigned(ntiles < grid_max ? ntiles : grid_max);
   if (mode == 1)
-    dg_stage_mma<N, true><<<grid, C::NT, C::SMEM_BYTES, st>>>(p, opsA);
+    launch_pdl(N >= 3, dg_stage_mma<N, true>, grid, C::NT, C::SMEM_BYTES, st, p, opsA);
   else
-    dg_stage_mma<N, false><<<grid, C::NT, C::SMEM_BYTES, st>>>(p, opsA);
+    launch_pdl(N >= 3, dg_stage_mma<N, false>, grid, C::NT, C::SMEM_BYTES, st, p, opsA);
 }
 
 }  // namespace dg

@@ -14,15 +14,16 @@
 //
 // Warp roles (one persistent CTA per SM, S-slot smem ring, mbarrier handshakes):
 //   warp 0            TMA loader (lane 0): U, residual, geometry, gather indices
-//   warps 1..4        flux: cp.async trace gather (LA tiles ahead) -> upwind/PEC flux
-//                     in place (a2+a3) -> B_lo splits of U and Flux -> fence.proxy.async
-//                     -> full[s]
-//   warp 5            TMEM allocator + MMA issuer (lane 0): 3 x (KV/8 + KL/8)
+//   warps 1..8        flux (PW = 8): cp.async trace gather (LA tiles ahead) -> upwind/PEC
+//                     flux in place (a2+a3) -> B_lo splits of U and Flux ->
+//                     fence.proxy.async -> full[s]
+//   warp 9            TMEM allocator + MMA issuer (lane 0): 3 x (KV/8 + KL/8)
 //                     tcgen05.mma per tile into a double-buffered accumulator,
 //                     tcgen05.commit -> acc_full[a]
-//   warps 6..9        epilogue (one per TMEM lane quarter): tcgen05.ld rows -> smem,
-//                     then per (node, element): chain rule + curl + lift + LSERK update
-//                     (a5), release acc_empty[a] and the ring slot empty[s].
+//   warps 10..17      epilogue (EW = 8, two per TMEM lane quarter): tcgen05.ld rows ->
+//                     smem staging (Y_V, Y_L), then per (node, element): chain rule +
+//                     curl + lift + LSERK update (a5) into smem, bulk store of the
+//                     u_out / res tiles, release acc_empty[a] and the ring slot empty[s].
 #pragma once
 #include <cuda_runtime.h>
 
@@ -124,6 +125,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
   constexpr int S = C::S, TS = C::TS;
   extern __shared__ __align__(1024) unsigned char smem_tc[];
   unsigned char* smem = smem_tc;
+  pdl_trigger();
   auto sU = [&](int s) { return reinterpret_cast<float*>(smem + size_t(s) * C::SLOT + C::OFF_U); };
   auto sUL = [&](int s) { return reinterpret_cast<float*>(smem + size_t(s) * C::SLOT + C::OFF_UL); };
   auto sR = [&](int s) { return reinterpret_cast<float*>(smem + size_t(s) * C::SLOT + C::OFF_R); };
@@ -182,6 +184,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // the previous stage's fields are complete from here on
 
   if (warp == C::W_LOAD) {
     // ============================ loader ============================
@@ -500,9 +503,9 @@ void launch_stage_tc(const StageParams<float>& p, const float* opsA, int mode, c
   const int64_t tc = (p.k_begin + p.K + C::E - 1) / C::E - t0;
   const unsigned grid = unsigned(tc < sms ? tc : sms);
   if (mode == 1)
-    dg_stage_tc<N, true><<<grid, C::NT, C::SMEM_BYTES, st>>>(p, opsA, t0, tc);
+    launch_pdl(true, dg_stage_tc<N, true>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc);
   else
-    dg_stage_tc<N, false><<<grid, C::NT, C::SMEM_BYTES, st>>>(p, opsA, t0, tc);
+    launch_pdl(true, dg_stage_tc<N, false>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc);
 }
 
 template <int N>

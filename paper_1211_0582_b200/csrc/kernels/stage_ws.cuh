@@ -48,8 +48,27 @@ struct WsCfg {
   static constexpr int LDL = ldx(NF);
   // per-order configuration: tile size, ring depth, warp roles,
   // operator residency, residual staging
-  static constexpr int E = N == 1 ? 32 : N == 2 ? 16 : N == 3 ? 8 : 4;
-  static constexpr int S = N == 2 ? 4 : N <= 4 ? 5 : N == 5 ? 3 : N == 6 ? 5 : N == 7 ? 4 : N == 8 ? 3 : 2;
+  // tuning builds (tools/tune_ws.sh, NEXT-4): -DDG_WS_TUNE_N=n -DDG_WS_E=e -DDG_WS_S=s override
+  // the tile size / ring depth of order n only
+#ifdef DG_WS_TUNE_N
+  static constexpr bool TUNED = N == DG_WS_TUNE_N;
+#else
+  static constexpr bool TUNED = false;
+#endif
+#ifdef DG_WS_E
+  static constexpr int E_TUNE = DG_WS_E;
+#else
+  static constexpr int E_TUNE = 0;
+#endif
+#ifdef DG_WS_S
+  static constexpr int S_TUNE = DG_WS_S;
+#else
+  static constexpr int S_TUNE = 0;
+#endif
+  // measured (NEXT-4 sweep, profiles/r1_tile_sweep.jsonl): N=3 E=4/S=8 beats E=8/S=5 by 6 %
+  static constexpr int E = (TUNED && E_TUNE) ? E_TUNE : N == 1 ? 32 : N == 2 ? 16 : 4;
+  static constexpr int S = (TUNED && S_TUNE) ? S_TUNE
+                           : N == 2 ? 4 : N == 3 ? 8 : N == 4 ? 5 : N == 5 ? 3 : N == 6 ? 3 : N == 7 ? 4 : N == 8 ? 3 : 2;
   static constexpr int LA = S - 2 < 2 ? S - 2 : 2;  // trace gathers issued LA tiles ahead of the flux
   static constexpr bool OPS_SMEM = N <= 5;
   static constexpr bool RES_SMEM = N <= 4;
@@ -158,6 +177,7 @@ __global__ void __launch_bounds__(WsCfg<N>::NT, 1)
   constexpr int E = C::E, LD = C::LD, LDF = C::LDF, S = C::S, TS = C::TS;
   extern __shared__ __align__(128) unsigned char smem_ws[];
   unsigned char* smem = smem_ws;
+  pdl_trigger();
   double* sA = reinterpret_cast<double*>(smem + size_t(S) * C::SLOT);
   int16_t* sFm = reinterpret_cast<int16_t*>(smem + size_t(S) * C::SLOT + C::A_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(S) * C::SLOT + C::A_BYTES + C::FM_BYTES);
@@ -206,6 +226,7 @@ __global__ void __launch_bounds__(WsCfg<N>::NT, 1)
     cp_wait<0>();
   }
   __syncthreads();
+  pdl_wait();  // the previous stage's fields are complete from here on
 
   if (warp == C::MW) {
     // ====================== TMA loader warp (one lane) ======================
@@ -502,9 +523,9 @@ void launch_stage_ws(const StageParams<double>& p, const double* opsA, int mode,
   const int64_t tc = (p.k_begin + p.K + C::E - 1) / C::E - t0;
   const unsigned grid = unsigned(tc < sms ? tc : sms);
   if (mode == 1)
-    dg_stage_ws<N, true><<<grid, C::NT, C::SMEM_BYTES, st>>>(p, opsA, t0, tc);
+    launch_pdl(true, dg_stage_ws<N, true>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc);
   else
-    dg_stage_ws<N, false><<<grid, C::NT, C::SMEM_BYTES, st>>>(p, opsA, t0, tc);
+    launch_pdl(true, dg_stage_ws<N, false>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc);
 }
 
 #ifdef DG_WS_PROFILE

@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
   constexpr int E = C::E, LD = C::LD, LDF = C::LDF, S = C::S, TS = C::TS;
   extern __shared__ __align__(128) unsigned char smem_ws32[];
   unsigned char* smem = smem_ws32;
+  pdl_trigger();
   float* sA = reinterpret_cast<float*>(smem + size_t(S) * C::SLOT);  // hi then lo
   int16_t* sFm = reinterpret_cast<int16_t*>(smem + size_t(S) * C::SLOT + C::A_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(S) * C::SLOT + C::A_BYTES + C::FM_BYTES);
@@ -149,6 +150,7 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
     }
   }
   __syncthreads();
+  pdl_wait();  // the previous stage's fields are complete from here on
 
   if (warp == C::MW) {
     // ===================== TMA loader warp (one lane) =====================
@@ -418,9 +420,9 @@ void launch_stage_ws32(const StageParams<float>& p, const float* opsA, int mode,
   const int64_t tc = (p.k_begin + p.K + C::E - 1) / C::E - t0;
   const unsigned grid = unsigned(tc < sms ? tc : sms);
   if (mode == 1)
-    dg_stage_ws32<N, true><<<grid, C::NT, C::SMEM_BYTES, st>>>(p, opsA, t0, tc);
+    launch_pdl(true, dg_stage_ws32<N, true>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc);
   else
-    dg_stage_ws32<N, false><<<grid, C::NT, C::SMEM_BYTES, st>>>(p, opsA, t0, tc);
+    launch_pdl(true, dg_stage_ws32<N, false>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc);
 }
 
 template <int N>
