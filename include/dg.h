@@ -75,8 +75,12 @@ typedef enum {
                             (FP32: same as BASIC) */
   DG_VARIANT_MMA_WS = 3, /* warp-specialized TMA/mbarrier pipeline; contractions on tensor
                             cores: FP64 DMMA, FP32 3xTF32 HMMA */
-  DG_VARIANT_TC = 4      /* FP32, N <= 4: tcgen05.mma kind::tf32 (3xTF32) with TMEM
+  DG_VARIANT_TC = 4,     /* FP32, N <= 4: tcgen05.mma kind::tf32 (3xTF32) with TMEM
                             accumulators (5th-generation tensor cores) */
+  DG_VARIANT_FUSED = 5   /* FP64, single rank: the MMA_WS kernel running all 5 x nsteps stages of a
+                            dg_lserk_step call in ONE persistent launch, tiles ordered by per-tile
+                            completion counters instead of kernel boundaries.  Bitwise equal to
+                            MMA_WS; measured slower on B200, hence not AUTO */
 } dg_variant;
 
 /* The linear hyperbolic system u_t + div F(u) = 0 the operator is
@@ -114,7 +118,8 @@ DG_API void dg_config_default(dg_config* cfg);
 
 /* Create a solver.  Builds the reference element of order N on the host (FP64).
  * Errors: DG_ERR_ARG (null, precision not 4/8, nranks < 1, rank out of range, bad
- * variant), DG_ERR_ORDER, DG_ERR_CUDA (device unusable), DG_ERR_NCCL. */
+ * variant or variant/system/precision/rank combination), DG_ERR_ORDER, DG_ERR_CUDA
+ * (device unusable), DG_ERR_NCCL. */
 DG_API dg_status dg_create(const dg_config* cfg, dg_solver** out);
 
 /* Upload the (global) mesh: nv vertices VX[nv][3] (FP64), K tets EToV[K][4]

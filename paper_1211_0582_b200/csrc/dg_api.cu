@@ -2,7 +2,9 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -105,6 +107,13 @@ struct dg_solver {
   int16_t* d_fmask = nullptr;
   void* d_send = nullptr;      // [n_ghost][nc][Nfp]
   int32_t* d_sidx = nullptr;   // [n_ghost][Nfp] element-node offsets for packing
+  // stage-fused launches (single rank, FP64 MMA_WS): per-tile completed-stage counters and
+  // the tile dependency lists (kernels/stage_params.h FusedParams)
+  bool fused = false;
+  unsigned* d_flags = nullptr;
+  int32_t* d_nbr_off = nullptr;
+  int32_t* d_nbr = nullptr;
+  unsigned stage_count = 0;    // stages completed since the last field upload
   cudaStream_t stream = nullptr, comm = nullptr;
   bool own_stream = false;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
@@ -150,7 +159,13 @@ void release_device(dg_solver* s) {
   p = s->d_fmask; free_dev(p); s->d_fmask = nullptr;
   free_dev(s->d_send);
   p = s->d_sidx; free_dev(p); s->d_sidx = nullptr;
+  p = s->d_flags; free_dev(p); s->d_flags = nullptr;
+  p = s->d_nbr_off; free_dev(p); s->d_nbr_off = nullptr;
+  p = s->d_nbr; free_dev(p); s->d_nbr = nullptr;
+  s->fused = false;
 }
+
+
 
 // DG_VARIANT_AUTO: the measured-best kernel per (precision, order) on the bench
 // config (NEXT-4 sweep, tools/variant_sweep.py, profiles/r1_pdl_sweep.jsonl):
@@ -440,7 +455,70 @@ dg_status upload_setup(dg_solver* s) {
     CK(cudaMalloc((void**)&s->d_sidx, sidx.size() * sizeof(int32_t)));
     CK(cudaMemcpy(s->d_sidx, sidx.data(), sidx.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   }
+  if (sizeof(T) == 8 && s->cfg.variant == DG_VARIANT_FUSED && P.n_ghost_faces == 0 && dg::fused_launcher_f64(s->N)) {
+    // tile dependency lists: the tiles holding a face neighbour of any element of the tile, and itself
+    const int64_t ntl = s->ntiles, E = s->lay.E;
+    std::vector<int32_t> off(size_t(ntl) + 1, 0), lst;
+    std::vector<int32_t> tmp;
+    for (int64_t t = 0; t < ntl; ++t) {
+      tmp.clear();
+      tmp.push_back(int32_t(t));
+      for (int64_t l = t * E; l < std::min((t + 1) * E, Kl); ++l) {
+        const int64_t k = P.local_ids[l];
+        for (int f = 0; f < 4; ++f) {
+          const int64_t k2 = m.EToE[4 * k + f];
+          if (k2 == k) continue;
+          tmp.push_back(int32_t(P.g2l[k2] / E));
+        }
+      }
+      std::sort(tmp.begin(), tmp.end());
+      tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+      lst.insert(lst.end(), tmp.begin(), tmp.end());
+      off[t + 1] = int32_t(lst.size());
+    }
+    CK(cudaMalloc((void**)&s->d_flags, std::max<int64_t>(ntl, 1) * sizeof(unsigned)));
+    CK(cudaMemsetAsync(s->d_flags, 0, std::max<int64_t>(ntl, 1) * sizeof(unsigned), s->stream));
+    CK(cudaMalloc((void**)&s->d_nbr_off, off.size() * sizeof(int32_t)));
+    CK(cudaMemcpy(s->d_nbr_off, off.data(), off.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    CK(cudaMalloc((void**)&s->d_nbr, std::max<size_t>(lst.size(), 1) * sizeof(int32_t)));
+    CK(cudaMemcpy(s->d_nbr, lst.data(), lst.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    s->fused = true;
+    s->stage_count = 0;
+  }
   CK(cudaStreamSynchronize(s->stream));
+  return DG_OK;
+}
+
+// All nsteps LSERK4 steps as one stage-fused launch (kernels/stage_ws.cuh, FUSED).
+dg_status fused_steps(dg_solver* s, double dt, int nsteps) {
+  if (nsteps <= 0) return DG_OK;
+  dg::StageParams<double> p = base_params<double>(s);
+  dg::FusedParams<double> fp{};
+  fp.u[0] = static_cast<double*>(s->d_u[0]);
+  fp.u[1] = static_cast<double*>(s->d_u[1]);
+  fp.par0 = s->cur;
+  fp.nst = 5 * nsteps;
+  fp.stage0 = 0;
+  fp.g0 = s->stage_count;
+  fp.flags = s->d_flags;
+  fp.nbr_off = s->d_nbr_off;
+  fp.nbr = s->d_nbr;
+  for (int i = 0; i < 5; ++i) {
+    fp.rk_a[i] = kRkA[i];
+    fp.rk_b[i] = kRkB[i];
+  }
+  p.u_in = fp.u[s->cur];
+  p.u_out = fp.u[s->cur ^ 1];
+  p.res = static_cast<double*>(s->d_res);
+  p.dt = dt;
+  p.first_stage = 1;
+  if (!dg::fused_launcher_f64(s->N)(p, fp, s->stream)) {
+    cudaGetLastError();
+    return fail(DG_ERR_CUDA, "stage-fused cooperative launch refused (use DG_VARIANT_MMA_WS)");
+  }
+  CK(cudaGetLastError());
+  s->stage_count += unsigned(fp.nst);
+  s->cur = (s->cur + fp.nst) & 1;
   return DG_OK;
 }
 
@@ -470,6 +548,7 @@ dg_status capture_step(dg_solver* s, int parity, double dt) {
 
 template <typename T>
 dg_status lserk_steps(dg_solver* s, double dt, int nsteps) {
+  if (sizeof(T) == 8 && s->fused) return fused_steps(s, dt, nsteps);
   for (int n = 0; n < nsteps; ++n) {
     const int par = s->cur;
     if (!s->graph[par] || s->graph_dt[par] != dt) {
@@ -552,7 +631,9 @@ dg_status dg_create(const dg_config* cfg, dg_solver** out) {
   if (cfg->order < 1 || cfg->order > 9) return fail(DG_ERR_ORDER, "order N must be in 1..9");
   if (cfg->precision != 4 && cfg->precision != 8) return fail(DG_ERR_ARG, "precision must be 4 or 8");
   if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return fail(DG_ERR_ARG, "bad rank/nranks");
-  if (cfg->variant < 0 || cfg->variant > 4) return fail(DG_ERR_ARG, "bad variant");
+  if (cfg->variant < 0 || cfg->variant > 5) return fail(DG_ERR_ARG, "bad variant");
+  if (cfg->variant == DG_VARIANT_FUSED && (cfg->precision != 8 || cfg->nranks != 1))
+    return fail(DG_ERR_ARG, "DG_VARIANT_FUSED is the single-rank FP64 stage-fused WS kernel");
   if (cfg->variant == DG_VARIANT_TC && (cfg->precision != 4 || cfg->order > 4))
     return fail(DG_ERR_ARG, "DG_VARIANT_TC is the FP32 tcgen05 kernel for N <= 4");
   if (cfg->system != DG_SYSTEM_MAXWELL && cfg->system != DG_SYSTEM_ACOUSTICS) return fail(DG_ERR_ARG, "bad system");
@@ -566,6 +647,7 @@ dg_status dg_create(const dg_config* cfg, dg_solver** out) {
   s->nc = cfg->system == DG_SYSTEM_ACOUSTICS ? 4 : 6;
   s->variant = cfg->system == DG_SYSTEM_ACOUSTICS ? DG_VARIANT_BASIC
                : cfg->variant == DG_VARIANT_AUTO  ? auto_variant(cfg->precision == 8, cfg->order)
+               : cfg->variant == DG_VARIANT_FUSED ? DG_VARIANT_MMA_WS  // same kernel and layout
                                                   : cfg->variant;
   s->host_only = cfg->device < 0;
   try {
@@ -673,6 +755,10 @@ static dg_status upload_common(dg_solver* s, const void* src, bool from_host) {
   }
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(s->d_res, 0, std::max<int64_t>(s->ntiles * s->lay.TS, 1) * s->wsize, s->stream));
+  if (s->fused) {
+    CK(cudaMemsetAsync(s->d_flags, 0, std::max<int64_t>(s->ntiles, 1) * sizeof(unsigned), s->stream));
+    s->stage_count = 0;
+  }
   if (from_host) CK(cudaStreamSynchronize(s->stream));
   s->has_fields = true;
   return DG_OK;
@@ -835,7 +921,9 @@ dg_status dg_time_stage_kernel(dg_solver* s, int32_t reps, double* ms) {
 dg_status dg_launches_per_step(dg_solver* s, int32_t* n) {
   if (!s || !n) return fail(DG_ERR_ARG, "null argument");
   const bool halo = s->has_mesh && s->part.n_ghost_faces > 0;
-  *n = 5 * (halo ? 3 : 1);  // per stage: stage kernel (+ pack kernel + second stage range)
+  // stage-fused: one launch per dg_lserk_step call; otherwise per stage: stage kernel
+  // (+ pack kernel + second stage range)
+  *n = s->fused ? 1 : 5 * (halo ? 3 : 1);
   return DG_OK;
 }
 

@@ -33,6 +33,9 @@ void ws32_ops_N1(const double* Dr, const double* Ds, const double* Dt, const dou
 }
 
 TileLayout ws_layout_N1() { return ws_layout<1>(); }
+bool launch_fused_f64_N1(const StageParams<double>& p, const FusedParams<double>& fp, void* st) {
+  return launch_stage_ws_fused<1>(p, p.ops_pad, fp, static_cast<cudaStream_t>(st));
+}
 
 #ifdef DG_WS_PROFILE
 void ws_prof_N1(unsigned long long* out, int reset) {

@@ -29,6 +29,9 @@ void ws32_ops_N6(const double* Dr, const double* Ds, const double* Dt, const dou
 }
 
 TileLayout ws_layout_N6() { return ws_layout<6>(); }
+bool launch_fused_f64_N6(const StageParams<double>& p, const FusedParams<double>& fp, void* st) {
+  return launch_stage_ws_fused<6>(p, p.ops_pad, fp, static_cast<cudaStream_t>(st));
+}
 
 #ifdef DG_WS_PROFILE
 void ws_prof_N6(unsigned long long* out, int reset) {

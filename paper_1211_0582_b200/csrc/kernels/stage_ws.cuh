@@ -69,7 +69,15 @@ struct WsCfg {
   static constexpr int E = (TUNED && E_TUNE) ? E_TUNE : N == 1 ? 32 : N == 2 ? 16 : 4;
   static constexpr int S = (TUNED && S_TUNE) ? S_TUNE
                            : N == 2 ? 4 : N == 3 ? 8 : N == 4 ? 5 : N == 5 ? 3 : N == 6 ? 3 : N == 7 ? 4 : N == 8 ? 3 : 2;
-  static constexpr int LA = S - 2 < 2 ? S - 2 : 2;  // trace gathers issued LA tiles ahead of the flux
+#ifdef DG_WS_LA
+  static constexpr int LA_TUNE = DG_WS_LA;
+#else
+  static constexpr int LA_TUNE = 0;
+#endif
+  // trace gathers issued LA tiles ahead of the flux (LA <= S - 2: the slot of tile j+LA
+  // must have been released by the MMA warps, which may still be on tile j-1)
+  static constexpr int LA = (TUNED && LA_TUNE) ? LA_TUNE : S - 2 < 2 ? S - 2 : 2;
+  static_assert(LA <= S - 2 || S <= 2, "look-ahead beyond the ring");
   static constexpr bool OPS_SMEM = N <= 5;
   static constexpr bool RES_SMEM = N <= 4;
   // warp roles (measured, tools/tune_ws.sh): >= 2 MMA warps per SMSP so one's epilogue hides
@@ -100,7 +108,10 @@ struct WsCfg {
   static constexpr int SLOT = OFF_F + r16(6 * E * LDF * 8);
   static constexpr int A_BYTES = OPS_SMEM ? r16((3 * M8 * LDA + M8 * LDL) * 8) : 0;
   static constexpr int FM_BYTES = r16(NF * 2);
-  static constexpr int BAR_BYTES = 4 * S * 8;
+  static constexpr int NTF = NT + 32;  // fused launches: + one publisher warp
+  static constexpr int VB = 8;         // fused: tiles verified per dependency poll round
+  // mbarriers load/tr/full/empty [S] (+ fused: done[2S], published counter, verify flags)
+  static constexpr int BAR_BYTES = 6 * S * 8 + 16 + r16(VB * 4);
   static constexpr size_t SMEM_BYTES = size_t(S) * SLOT + A_BYTES + FM_BYTES + BAR_BYTES;
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   static_assert(E % 4 == 0, "tile = whole 4-element column groups");
@@ -131,6 +142,32 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
 }
 __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* b) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* b, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n.reg .pred P1;\n"
+      "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -169,9 +206,13 @@ __device__ unsigned long long g_ws_prof[16];
 // ---------------------------------------------------------------- kernel
 // Tiles [t_begin, t_begin + t_count) of the tiled arrays; p.k_begin/p.K give the
 // element range (tile-aligned start) used to count elements in the last tile.
-template <int N, bool UPDATE>
-__global__ void __launch_bounds__(WsCfg<N>::NT, 1)
-    dg_stage_ws(const StageParams<double> p, const double* __restrict__ opsA, int64_t t_begin, int64_t t_count) {
+// FUSED: one launch runs fp.nst LSERK stages (StageParams supplies the geometry, indices
+// and operators; FusedParams the buffers, coefficients and tile dependencies).  The
+// ring position jj = g * J + j walks stage g's tiles j = 0..J-1 of this CTA.
+template <int N, bool UPDATE, bool FUSED>
+__global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
+    dg_stage_ws(const StageParams<double> p, const double* __restrict__ opsA, int64_t t_begin, int64_t t_count,
+                const FusedParams<double> fp) {
   using C = WsCfg<N>;
   constexpr int Np = C::Np, Nfp = C::Nfp, NF = C::NF, M8 = C::M8, KV = C::KV, KL = C::KL;
   constexpr int E = C::E, LD = C::LD, LDF = C::LDF, S = C::S, TS = C::TS;
@@ -185,6 +226,10 @@ __global__ void __launch_bounds__(WsCfg<N>::NT, 1)
   uint64_t* bar_tr = bars + S;
   uint64_t* bar_full = bars + 2 * S;
   uint64_t* bar_empty = bars + 3 * S;
+  uint64_t* bar_done = bars + 4 * S;  // fused [2S]: MMA warps done with tile jj (-> publisher)
+  volatile long long* published = reinterpret_cast<volatile long long*>(bars + 6 * S);  // fused
+  int* vok = reinterpret_cast<int*>(bars + 6 * S + 2);  // fused: per-candidate dependency check results
+  constexpr int NTK = FUSED ? C::NTF : C::NT;
   auto sU = [&](int s) { return reinterpret_cast<double*>(smem + size_t(s) * C::SLOT + C::OFF_U); };
   auto sR = [&](int s) { return reinterpret_cast<double*>(smem + size_t(s) * C::SLOT + C::OFF_R); };
   auto sG = [&](int s) { return reinterpret_cast<double*>(smem + size_t(s) * C::SLOT + C::OFF_G); };
@@ -192,11 +237,18 @@ __global__ void __launch_bounds__(WsCfg<N>::NT, 1)
   auto sF = [&](int s) { return reinterpret_cast<double*>(smem + size_t(s) * C::SLOT + C::OFF_F); };
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool res_in = UPDATE && !p.first_stage;
-  // tiles of this CTA: t_begin + blockIdx.x + j * gridDim.x, j < J
+  // tiles of this CTA: t_begin + blockIdx.x + j * gridDim.x, j < J; fused: JJ = nst * J positions
   const int64_t J = t_count > blockIdx.x ? (t_count - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int64_t JJ = FUSED ? int64_t(fp.nst) * J : J;
   const int64_t kend = p.k_begin + p.K;
-  auto tile_of = [&](int64_t j) { return t_begin + blockIdx.x + j * gridDim.x; };
+  auto stage_of = [&](int64_t jj) { return FUSED ? int(jj / J) : 0; };
+  auto tile_of = [&](int64_t jj) { return t_begin + blockIdx.x + (FUSED ? jj % J : jj) * gridDim.x; };
+  auto stage_end = [&](int64_t jj) { return FUSED ? (jj / J + 1) * J : JJ; };
+  auto u_in_of = [&](int g) -> const double* { return FUSED ? fp.u[(fp.par0 + g) & 1] : p.u_in; };
+  auto u_out_of = [&](int g) -> double* { return FUSED ? fp.u[(fp.par0 + g + 1) & 1] : p.u_out; };
+  auto res_in_of = [&](int g) { return UPDATE && (FUSED ? (fp.stage0 + g) % 5 != 0 : !p.first_stage); };
+  auto rk_a_of = [&](int g) { return FUSED ? fp.rk_a[(fp.stage0 + g) % 5] : p.rk_a; };
+  auto rk_b_of = [&](int g) { return FUSED ? fp.rk_b[(fp.stage0 + g) % 5] : p.rk_b; };
   auto count_of = [&](int64_t tile) {
     const int64_t k0 = tile * E;
     return int(kend - k0 < E ? kend - k0 : E);
@@ -208,17 +260,20 @@ __global__ void __launch_bounds__(WsCfg<N>::NT, 1)
       mbar_init(bar_tr + s, C::PT);
       mbar_init(bar_full + s, C::PT);
       mbar_init(bar_empty + s, C::MW);
+      mbar_init(bar_done + s, C::MW);
+      mbar_init(bar_done + S + s, C::MW);
     }
+    *published = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int m = tid; m < NF; m += C::NT) sFm[m] = p.fmask[m];
+  for (int m = tid; m < NF; m += NTK) sFm[m] = p.fmask[m];
   if constexpr (C::OPS_SMEM) {
-    for (int w = tid; w < 3 * M8 * KV; w += C::NT) {
+    for (int w = tid; w < 3 * M8 * KV; w += NTK) {
       const int r = w / KV, k = w - r * KV;
       cp_async8(sA + r * C::LDA + k, opsA + w);
     }
     const double* Lg = opsA + 3 * M8 * KV;
-    for (int w = tid; w < M8 * KL; w += C::NT) {
+    for (int w = tid; w < M8 * KL; w += NTK) {
       const int r = w / KL, k = w - r * KL;
       cp_async8(sA + 3 * M8 * C::LDA + r * C::LDL + k, Lg + w);
     }
@@ -231,10 +286,45 @@ __global__ void __launch_bounds__(WsCfg<N>::NT, 1)
   if (warp == C::MW) {
     // ====================== TMA loader warp (one lane) ======================
     // Runs ahead of everybody, bounded only by free ring slots: tile j's bulk
-    // loads are issued as soon as the MMA warps release tile j - S.
-    if (lane == 0) {
+    // loads are issued as soon as the MMA warps release tile j - S (fused launches: as
+    // soon as the publisher has published it).
+    // Fused: the whole warp verifies tile dependencies in batches (verify_from), lane 0
+    // issues the copies.
+    int64_t verified = 0;  // fused: positions < verified have their dependencies satisfied
+    auto verify_from = [&](int64_t j0, bool block) {
+      // candidates j0 .. j1-1 (same stage): poll all their neighbour counters with relaxed
+      // loads, spread over the lanes; take the longest satisfied prefix (at least j0,
+      // waiting for it if needed); one acquire fence + one proxy fence for the batch.
+      const int64_t j1 = j0 + C::VB < stage_end(j0) ? j0 + C::VB : stage_end(j0);
+      const unsigned target = fp.g0 + unsigned(stage_of(j0));
+      const long long t0 = clock64();
+      int64_t hi = j0;
+      for (;;) {
+        if (lane < C::VB) vok[lane] = 1;
+        __syncwarp();
+        for (int64_t x = j0; x < j1; ++x) {
+          const int64_t t = tile_of(x);
+          const int q0 = fp.nbr_off[t], q1 = fp.nbr_off[t + 1];
+          for (int q = q0 + lane; q < q1; q += 32)
+            if (ld_relaxed_gpu(fp.flags + fp.nbr[q]) < target) vok[x - j0] = 0;
+        }
+        __syncwarp();
+        hi = j0;
+        while (hi < j1 && vok[hi - j0]) ++hi;
+        __syncwarp();
+        if (hi > j0 || !block) break;
+        __nanosleep(64);
+        if (clock64() - t0 > (1ll << 35)) __trap();  // broken dependency graph: no silent hang
+      }
+      if (hi == j0) return;
+      fence_acq_rel_gpu();
+      fence_proxy_async_global();
+      __syncwarp();
+      verified = hi;
+    };
+    if (FUSED || lane == 0) {
       DG_T0();
-      for (int64_t j = 0; j < J; ++j) {
+      for (int64_t j = 0; j < JJ; ++j) {
         const int s = int(j % S);
         const unsigned u = unsigned(j / S);
         {
@@ -243,13 +333,47 @@ __global__ void __launch_bounds__(WsCfg<N>::NT, 1)
           DG_ACC(0);
         }
         const int64_t tile = tile_of(j);
-        unsigned bytes = TS * 8 + C::GEOT * 8 + C::IDXT * 4;
-        if (C::RES_SMEM && res_in) bytes += TS * 8;
-        mbar_arrive_tx(bar_load + s, bytes);
-        bulk_g2s(sU(s), p.u_in + tile * TS, TS * 8, bar_load + s);
-        if (C::RES_SMEM && res_in) bulk_g2s(sR(s), p.res + tile * TS, TS * 8, bar_load + s);
-        bulk_g2s(sG(s), p.geo + tile * C::GEOT, C::GEOT * 8, bar_load + s);
-        bulk_g2s(sI(s), p.gidx + tile * C::IDXT, C::IDXT * 4, bar_load + s);
+        const int g = stage_of(j);
+        const bool res_in = res_in_of(g);
+        if constexpr (FUSED) {
+          if (j >= verified) verify_from(j, true);
+          // done[] phase safety: tile j reuses done[j % 2S] only after tile j - 2S is published
+          while (*published <= j - 2 * S) __nanosleep(32);
+        }
+        if (lane == 0) {
+          unsigned bytes = TS * 8 + C::GEOT * 8 + C::IDXT * 4;
+          if (C::RES_SMEM && res_in) bytes += TS * 8;
+          mbar_arrive_tx(bar_load + s, bytes);
+          bulk_g2s(sU(s), u_in_of(g) + tile * TS, TS * 8, bar_load + s);
+          if (C::RES_SMEM && res_in) bulk_g2s(sR(s), p.res + tile * TS, TS * 8, bar_load + s);
+          bulk_g2s(sG(s), p.geo + tile * C::GEOT, C::GEOT * 8, bar_load + s);
+          bulk_g2s(sI(s), p.gidx + tile * C::IDXT, C::IDXT * 4, bar_load + s);
+        }
+        if constexpr (FUSED) {  // verify ahead while the ring is full (hides the poll + fence latency)
+          __syncwarp();
+          if (verified - j < C::VB / 2 && verified < JJ) verify_from(verified, false);
+        }
+      }
+    }
+  } else if (FUSED && warp == C::MW + 1 + C::PW) {
+    // ===================== publisher warp (fused launches, one lane) =====================
+    // Publishes tile completions in order: waits until the MMA warps are done with tile jj
+    // (done[jj % 2S]), batches every later tile already done (non-blocking test), then one
+    // release fence — cumulative over the MMA warps' stores, which the done barrier ordered
+    // before it at CTA scope — and the counters.  The loader does not load tile x before
+    // tile x - 2S is published, so done[] never runs two phases ahead of this warp.
+    if (lane == 0) {
+      int64_t jj = 0;
+      while (jj < JJ) {
+        mbar_wait(bar_done + int(jj % (2 * S)), unsigned(jj / (2 * S)) & 1);
+        int64_t hi = jj + 1;
+        while (hi < JJ && hi < jj + 2 * S && mbar_test(bar_done + int(hi % (2 * S)), unsigned(hi / (2 * S)) & 1))
+          ++hi;
+        // release stores: cumulative over the MMA warps' stores (ordered before this point
+        // at CTA scope by the done barrier)
+        for (int64_t x = jj; x < hi; ++x) st_release_gpu(fp.flags + tile_of(x), fp.g0 + unsigned(stage_of(x)) + 1u);
+        *published = hi;
+        jj = hi;
       }
     }
   } else if (warp > C::MW) {
@@ -265,12 +389,13 @@ __global__ void __launch_bounds__(WsCfg<N>::NT, 1)
       DG_T0();
       const int32_t* I = sI(s);
       double* F = sF(s);
+      const double* uin = u_in_of(stage_of(j));
       for (int w = ptid; w < E * NF; w += C::PT) {
         const int32_t gi = I[w];
         if (gi >= 0 && !(gi & TileLayout::INTRA_FLAG)) {  // intra-tile faces need no gather
           const int e = w / NF, m = w - e * NF;
           const bool ghost = gi >= p.ghost_base;
-          const double* src = p.u_in + gi;
+          const double* src = uin + gi;
           const int cb = 24 * (e >> 2) + 2 * (e & 3);
 #pragma unroll
           for (int c = 0; c < 6; ++c) {
@@ -341,23 +466,29 @@ __global__ void __launch_bounds__(WsCfg<N>::NT, 1)
     };
     // flux warps: tile j's flux, then tile j+LA's trace gather (its bulk load was issued
     // by the loader warp as soon as a slot was free)
+    //
+    // The look-ahead never crosses a stage boundary of a fused launch: the flux warps block
+    // on a stage-g load only after they finished all of stage g-1, so every cross-CTA
+    // dependency wait (loader, verify_from) points at strictly earlier work and the
+    // schedule cannot deadlock.
     DG_T0();
-    DG_CNT(7, J);
-    for (int64_t t = 0; t < C::LA && t < J; ++t) traces(t);
-    for (int64_t j = 0; j < J; ++j) {
-      if (C::LA == 0) {
-        traces(j);
-        flux(j);
-      } else {
-        flux(j);
-        if (j + C::LA < J) traces(j + C::LA);
-      }
+    DG_CNT(7, JJ);
+    int64_t issued = 0;  // traces issued for positions < issued
+    auto issue_upto = [&](int64_t lim) {
+      while (issued < lim) traces(issued++);
+    };
+    for (int64_t j = 0; j < JJ; ++j) {
+      const int64_t end = stage_end(j);
+      const bool first = j == 0 || (FUSED && j % J == 0);
+      issue_upto(first ? (j + C::LA < end ? (C::LA > 0 ? j + C::LA : j + 1) : end) : j + 1);
+      flux(j);
+      issue_upto(j + 1 + C::LA < end ? j + 1 + C::LA : end);
     }
     DG_ACC(9);
   } else {
     // ============================= MMA warps =============================
     const int gid = lane >> 2, tig = lane & 3;
-    const int64_t total = J * C::T;
+    const int64_t total = JJ * C::T;
     int64_t released = 0, waited = -1;
     auto release = [&](int64_t jj) {  // this warp is done with tile jj (waits for it to exist first)
       if (waited < jj) {
@@ -365,7 +496,10 @@ __global__ void __launch_bounds__(WsCfg<N>::NT, 1)
         waited = jj;
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(bar_empty + int(jj % S));
+      if (lane == 0) {
+        mbar_arrive(bar_empty + int(jj % S));
+        if constexpr (FUSED) mbar_arrive(bar_done + int(jj % (2 * S)));
+      }
     };
     DG_T0();
     for (int64_t q = warp; q < total; q += C::MW) {
@@ -389,6 +523,10 @@ __global__ void __launch_bounds__(WsCfg<N>::NT, 1)
 #endif
       const int64_t tile = tile_of(j);
       const int ne = count_of(tile);
+      const int gs = stage_of(j);
+      const bool res_in = res_in_of(gs);
+      const double rk_a = rk_a_of(gs), rk_b = rk_b_of(gs);
+      double* const u_out = u_out_of(gs);
       const int t = task % C::MT, g = task / C::MT;
       const int row = 8 * t + gid;
       const double* U = sU(s);
@@ -489,9 +627,9 @@ __global__ void __launch_bounds__(WsCfg<N>::NT, 1)
           if (UPDATE) {
             double rold = 0.0;
             if (res_in) rold = C::RES_SMEM ? sR(s)[col * LD + row] : p.res[idx];
-            const double rr = p.rk_a * rold + p.dt * rhs;
+            const double rr = rk_a * rold + p.dt * rhs;
             p.res[idx] = rr;
-            p.u_out[idx] = U[col * LD + row] + p.rk_b * rr;
+            u_out[idx] = U[col * LD + row] + rk_b * rr;
           } else {
             p.rhs_out[idx] = rhs;
           }
@@ -501,7 +639,7 @@ __global__ void __launch_bounds__(WsCfg<N>::NT, 1)
       if (lane == 0) atomicAdd(&g_ws_prof[6], (unsigned long long)(clock64() - _tc));
 #endif
     }
-    while (released < J) release(released++);
+    while (released < JJ) release(released++);
     DG_ACC(10);
   }
 }
@@ -511,8 +649,9 @@ void launch_stage_ws(const StageParams<double>& p, const double* opsA, int mode,
   using C = WsCfg<N>;
   static int sms = 0;
   if (!sms) {
-    cudaFuncSetAttribute(dg_stage_ws<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
-    cudaFuncSetAttribute(dg_stage_ws<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+    cudaFuncSetAttribute(dg_stage_ws<N, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+    cudaFuncSetAttribute(dg_stage_ws<N, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+    cudaFuncSetAttribute(dg_stage_ws<N, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -522,10 +661,41 @@ void launch_stage_ws(const StageParams<double>& p, const double* opsA, int mode,
   const int64_t t0 = p.k_begin / C::E;
   const int64_t tc = (p.k_begin + p.K + C::E - 1) / C::E - t0;
   const unsigned grid = unsigned(tc < sms ? tc : sms);
+  const FusedParams<double> nf{};
   if (mode == 1)
-    launch_pdl(true, dg_stage_ws<N, true>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc);
+    launch_pdl(true, dg_stage_ws<N, true, false>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc, nf);
   else
-    launch_pdl(true, dg_stage_ws<N, false>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc);
+    launch_pdl(true, dg_stage_ws<N, false, false>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc, nf);
+}
+
+// Stage-fused launch over all tiles (single rank): grid = min(#tiles, #SMs), one CTA per
+// SM, launched cooperatively so that every CTA is co-resident (the tile-dependency waits
+// need all of them running); returns false if the launch was refused.
+template <int N>
+bool launch_stage_ws_fused(const StageParams<double>& p, const double* opsA, const FusedParams<double>& fp,
+                           cudaStream_t st) {
+  using C = WsCfg<N>;
+  static int sms = 0;
+  if (!sms) {
+    cudaFuncSetAttribute(dg_stage_ws<N, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if (p.K <= 0 || fp.nst <= 0) return true;
+  const int64_t tc = (p.K + C::E - 1) / C::E;
+  const unsigned grid = unsigned(tc < sms ? tc : sms);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(C::NTF);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, dg_stage_ws<N, true, true>, p, opsA, int64_t(0), tc, fp) == cudaSuccess;
 }
 
 #ifdef DG_WS_PROFILE

@@ -58,6 +58,13 @@ def test_argument_errors():
         assert e.value.status == dg.DG_ERR_ARG
     s = Solver(3, device=-1, system=dg.DG_SYSTEM_ACOUSTICS)
     assert s.nfields == 4
+    for kw in (dict(precision=4), dict(rank=0, nranks=2)):  # fused: single-rank FP64 only
+        with pytest.raises(DGError) as e:
+            Solver(3, device=-1, variant=dg.DG_VARIANT_FUSED, **kw)
+        assert e.value.status == dg.DG_ERR_ARG
+    with pytest.raises(DGError) as e:
+        Solver(3, device=-1, variant=6)
+    assert e.value.status == dg.DG_ERR_ARG
 
 
 def test_host_only_solver_refuses_compute():
