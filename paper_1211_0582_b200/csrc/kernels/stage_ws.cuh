@@ -65,10 +65,12 @@ struct WsCfg {
 #else
   static constexpr int S_TUNE = 0;
 #endif
-  // measured (NEXT-4 sweep, profiles/r1_tile_sweep.jsonl): N=3 E=4/S=8 beats E=8/S=5 by 6 %
+  // measured (NEXT-4 sweeps, profiles/r1_tile_sweep*.jsonl): N=3 E=4/S=8 beats E=8/S=5 by 6 %;
+  // N=4 with the residual out of the ring (register prefetch) fits S=8 and a 4-tile trace
+  // look-ahead (+3.4 %); N=7/8 prefer shallower rings with 11 MMA warps
   static constexpr int E = (TUNED && E_TUNE) ? E_TUNE : N == 1 ? 32 : N == 2 ? 16 : 4;
   static constexpr int S = (TUNED && S_TUNE) ? S_TUNE
-                           : N == 2 ? 4 : N == 3 ? 8 : N == 4 ? 5 : N == 5 ? 3 : N == 6 ? 3 : N == 7 ? 4 : N == 8 ? 3 : 2;
+                           : N == 2 ? 4 : N == 3 ? 8 : N == 4 ? 8 : N == 5 ? 3 : N == 6 ? 3 : N == 7 ? 3 : 2;
 #ifdef DG_WS_LA
   static constexpr int LA_TUNE = DG_WS_LA;
 #else
@@ -76,22 +78,34 @@ struct WsCfg {
 #endif
   // trace gathers issued LA tiles ahead of the flux (LA <= S - 2: the slot of tile j+LA
   // must have been released by the MMA warps, which may still be on tile j-1)
-  static constexpr int LA = (TUNED && LA_TUNE) ? LA_TUNE : S - 2 < 2 ? S - 2 : 2;
+  static constexpr int LA = (TUNED && LA_TUNE) ? LA_TUNE : N == 4 ? 4 : S - 2 < 2 ? S - 2 : 2;
   static_assert(LA <= S - 2 || S <= 2, "look-ahead beyond the ring");
+#ifdef DG_WS_OPS
+  static constexpr bool OPS_SMEM = TUNED ? bool(DG_WS_OPS) : N <= 5;
+#else
   static constexpr bool OPS_SMEM = N <= 5;
-  static constexpr bool RES_SMEM = N <= 4;
-  // warp roles (measured, tools/tune_ws.sh): >= 2 MMA warps per SMSP so one's epilogue hides
-  // under the other's DMMAs; 3 per SMSP when the operators come through L1/L2 (N >= 5)
+#endif
+#ifdef DG_WS_RES
+  static constexpr bool RES_SMEM = TUNED ? bool(DG_WS_RES) : N <= 3;
+#else
+  static constexpr bool RES_SMEM = N <= 3;
+#endif
+  // warp roles (measured, tools/gpu_tile_sweep.sh): >= 2 MMA warps per SMSP so one's epilogue
+  // hides under the other's DMMAs; 11 for N >= 5, which keeps the CTA at 16 warps (a 17th
+  // warp would cap registers at 96 per thread and force the residual prefetch off)
 #ifdef DG_WS_MW
   static constexpr int MW = DG_WS_MW;
 #else
-  static constexpr int MW = N >= 5 ? 12 : 8;
+  static constexpr int MW = N >= 5 ? 11 : 8;
 #endif
 #ifdef DG_WS_PW
   static constexpr int PW = DG_WS_PW;  // flux warps (trace gather + flux); plus one dedicated TMA loader warp
 #else
   static constexpr int PW = N == 3 ? 6 : 4;
 #endif
+  // residual from global memory: prefetched into registers at task start, unless a
+  // 17-warp CTA (register cap 96 per thread: the file is split per SMSP) would spill
+  static constexpr bool RES_PREFETCH = !RES_SMEM && (N <= 5 || MW + 1 + PW <= 16);
   static constexpr int NT = 32 * (MW + 1 + PW);
   static constexpr int PT = 32 * PW;
   static constexpr int G = E / 4;
@@ -536,6 +550,18 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
       for (int b = 0; b < 3; ++b)
 #pragma unroll
         for (int nt = 0; nt < 3; ++nt) acc[b][nt][0] = acc[b][nt][1] = 0.0;
+      // residual through global memory (!RES_SMEM): prefetched into registers now, used
+      // in the update after the contractions (hides the load latency behind the DMMAs)
+      double rpre[6];
+      if constexpr (UPDATE && C::RES_PREFETCH) {
+        const int e = 4 * g + tig;
+        const int64_t tb = tile * TS + 8 * t + gid;
+#pragma unroll
+        for (int c = 0; c < 6; ++c)
+          rpre[c] = (res_in && 8 * t + gid < Np && e < ne)
+                        ? p.res[tb + int64_t(24 * g + 8 * (c >> 1) + 2 * tig + (c & 1)) * LD]
+                        : 0.0;
+      }
       const double* bp = U + (24 * g + gid) * LD + tig;
       if constexpr (C::OPS_SMEM) {
         const double* ap = sA + row * C::LDA + tig;
@@ -626,7 +652,13 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
           const double rhs = r[c >> 1][c & 1] + r2[c >> 1][c & 1];
           if (UPDATE) {
             double rold = 0.0;
-            if (res_in) rold = C::RES_SMEM ? sR(s)[col * LD + row] : p.res[idx];
+            if constexpr (C::RES_SMEM) {
+              if (res_in) rold = sR(s)[col * LD + row];
+            } else if constexpr (C::RES_PREFETCH) {
+              rold = rpre[c];
+            } else {
+              if (res_in) rold = p.res[idx];
+            }
             const double rr = rk_a * rold + p.dt * rhs;
             p.res[idx] = rr;
             u_out[idx] = U[col * LD + row] + rk_b * rr;
