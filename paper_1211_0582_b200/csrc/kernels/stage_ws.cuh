@@ -282,14 +282,16 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
   }
   for (int m = tid; m < NF; m += NTK) sFm[m] = p.fmask[m];
   if constexpr (C::OPS_SMEM) {
-    for (int w = tid; w < 3 * M8 * KV; w += NTK) {
-      const int r = w / KV, k = w - r * KV;
-      cp_async8(sA + r * C::LDA + k, opsA + w);
+    // 16-byte cp.async chunks (rows of KV, KL, LDA, LDL doubles are 16-B aligned)
+    static_assert(KV % 2 == 0 && KL % 2 == 0 && C::LDA % 2 == 0 && C::LDL % 2 == 0, "16-B operator rows");
+    for (int w = tid; w < 3 * M8 * KV / 2; w += NTK) {
+      const int r = (2 * w) / KV, k = 2 * w - r * KV;
+      cp_async16(sA + r * C::LDA + k, opsA + 2 * w);
     }
     const double* Lg = opsA + 3 * M8 * KV;
-    for (int w = tid; w < M8 * KL; w += NTK) {
-      const int r = w / KL, k = w - r * KL;
-      cp_async8(sA + 3 * M8 * C::LDA + r * C::LDL + k, Lg + w);
+    for (int w = tid; w < M8 * KL / 2; w += NTK) {
+      const int r = (2 * w) / KL, k = 2 * w - r * KL;
+      cp_async16(sA + 3 * M8 * C::LDA + r * C::LDL + k, Lg + 2 * w);
     }
     cp_commit();
     cp_wait<0>();

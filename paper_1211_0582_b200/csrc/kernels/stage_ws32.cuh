@@ -38,13 +38,43 @@ struct Ws32Cfg {
   static constexpr int LDF = ldx8(KL);
   static constexpr int LDA = ldx8(KV);
   static constexpr int LDL = ldx8(KL);
-  static constexpr int E = N == 1 ? 32 : N == 2 ? 16 : N == 3 ? 8 : 4;
-  static constexpr int S = N <= 6 ? 5 : N <= 8 ? 4 : 3;
-  static constexpr int LA = S - 2 < 2 ? S - 2 : 2;
+  // tuning builds: -DDG_W32_TUNE_N=n with -DDG_W32_{E,S,LA,RES,MW,PW}=v override order n only
+#ifdef DG_W32_TUNE_N
+  static constexpr bool TUNED = N == DG_W32_TUNE_N;
+#else
+  static constexpr bool TUNED = false;
+#endif
+#ifndef DG_W32_E
+#define DG_W32_E 0
+#endif
+#ifndef DG_W32_S
+#define DG_W32_S 0
+#endif
+#ifndef DG_W32_LA
+#define DG_W32_LA -1
+#endif
+#ifndef DG_W32_RES
+#define DG_W32_RES -1
+#endif
+#ifndef DG_W32_MW
+#define DG_W32_MW 0
+#endif
+#ifndef DG_W32_PW
+#define DG_W32_PW 0
+#endif
+  static constexpr int E = (TUNED && DG_W32_E) ? DG_W32_E : N == 1 ? 32 : N == 2 ? 16 : N == 3 ? 8 : 4;
+  static constexpr int S = (TUNED && DG_W32_S) ? DG_W32_S : N <= 6 ? 5 : N <= 8 ? 4 : 3;
+  static constexpr int LA = (TUNED && DG_W32_LA >= 0) ? DG_W32_LA : S - 2 < 2 ? S - 2 : 2;
   static constexpr bool OPS_SMEM = N <= 4;
-  static constexpr bool RES_SMEM = N <= 6;
-  static constexpr int MW = 8;  // 12 spills at the 544-thread register budget
-  static constexpr int PW = 4;
+  // measured (tools/gpu_tile_sweep.sh, profiles/r1_tile_sweep_f32.jsonl): 11 MMA warps with
+  // the residual prefetched into registers win at N = 5, 7, 8 (+6..7 %); N = 3, 4, 6 keep
+  // the residual in the ring and 8 MMA warps
+  static constexpr bool RES_SMEM = (TUNED && DG_W32_RES >= 0) ? bool(DG_W32_RES) : N <= 4 || N == 6;
+  static constexpr int MW = (TUNED && DG_W32_MW) ? DG_W32_MW : (N == 5 || N == 7 || N == 8) ? 11 : 8;
+  static constexpr int PW = (TUNED && DG_W32_PW) ? DG_W32_PW : 4;
+  // residual from global memory: prefetched into registers at task start while the CTA
+  // has at most 16 warps (128 registers per thread; the file is split per SMSP)
+  static constexpr bool RES_PREFETCH = !RES_SMEM && MW + 1 + PW <= 16;
   static constexpr int NT = 32 * (MW + 1 + PW);
   static constexpr int PT = 32 * PW;
   static constexpr int G = E / 4;
@@ -136,18 +166,22 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
   }
   for (int m = tid; m < NF; m += C::NT) sFm[m] = p.fmask[m];
   if constexpr (C::OPS_SMEM) {
+    // hi/lo operators into shared memory: 16-byte cp.async chunks (rows are 16-B aligned)
+    static_assert(KV % 4 == 0 && KL % 4 == 0 && C::LDA % 4 == 0 && C::LDL % 4 == 0, "16-B operator rows");
     for (int h = 0; h < 2; ++h) {
       const float* src = opsA + size_t(h) * C::OPS_ONE;
       float* dst = sA + h * C::A_ONE;
-      for (int w = tid; w < 3 * M16 * KV; w += C::NT) {
-        const int r = w / KV, k = w - r * KV;
-        dst[r * C::LDA + k] = src[w];
+      for (int w = tid; w < 3 * M16 * KV / 4; w += C::NT) {
+        const int r = (4 * w) / KV, k = 4 * w - r * KV;
+        cp_async16(dst + r * C::LDA + k, src + 4 * w);
       }
-      for (int w = tid; w < M16 * KL; w += C::NT) {
-        const int r = w / KL, k = w - r * KL;
-        dst[3 * M16 * C::LDA + r * C::LDL + k] = src[3 * M16 * KV + w];
+      for (int w = tid; w < M16 * KL / 4; w += C::NT) {
+        const int r = (4 * w) / KL, k = 4 * w - r * KL;
+        cp_async16(dst + 3 * M16 * C::LDA + r * C::LDL + k, src + 3 * M16 * KV + 4 * w);
       }
     }
+    cp_commit();
+    cp_wait<0>();
   }
   __syncthreads();
   pdl_wait();  // the previous stage's fields are complete from here on
@@ -304,6 +338,18 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
       for (int b = 0; b < 3; ++b)
 #pragma unroll
         for (int nt = 0; nt < 3; ++nt) acc[b][nt][0] = acc[b][nt][1] = acc[b][nt][2] = acc[b][nt][3] = 0.0f;
+      float rpre[2][6];  // residual prefetch (RES_PREFETCH): rows r0, r0 + 8
+      if constexpr (UPDATE && C::RES_PREFETCH) {
+        const int e = 4 * g + tig;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int c = 0; c < 6; ++c)
+            rpre[h][c] = (res_in && r0 + 8 * h < Np && e < ne)
+                             ? p.res[tile * TS + r0 + 8 * h +
+                                     int64_t(24 * g + 8 * (c >> 1) + 2 * tig + (c & 1)) * LD]
+                             : 0.0f;
+      }
       const float* bp = U + (24 * g + gid) * LD + tig;
 #pragma unroll 2
       for (int kk = 0; kk < KV; kk += 8) {
@@ -388,7 +434,13 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
               const float rhs = r[c >> 1][2 * h + (c & 1)];
               if (UPDATE) {
                 float rold = 0.0f;
-                if (res_in) rold = C::RES_SMEM ? sR(s)[col * LD + row] : p.res[idx];
+                if constexpr (C::RES_SMEM) {
+                  if (res_in) rold = sR(s)[col * LD + row];
+                } else if constexpr (C::RES_PREFETCH) {
+                  rold = rpre[h][c];
+                } else {
+                  if (res_in) rold = p.res[idx];
+                }
                 const float rr = p.rk_a * rold + p.dt * rhs;
                 p.res[idx] = rr;
                 p.u_out[idx] = U[col * LD + row] + p.rk_b * rr;
