@@ -169,7 +169,23 @@ DG_API dg_status dg_group_lserk_step(dg_solver* const* group, int32_t n, double 
 DG_API dg_status dg_fields_download(dg_solver* s, double* f);
 DG_API dg_status dg_fields_download_device(dg_solver* s, void* f_dev);
 
-/* Wait for all work enqueued by this solver; surfaces asynchronous CUDA errors. */
+/* Pipelined host I/O (FP64 host layout as dg_fields_upload / dg_fields_download).
+ * Both calls only ENQUEUE work and return: the host->device copy runs on a solver-owned
+ * copy-in stream into one of two staging buffers, the device->host copy on a copy-out
+ * stream from one of two staging buffers, and the layout conversions on the compute
+ * stream, ordered with dg_lserk_step / dg_rhs by events.  Consecutive
+ * upload_async / lserk_step / download_async cycles therefore overlap the copies of one
+ * cycle with the computation of its neighbours (PCIe is full duplex).  The host arrays
+ * are borrowed until dg_synchronize returns (use page-locked memory for asynchronous
+ * copies; pageable memory works but the driver then stages synchronously).  The fields
+ * are ready for stepping when upload_async returns (ordering is on the device); a
+ * download's data is valid after dg_synchronize.  upload_async resets the residual like
+ * dg_fields_upload.  Errors: DG_ERR_ARG, DG_ERR_STATE (no mesh / no fields), DG_ERR_CUDA. */
+DG_API dg_status dg_fields_upload_async(dg_solver* s, const double* f);
+DG_API dg_status dg_fields_download_async(dg_solver* s, double* f);
+
+/* Wait for all work enqueued by this solver (compute and copy streams); surfaces
+ * asynchronous CUDA errors. */
 DG_API dg_status dg_synchronize(dg_solver* s);
 
 /* Parity exports of the host setup (work on host-only solvers too).

@@ -115,6 +115,13 @@ struct dg_solver {
   int32_t* d_nbr = nullptr;
   unsigned stage_count = 0;    // stages completed since the last field upload
   cudaStream_t stream = nullptr, comm = nullptr;
+  // pipelined host I/O (dg_fields_upload_async / dg_fields_download_async): copy streams,
+  // double-buffered FP64 staging, and the events that order them with the compute stream
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  double* d_in[2] = {nullptr, nullptr};
+  double* d_out[2] = {nullptr, nullptr};
+  cudaEvent_t ev_in_ready[2] = {}, ev_in_free[2] = {}, ev_out_ready[2] = {}, ev_out_free[2] = {};
+  int in_idx = 0, out_idx = 0;
   bool own_stream = false;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
   cudaEvent_t ev_packed = nullptr, ev_copied = nullptr;  // loopback transport
@@ -160,6 +167,10 @@ void release_device(dg_solver* s) {
   free_dev(s->d_send);
   p = s->d_sidx; free_dev(p); s->d_sidx = nullptr;
   p = s->d_flags; free_dev(p); s->d_flags = nullptr;
+  for (int i = 0; i < 2; ++i) {
+    p = s->d_in[i]; free_dev(p); s->d_in[i] = nullptr;
+    p = s->d_out[i]; free_dev(p); s->d_out[i] = nullptr;
+  }
   p = s->d_nbr_off; free_dev(p); s->d_nbr_off = nullptr;
   p = s->d_nbr; free_dev(p); s->d_nbr = nullptr;
   s->fused = false;
@@ -710,6 +721,8 @@ dg_status dg_mesh_upload(dg_solver* s, int64_t nv, const double* VX, int64_t K, 
   dg_status st = need_device(s);
   if (st != DG_OK) return st;
   CK(cudaStreamSynchronize(s->stream));
+  if (s->h2d) CK(cudaStreamSynchronize(s->h2d));  // staging buffers may still be in use
+  if (s->d2h) CK(cudaStreamSynchronize(s->d2h));
   release_device(s);
   s->cur = 0;
   return s->fp64 ? upload_setup<double>(s) : upload_setup<float>(s);
@@ -801,6 +814,83 @@ static dg_status download_common(dg_solver* s, void* dst, bool to_host, bool rhs
   return DG_OK;
 }
 
+// lazily create the copy streams / events and the staging buffers of the pipelined I/O
+static dg_status io_setup(dg_solver* s) {
+  if (!s->h2d) {
+    CK(cudaStreamCreateWithFlags(&s->h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&s->d2h, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventCreateWithFlags(&s->ev_in_ready[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&s->ev_in_free[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&s->ev_out_ready[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&s->ev_out_free[i], cudaEventDisableTiming));
+    }
+  }
+  const size_t bytes = size_t(std::max<int64_t>(s->nc * s->Kl * s->Np, 1)) * sizeof(double);
+  for (int i = 0; i < 2; ++i) {
+    if (!s->d_in[i]) CK(cudaMalloc((void**)&s->d_in[i], bytes));
+    if (!s->d_out[i]) CK(cudaMalloc((void**)&s->d_out[i], bytes));
+  }
+  return DG_OK;
+}
+
+dg_status dg_fields_upload_async(dg_solver* s, const double* f) {
+  g_err.clear();
+  dg_status st = need_device(s);
+  if (st != DG_OK) return st;
+  if (!s->has_mesh) return fail(DG_ERR_STATE, "no mesh uploaded");
+  if (!f) return fail(DG_ERR_ARG, "null field pointer");
+  st = io_setup(s);
+  if (st != DG_OK) return st;
+  const int i = s->in_idx;
+  s->in_idx ^= 1;
+  const size_t bytes = size_t(s->nc * s->Kl * s->Np) * sizeof(double);
+  CK(cudaStreamWaitEvent(s->h2d, s->ev_in_free[i], 0));  // the conversion that last read d_in[i]
+  CK(cudaMemcpyAsync(s->d_in[i], f, bytes, cudaMemcpyHostToDevice, s->h2d));
+  CK(cudaEventRecord(s->ev_in_ready[i], s->h2d));
+  CK(cudaStreamWaitEvent(s->stream, s->ev_in_ready[i], 0));
+  s->cur = 0;
+  if (s->fp64)
+    dg::cm_to_tiles<double, double>(s->d_in[i], static_cast<double*>(s->d_u[0]), s->Kl, s->Np, s->lay, s->stream);
+  else
+    dg::cm_to_tiles<double, float>(s->d_in[i], static_cast<float*>(s->d_u[0]), s->Kl, s->Np, s->lay, s->stream);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(s->ev_in_free[i], s->stream));
+  CK(cudaMemsetAsync(s->d_res, 0, std::max<int64_t>(s->ntiles * s->lay.TS, 1) * s->wsize, s->stream));
+  if (s->fused) {
+    CK(cudaMemsetAsync(s->d_flags, 0, std::max<int64_t>(s->ntiles, 1) * sizeof(unsigned), s->stream));
+    s->stage_count = 0;
+  }
+  s->has_fields = true;
+  return DG_OK;
+}
+
+dg_status dg_fields_download_async(dg_solver* s, double* f) {
+  g_err.clear();
+  dg_status st = need_device(s);
+  if (st != DG_OK) return st;
+  if (!s->has_fields) return fail(DG_ERR_STATE, "no fields uploaded");
+  if (!f) return fail(DG_ERR_ARG, "null output pointer");
+  st = io_setup(s);
+  if (st != DG_OK) return st;
+  const int o = s->out_idx;
+  s->out_idx ^= 1;
+  const size_t bytes = size_t(s->nc * s->Kl * s->Np) * sizeof(double);
+  CK(cudaStreamWaitEvent(s->stream, s->ev_out_free[o], 0));  // the copy that last read d_out[o]
+  if (s->fp64)
+    dg::tiles_to_cm<double, double>(static_cast<const double*>(s->d_u[s->cur]), s->d_out[o], s->Kl, s->Np, s->lay,
+                                    s->stream);
+  else
+    dg::tiles_to_cm<float, double>(static_cast<const float*>(s->d_u[s->cur]), s->d_out[o], s->Kl, s->Np, s->lay,
+                                   s->stream);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(s->ev_out_ready[o], s->stream));
+  CK(cudaStreamWaitEvent(s->d2h, s->ev_out_ready[o], 0));
+  CK(cudaMemcpyAsync(f, s->d_out[o], bytes, cudaMemcpyDeviceToHost, s->d2h));
+  CK(cudaEventRecord(s->ev_out_free[o], s->d2h));
+  return DG_OK;
+}
+
 dg_status dg_fields_download(dg_solver* s, double* f) { g_err.clear(); return download_common(s, f, true, false); }
 dg_status dg_fields_download_device(dg_solver* s, void* f) { g_err.clear(); return download_common(s, f, false, false); }
 dg_status dg_rhs(dg_solver* s, double* r) { g_err.clear(); return download_common(s, r, true, true); }
@@ -851,6 +941,8 @@ dg_status dg_synchronize(dg_solver* s) {
   if (st != DG_OK) return st;
   CK(cudaStreamSynchronize(s->stream));
   CK(cudaStreamSynchronize(s->comm));
+  if (s->h2d) CK(cudaStreamSynchronize(s->h2d));
+  if (s->d2h) CK(cudaStreamSynchronize(s->d2h));
   CK(cudaGetLastError());
   return DG_OK;
 }
@@ -933,7 +1025,17 @@ void dg_destroy(dg_solver* s) {
     cudaSetDevice(s->cfg.device);
     if (s->stream) cudaStreamSynchronize(s->stream);
     if (s->comm) cudaStreamSynchronize(s->comm);
+    if (s->h2d) cudaStreamSynchronize(s->h2d);
+    if (s->d2h) cudaStreamSynchronize(s->d2h);
     release_device(s);
+    for (int i = 0; i < 2; ++i) {
+      if (s->ev_in_ready[i]) cudaEventDestroy(s->ev_in_ready[i]);
+      if (s->ev_in_free[i]) cudaEventDestroy(s->ev_in_free[i]);
+      if (s->ev_out_ready[i]) cudaEventDestroy(s->ev_out_ready[i]);
+      if (s->ev_out_free[i]) cudaEventDestroy(s->ev_out_free[i]);
+    }
+    if (s->h2d) cudaStreamDestroy(s->h2d);
+    if (s->d2h) cudaStreamDestroy(s->d2h);
     if (s->ncomm && nccl().ok) nccl().CommDestroy(s->ncomm);
     if (s->ev_fork) cudaEventDestroy(s->ev_fork);
     if (s->ev_join) cudaEventDestroy(s->ev_join);

@@ -56,6 +56,8 @@ _SIGS = {
     "dg_fields_download": (C.c_int, [_P, _D]),
     "dg_fields_download_device": (C.c_int, [_P, _P]),
     "dg_synchronize": (C.c_int, [_P]),
+    "dg_fields_upload_async": (C.c_int, [_P, _D]),
+    "dg_fields_download_async": (C.c_int, [_P, _D]),
     "dg_get_maps": (C.c_int, [_P, _I64, _I8, _I64, _I64]),
     "dg_get_nodes": (C.c_int, [_P, _D, _D, _D]),
     "dg_get_reference": (C.c_int, [_P, _D, _D, _D, _D, _D, _D, _D, _D, _I32]),
@@ -111,6 +113,7 @@ class Solver:
         cfg.rank, cfg.nranks, cfg.variant, cfg.reorder = rank, nranks, variant, int(bool(reorder))
         cfg.system = system
         self.nfields = 4 if system == DG_SYSTEM_ACOUSTICS else 6
+        self._io_refs = []  # host arrays borrowed by pending async copies
         self._id_buf = None
         if nccl_id is not None:
             self._id_buf = C.create_string_buffer(bytes(nccl_id), 128)
@@ -156,6 +159,22 @@ class Solver:
         assert f.shape == (self.nfields, self.K_local, self.Np), f.shape
         check(dg_fields_upload(self.h, _ptr(f, _D)), "dg_fields_upload")
 
+    def fields_upload_async(self, f):
+        """Enqueue an upload from a C-contiguous float64 host array (page-locked for real
+        overlap, e.g. torch.empty(..., pin_memory=True).numpy()); `f` must stay alive and
+        unchanged until synchronize()."""
+        assert f.dtype == np.float64 and f.flags.c_contiguous
+        assert f.shape == (self.nfields, self.K_local, self.Np), f.shape
+        self._io_refs.append(f)
+        check(dg_fields_upload_async(self.h, _ptr(f, _D)), "dg_fields_upload_async")
+
+    def fields_download_async(self, out):
+        """Enqueue a download into `out` (float64, C-contiguous); valid after synchronize()."""
+        assert out.dtype == np.float64 and out.flags.c_contiguous
+        assert out.shape == (self.nfields, self.K_local, self.Np), out.shape
+        self._io_refs.append(out)
+        check(dg_fields_download_async(self.h, _ptr(out, _D)), "dg_fields_download_async")
+
     def fields_upload_device(self, t):
         check(dg_fields_upload_device(self.h, C.c_void_p(t.data_ptr())), "dg_fields_upload_device")
 
@@ -180,6 +199,7 @@ class Solver:
 
     def synchronize(self):
         check(dg_synchronize(self.h), "dg_synchronize")
+        self._io_refs = []
 
     def get_maps(self):
         K, Nfp = self.K, self.Nfp

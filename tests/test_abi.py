@@ -77,6 +77,10 @@ def test_host_only_solver_refuses_compute():
     with pytest.raises(DGError) as e:
         s.lserk_step(1e-3, 1)
     assert e.value.status == dg.DG_ERR_STATE
+    for f in (s.fields_upload_async, s.fields_download_async):
+        with pytest.raises(DGError) as e:
+            f(np.zeros((6, s.K_local, s.Np)))
+        assert e.value.status == dg.DG_ERR_STATE
 
 
 def test_call_order_state_errors():

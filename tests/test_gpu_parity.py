@@ -496,3 +496,31 @@ def test_stage_fused_bitwise_equal_to_per_stage(N, n, sh):
     if n == 6 and N <= 4:
         st = setup("fz6", VX, E, N)
         assert relerr(Ua, oracle.lserk4(st, U0, dt, 6)) < 1e-12
+
+
+# ------------------------------------------------------------------ pipelined host I/O
+@pytest.mark.parametrize("prec", [8, 4])
+def test_pipelined_async_io_equals_synchronous(prec):
+    # upload_async / lserk_step / download_async cycles (copy streams, double-buffered
+    # staging) give exactly the fields of the synchronous calls, for every cycle
+    N = 4
+    VX, E = mesh(5, 61, 62, 63)
+    K = E.shape[0]
+    dt = di.dt_rule(VX, E, N)
+    ins = [torch.from_numpy(di.random_fields(K, N, seed=20 + k)).pin_memory().numpy() for k in range(4)]
+    outs = [torch.empty((6, K, di.np_of(N)), dtype=torch.float64).pin_memory().numpy() for _ in range(4)]
+    a = Solver(N, precision=prec)
+    a.mesh_upload(VX, E)
+    for k in range(4):
+        a.fields_upload_async(ins[k])
+        a.lserk_step(dt, 1 + k % 2)
+        a.fields_download_async(outs[k])
+    a.synchronize()
+    ref = Solver(N, precision=prec)
+    ref.mesh_upload(VX, E)
+    for k in range(4):
+        ref.fields_upload(ins[k])
+        ref.lserk_step(dt, 1 + k % 2)
+        assert np.array_equal(outs[k], ref.fields_download())
+    a.close()
+    ref.close()
