@@ -1,0 +1,48 @@
+#!/usr/bin/env python
+"""Render BASELINE.md §4 (measured table) from a bench.py JSON line.
+Usage: python tools/baseline_table.py profiles/r1_bench_c2.json > /tmp/section.md"""
+import json
+import sys
+
+
+def main(path):
+    d = json.loads([ln for ln in open(path) if ln.startswith("{")][-1])
+    r = d["roofline"]
+    e = d["e2e"]
+    cpu = d.get("cpu_baseline") or {}
+    out = []
+    out.append("## 4. Measured on B200 (round 1; `bench.py`, config C2: Kuhn n=15, K = 20 250, 1 GPU)\n")
+    out.append(f"Headline: N={d['config']['order']} {d['dtype'].upper()}, {d['value'] / 1e9:.2f} G DOF-updates/s = "
+               f"{r['achieved']:.2f} TFLOP/s ({100 * r['frac']:.1f}% of the measured FP64 DMMA peak), "
+               f"{d['ms_per_step']:.4f} ms per LSERK4 step.")
+    out.append(f"End to end through the C ABI with host buffers (H2D + step + D2H every step, pipelined async API): "
+               f"{e['value'] / 1e9:.2f} G DOF-updates/s ({e['ms_per_step']:.3f} ms/step); blocking API: "
+               f"{e['sync']['value'] / 1e9:.2f} G DOF-updates/s ({e['sync']['ms_per_step']:.3f} ms/step).")
+    if cpu:
+        out.append(f"CPU oracle on the same config, {cpu['cores']} host cores: {cpu['value'] / 1e6:.2f} M DOF-updates/s.")
+    lg = d.get("large")
+    if lg:
+        out.append(f"HBM-resident C4 (K = {lg['K_total']}, N=4 FP64): {lg['ms_per_step']:.3f} ms/step, "
+                   f"{lg['dof_updates_per_s'] / 1e9:.2f} G DOF-updates/s, {100 * lg['roofline']['frac']:.1f}% of DMMA peak, "
+                   f"DRAM traffic {lg['roofline']['traffic'] / 1e9:.2f} GB per stage launch (ncu).")
+    out.append("The paper's best single-precision figure on a GTX 280 (250 GFLOP/s, PAPER.md:1189-1216) is context only.\n")
+    out.append("| prec | N | ms/step | G DOF-upd/s | TFLOP/s | bound | roofline |")
+    out.append("|---|---|---|---|---|---|---|")
+    for x in d.get("sweep", []):
+        rr = x["roofline"]
+        out.append(f"| {x['precision']} | {x['N']} | {x['ms_per_step']:.4f} | {x['dof_updates_per_s'] / 1e9:.2f} | "
+                   f"{x['gflops'] / 1e3:.2f} | {rr['bound']} | {100 * rr['frac']:.1f}% of {rr['peak']} {rr['unit']} |")
+    for x in d.get("acoustics", []):
+        rr = x["roofline"]
+        out.append(f"| {x['precision']} acoustics | {x['N']} | {x['ms_per_step']:.4f} | {x['dof_updates_per_s'] / 1e9:.2f} | "
+                   f"{x['gflops'] / 1e3:.2f} | {rr['bound']} | {100 * rr['frac']:.1f}% of {rr['peak']} {rr['unit']} |")
+    out.append("")
+    out.append("* The state at C2 is L2-resident for small N, and L2 is flushed before every timed step; C4 is the HBM-resident line.")
+    out.append("* FP64 contractions run on DMMA (WS kernel; MMA kernel at N=1); FP32 on 3xTF32 HMMA, except N=1 FP32 (FFMA BASIC).")
+    out.append("* Acoustics (NEXT-3) runs on the BASIC kernel.")
+    out.append(f"* Raw JSON: `{path}`.")
+    print("\n".join(out))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
