@@ -167,9 +167,11 @@ __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
 }
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// no "memory" clobber: consecutive polls may be in flight together (ordering comes from the
+// acquire fence that follows them)
 __device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
   unsigned v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ bool mbar_test(uint64_t* b, unsigned parity) {
@@ -242,7 +244,6 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
   uint64_t* bar_empty = bars + 3 * S;
   uint64_t* bar_done = bars + 4 * S;  // fused [2S]: MMA warps done with tile jj (-> publisher)
   volatile long long* published = reinterpret_cast<volatile long long*>(bars + 6 * S);  // fused
-  int* vok = reinterpret_cast<int*>(bars + 6 * S + 2);  // fused: per-candidate dependency check results
   constexpr int NTK = FUSED ? C::NTF : C::NT;
   auto sU = [&](int s) { return reinterpret_cast<double*>(smem + size_t(s) * C::SLOT + C::OFF_U); };
   auto sR = [&](int s) { return reinterpret_cast<double*>(smem + size_t(s) * C::SLOT + C::OFF_R); };
@@ -316,18 +317,16 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
       const long long t0 = clock64();
       int64_t hi = j0;
       for (;;) {
-        if (lane < C::VB) vok[lane] = 1;
-        __syncwarp();
+        // all polls of the batch issued back to back; results in a register bitmask
+        unsigned bad = 0;
         for (int64_t x = j0; x < j1; ++x) {
           const int64_t t = tile_of(x);
           const int q0 = fp.nbr_off[t], q1 = fp.nbr_off[t + 1];
           for (int q = q0 + lane; q < q1; q += 32)
-            if (ld_relaxed_gpu(fp.flags + fp.nbr[q]) < target) vok[x - j0] = 0;
+            bad |= unsigned(ld_relaxed_gpu(fp.flags + fp.nbr[q]) < target) << int(x - j0);
         }
-        __syncwarp();
-        hi = j0;
-        while (hi < j1 && vok[hi - j0]) ++hi;
-        __syncwarp();
+        bad = __reduce_or_sync(0xffffffffu, bad);
+        hi = j0 + (bad ? __ffs(bad) - 1 : int(j1 - j0));
         if (hi > j0 || !block) break;
         __nanosleep(64);
         if (clock64() - t0 > (1ll << 35)) __trap();  // broken dependency graph: no silent hang

@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """Stage-fused vs per-stage launch timing: ms per LSERK4 step for k steps per dg_lserk_step
-call, with and without an L2 flush before each call (run with DG_FUSED=0/1)."""
+call, with and without an L2 flush before each call, for DG_VARIANT_FUSED (5) and MMA_WS (3)."""
 import os
 import sys
 
@@ -13,9 +13,9 @@ from paper_1211_0582_b200.dg import Solver  # noqa: E402
 
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
 stream = torch.cuda.Stream()
-for N in [int(a) for a in sys.argv[1:]] or [4, 9]:
+for N, var in [(int(a), v) for a in (sys.argv[1:] or [4, 9]) for v in (5, 3)]:
     VX, E = di.kuhn_box(15)
-    s = Solver(N, variant=3, stream=stream.cuda_stream)
+    s = Solver(N, variant=var, stream=stream.cuda_stream)
     s.mesh_upload(VX, E)
     s.fields_upload(di.random_fields(s.K_local, N, 0))
     dt = di.dt_rule(VX, E, N)
@@ -34,6 +34,6 @@ for N in [int(a) for a in sys.argv[1:]] or [4, 9]:
                     b.record(stream)
                     torch.cuda.synchronize()
                     tot += a.elapsed_time(b)
-            print(f"fused={os.environ.get('DG_FUSED', '1')} N={N} steps/call={k} flush={fl}: "
+            print(f"variant={var} N={N} steps/call={k} flush={fl}: "
                   f"{tot / reps / k:.4f} ms/step", flush=True)
     s.close()
