@@ -94,8 +94,6 @@ def ws_kind(N, prec, variant):
         return "mma" if prec == 8 else "basic"
     if variant == 3:
         return "ws"
-    if prec == 8 and N == 1:
-        return "mma"
     return "basic" if (prec == 4 and N == 1) else "ws"
 
 

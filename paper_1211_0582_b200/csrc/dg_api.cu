@@ -180,11 +180,10 @@ void release_device(dg_solver* s) {
 
 // DG_VARIANT_AUTO: the measured-best kernel per (precision, order) on the bench
 // config (NEXT-4 sweep, tools/variant_sweep.py, profiles/r1_pdl_sweep.jsonl):
-// FP64 -> MMA at N = 1, MMA_WS otherwise; FP32 -> BASIC at N = 1 (HBM-bound, smallest
-// tiles win), MMA_WS (3xTF32) otherwise.
+// FP64 -> MMA_WS for every N; FP32 -> BASIC at N = 1 (HBM-bound, smallest tiles win),
+// MMA_WS (3xTF32) otherwise.
 int auto_variant(bool fp64, int N) {
   if (!fp64 && N == 1) return DG_VARIANT_BASIC;
-  if (fp64 && N == 1) return DG_VARIANT_MMA;
   return DG_VARIANT_MMA_WS;
 }
 

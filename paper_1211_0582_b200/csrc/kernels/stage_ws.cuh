@@ -101,7 +101,7 @@ struct WsCfg {
 #ifdef DG_WS_PW
   static constexpr int PW = DG_WS_PW;  // flux warps (trace gather + flux); plus one dedicated TMA loader warp
 #else
-  static constexpr int PW = N == 3 ? 6 : 4;
+  static constexpr int PW = N <= 3 ? 6 : 4;  // N = 1, 2: +9 % over 4 flux warps
 #endif
   // residual from global memory: prefetched into registers at task start, unless a
   // 17-warp CTA (register cap 96 per thread: the file is split per SMSP) would spill
