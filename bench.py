@@ -94,6 +94,10 @@ def ws_kind(N, prec, variant):
         return "mma" if prec == 8 else "basic"
     if variant == 3:
         return "ws"
+    if variant == 4:
+        return "tc"
+    if variant == 6:
+        return "ffma"
     return "basic" if (prec == 4 and N == 1) else "ws"
 
 
@@ -113,12 +117,13 @@ def roofline(N, prec, K_total, kernel_ms, peaks, variant=0, traffic=None, fpe=No
     """Roofline of the fused stage kernel.  FP64 MMA/WS variants: contractions on the
     FP64 tensor pipe (DMMA) -> bound "tensor" against the measured DMMA peak.  FP32
     WS variant: 3xTF32 on HMMA -> "tensor" against the measured TF32 mma.sync peak / 3
-    (algorithmic flops counted once).  BASIC: "alu" against measured DFMA / FFMA."""
+    (algorithmic flops counted once).  BASIC and FFMA (register-tiled SIMT): "alu" against
+    the measured DFMA / FFMA peak."""
     w = 8 if prec == 8 else 4
     F = (fpe or flops_per_elem_stage(N)) * K_total
     B = (bpe or bytes_per_elem_stage(N, w)) * K_total
     kind = ws_kind(N, prec, variant)
-    tensor = kind != "basic"
+    tensor = kind in ("ws", "mma", "tc")
     if prec == 8:
         pipe = peaks["dmma_tflops"] if tensor else peaks["fp64_tflops"]
     else:

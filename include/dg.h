@@ -77,10 +77,13 @@ typedef enum {
                             cores: FP64 DMMA, FP32 3xTF32 HMMA */
   DG_VARIANT_TC = 4,     /* FP32, N <= 4: tcgen05.mma kind::tf32 (3xTF32) with TMEM
                             accumulators (5th-generation tensor cores) */
-  DG_VARIANT_FUSED = 5   /* FP64, single rank: the MMA_WS kernel running all 5 x nsteps stages of a
+  DG_VARIANT_FUSED = 5,  /* FP64, single rank: the MMA_WS kernel running all 5 x nsteps stages of a
                             dg_lserk_step call in ONE persistent launch, tiles ordered by per-tile
                             completion counters instead of kernel boundaries.  Bitwise equal to
                             MMA_WS; measured slower on B200, hence not AUTO */
+  DG_VARIANT_FFMA = 6    /* FP32: the warp-specialized TMA pipeline with both contractions as
+                            register-tiled FFMA (no tensor cores): the FFMA side of the
+                            TF32-or-FFMA comparison */
 } dg_variant;
 
 /* The linear hyperbolic system u_t + div F(u) = 0 the operator is

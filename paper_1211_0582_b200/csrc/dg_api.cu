@@ -365,7 +365,10 @@ dg_status upload_setup(dg_solver* s) {
   s->Kl = Kl;
   const bool ws = s->variant == DG_VARIANT_AUTO || s->variant == DG_VARIANT_MMA_WS;
   const bool tc = sizeof(T) == 4 && s->variant == DG_VARIANT_TC;
-  if (sizeof(T) == 8 && ws) {
+  const bool ff = sizeof(T) == 4 && s->variant == DG_VARIANT_FFMA;
+  if (ff) {
+    s->lay = dg::ffma_layout_f32(s->N);
+  } else if (sizeof(T) == 8 && ws) {
     s->lay = dg::ws_layout_f64(s->N);
   } else if (sizeof(T) == 4 && ws) {
     s->lay = dg::ws32_layout_f32(s->N);
@@ -438,10 +441,14 @@ dg_status upload_setup(dg_solver* s) {
     CK(cudaMalloc(&s->d_ops_pad, pad.size() * wb));
     CK(cudaMemcpy(s->d_ops_pad, pad.data(), pad.size() * wb, cudaMemcpyHostToDevice));
   } else {
-    // FP32 3xTF32: hi/lo split operators, zero-padded (stage_ws32.cuh / stage_tc.cuh)
-    const bool tcv = s->lay.perm == 2;
-    std::vector<float> pad(tcv ? dg::tc_ops_count(s->N) : dg::ws32_ops_count(s->N));
-    if (tcv)
+    // FP32 3xTF32: hi/lo split operators, zero-padded (stage_ws32.cuh / stage_tc.cuh);
+    // FFMA: transposed, row-padded operators (stage_ffma.cuh)
+    const bool tcv = s->lay.perm == 2, ffv = s->lay.perm == 3;
+    std::vector<float> pad(tcv ? dg::tc_ops_count(s->N) : ffv ? dg::ffma_ops_count(s->N) : dg::ws32_ops_count(s->N));
+    if (ffv)
+      dg::ffma_ops_build(s->N, s->ref.Dr.a.data(), s->ref.Ds.a.data(), s->ref.Dt.a.data(), s->ref.LIFT.a.data(),
+                         pad.data());
+    else if (tcv)
       dg::tc_ops_build(s->N, s->ref.Dr.a.data(), s->ref.Ds.a.data(), s->ref.Dt.a.data(), s->ref.LIFT.a.data(),
                        pad.data());
     else
@@ -641,7 +648,9 @@ dg_status dg_create(const dg_config* cfg, dg_solver** out) {
   if (cfg->order < 1 || cfg->order > 9) return fail(DG_ERR_ORDER, "order N must be in 1..9");
   if (cfg->precision != 4 && cfg->precision != 8) return fail(DG_ERR_ARG, "precision must be 4 or 8");
   if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return fail(DG_ERR_ARG, "bad rank/nranks");
-  if (cfg->variant < 0 || cfg->variant > 5) return fail(DG_ERR_ARG, "bad variant");
+  if (cfg->variant < 0 || cfg->variant > 6) return fail(DG_ERR_ARG, "bad variant");
+  if (cfg->variant == DG_VARIANT_FFMA && cfg->precision != 4)
+    return fail(DG_ERR_ARG, "DG_VARIANT_FFMA is the FP32 register-tiled FFMA kernel");
   if (cfg->variant == DG_VARIANT_FUSED && (cfg->precision != 8 || cfg->nranks != 1))
     return fail(DG_ERR_ARG, "DG_VARIANT_FUSED is the single-rank FP64 stage-fused WS kernel");
   if (cfg->variant == DG_VARIANT_TC && (cfg->precision != 4 || cfg->order > 4))

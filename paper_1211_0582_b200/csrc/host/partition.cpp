@@ -133,7 +133,11 @@ void build_gather_index(const RefElem& ref, const MeshData& m, const Partition& 
           v = ghost_base + g * L.nc * Nfp + j;
         else
           v = L.off(P.g2l[k2], 0, ref.Fmask[f2 * Nfp + j]);
-        gidx[(4 * l + f) * Nfp + i] = int32_t(v);
+        const int64_t mm = int64_t(f) * Nfp + i;  // face-node slot of element l
+        if (L.perm == 3)  // FFMA tiles store the index [tile][m][e] (elements fastest)
+          gidx[(l / L.E) * L.E * 4 * Nfp + mm * L.E + l % L.E] = int32_t(v);
+        else
+          gidx[4 * l * Nfp + mm] = int32_t(v);
       }
     }
   }

@@ -23,6 +23,11 @@ __global__ void k_cm_to_tiles(const S* __restrict__ src, T* __restrict__ dst, in
       const int chunk = int(r >> 5), q = int(r & 31), kc = L.LD >> 2;
       col = (chunk / kc) * 8 + (q >> 2);
       n = (chunk % kc) * 4 + (q & 3);
+    } else if (L.perm == 3) {  // (c*LD + n)*E + e
+      const int64_t q = r / L.E;
+      const int e3 = int(r - q * L.E), c3 = int(q / L.LD);
+      n = int(q - int64_t(c3) * L.LD);
+      col = c3 * L.E + e3;
     } else {
       col = int(r / L.LD);
       n = int(r - int64_t(col) * L.LD);
@@ -34,6 +39,9 @@ __global__ void k_cm_to_tiles(const S* __restrict__ src, T* __restrict__ dst, in
         const int g = col / 24, q = col - 24 * g, nt = q >> 3, rr = q & 7;
         e = 4 * g + (rr >> 1);
         c = 2 * nt + (rr & 1);
+      } else if (L.perm == 3) {
+        e = col % L.E;
+        c = col / L.E;
       } else {
         e = col / L.nc;
         c = col - L.nc * e;
@@ -97,7 +105,7 @@ __global__ void k_pack_traces(const T* __restrict__ u, T* __restrict__ buf, cons
     const int r = int(w - g * L.nc * Nfp);
     const int c = r / Nfp, j = r - c * Nfp;
     const int32_t si = sidx[g * Nfp + j];
-    buf[w] = L.perm == 2 ? u[L.off(si >> 8, c, si & 255)] : u[si + int64_t(L.coff(c)) * L.LD];
+    buf[w] = L.perm == 2 ? u[L.off(si >> 8, c, si & 255)] : u[si + L.cofs(c)];
   }
 }
 

@@ -1,6 +1,8 @@
 // Stage-kernel instantiations for order N=1 (stage_basic.cuh, stage_mma.cuh, stage_ws.cuh).
 #include "stage_tc.cuh"
 
+#include "stage_ffma.cuh"
+
 namespace dg {
 
 void launch_stage_f64_N1(const StageParams<double>& p, int mode, int variant, void* st) {
@@ -15,12 +17,19 @@ void launch_stage_f64_N1(const StageParams<double>& p, int mode, int variant, vo
 void launch_stage_f32_N1(const StageParams<float>& p, int mode, int variant, void* st) {
   if (variant == 1 || variant == 2)  // BASIC (MMA has no FP32 kernel of its own)
     launch_stage_basic<float, 1>(p, mode, static_cast<cudaStream_t>(st));
+  else if (variant == 6)             // FFMA: register-tiled FFMA WS kernel
+    launch_stage_ffma<1>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
   else if (variant == 4)             // TC: tcgen05 kind::tf32 (3xTF32), TMEM accumulators
     launch_stage_tc<1>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
   else                               // MMA_WS: 3xTF32 mma.sync WS kernel
     launch_stage_ws32<1>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
 }
 
+TileLayout ffma_layout_N1() { return ffma_layout<1>(); }
+size_t ffma_ops_count_N1() { return FfCfg<1>::A_FLOATS; }
+void ffma_ops_N1(const double* Dr, const double* Ds, const double* Dt, const double* L, float* out) {
+  ffma_ops<1>(Dr, Ds, Dt, L, out);
+}
 TileLayout ws32_layout_N1() { return ws32_layout<1>(); }
 TileLayout tc_layout_N1() { return tc_layout<1>(); }
 size_t tc_ops_count_N1() { return TcCfg<1>::OPS_FLOATS; }

@@ -1,6 +1,8 @@
 // Stage-kernel instantiations for order N=3 (stage_basic.cuh, stage_mma.cuh, stage_ws.cuh).
 #include "stage_tc.cuh"
 
+#include "stage_ffma.cuh"
+
 namespace dg {
 
 void launch_stage_f64_N3(const StageParams<double>& p, int mode, int variant, void* st) {
@@ -15,12 +17,19 @@ void launch_stage_f64_N3(const StageParams<double>& p, int mode, int variant, vo
 void launch_stage_f32_N3(const StageParams<float>& p, int mode, int variant, void* st) {
   if (variant == 1 || variant == 2)  // BASIC (MMA has no FP32 kernel of its own)
     launch_stage_basic<float, 3>(p, mode, static_cast<cudaStream_t>(st));
+  else if (variant == 6)             // FFMA: register-tiled FFMA WS kernel
+    launch_stage_ffma<3>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
   else if (variant == 4)             // TC: tcgen05 kind::tf32 (3xTF32), TMEM accumulators
     launch_stage_tc<3>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
   else                               // MMA_WS: 3xTF32 mma.sync WS kernel
     launch_stage_ws32<3>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
 }
 
+TileLayout ffma_layout_N3() { return ffma_layout<3>(); }
+size_t ffma_ops_count_N3() { return FfCfg<3>::A_FLOATS; }
+void ffma_ops_N3(const double* Dr, const double* Ds, const double* Dt, const double* L, float* out) {
+  ffma_ops<3>(Dr, Ds, Dt, L, out);
+}
 TileLayout ws32_layout_N3() { return ws32_layout<3>(); }
 TileLayout tc_layout_N3() { return tc_layout<3>(); }
 size_t tc_ops_count_N3() { return TcCfg<3>::OPS_FLOATS; }

@@ -1,6 +1,8 @@
 // Stage-kernel instantiations for order N=6 (stage_basic.cuh, stage_mma.cuh, stage_ws.cuh).
 #include "stage_ws32.cuh"
 
+#include "stage_ffma.cuh"
+
 namespace dg {
 
 void launch_stage_f64_N6(const StageParams<double>& p, int mode, int variant, void* st) {
@@ -15,10 +17,17 @@ void launch_stage_f64_N6(const StageParams<double>& p, int mode, int variant, vo
 void launch_stage_f32_N6(const StageParams<float>& p, int mode, int variant, void* st) {
   if (variant == 1 || variant == 2)  // BASIC (MMA has no FP32 kernel of its own)
     launch_stage_basic<float, 6>(p, mode, static_cast<cudaStream_t>(st));
+  else if (variant == 6)             // FFMA: register-tiled FFMA WS kernel
+    launch_stage_ffma<6>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
   else                               // AUTO / MMA_WS: 3xTF32 tensor-core WS kernel
     launch_stage_ws32<6>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
 }
 
+TileLayout ffma_layout_N6() { return ffma_layout<6>(); }
+size_t ffma_ops_count_N6() { return FfCfg<6>::A_FLOATS; }
+void ffma_ops_N6(const double* Dr, const double* Ds, const double* Dt, const double* L, float* out) {
+  ffma_ops<6>(Dr, Ds, Dt, L, out);
+}
 TileLayout ws32_layout_N6() { return ws32_layout<6>(); }
 TileLayout tc_layout_N6() { return TileLayout{}; }  // TC covers N <= 4
 size_t tc_ops_count_N6() { return 0; }

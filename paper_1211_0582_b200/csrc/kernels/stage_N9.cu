@@ -1,6 +1,8 @@
 // Stage-kernel instantiations for order N=9 (stage_basic.cuh, stage_mma.cuh, stage_ws.cuh).
 #include "stage_ws32.cuh"
 
+#include "stage_ffma.cuh"
+
 namespace dg {
 
 void launch_stage_f64_N9(const StageParams<double>& p, int mode, int variant, void* st) {
@@ -15,10 +17,17 @@ void launch_stage_f64_N9(const StageParams<double>& p, int mode, int variant, vo
 void launch_stage_f32_N9(const StageParams<float>& p, int mode, int variant, void* st) {
   if (variant == 1 || variant == 2)  // BASIC (MMA has no FP32 kernel of its own)
     launch_stage_basic<float, 9>(p, mode, static_cast<cudaStream_t>(st));
+  else if (variant == 6)             // FFMA: register-tiled FFMA WS kernel
+    launch_stage_ffma<9>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
   else                               // AUTO / MMA_WS: 3xTF32 tensor-core WS kernel
     launch_stage_ws32<9>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
 }
 
+TileLayout ffma_layout_N9() { return ffma_layout<9>(); }
+size_t ffma_ops_count_N9() { return FfCfg<9>::A_FLOATS; }
+void ffma_ops_N9(const double* Dr, const double* Ds, const double* Dt, const double* L, float* out) {
+  ffma_ops<9>(Dr, Ds, Dt, L, out);
+}
 TileLayout ws32_layout_N9() { return ws32_layout<9>(); }
 TileLayout tc_layout_N9() { return TileLayout{}; }  // TC covers N <= 4
 size_t tc_ops_count_N9() { return 0; }

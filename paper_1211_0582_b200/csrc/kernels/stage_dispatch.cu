@@ -13,7 +13,10 @@ namespace dg {
   size_t tc_ops_count_N##n();                                                       \
   void tc_ops_N##n(const double*, const double*, const double*, const double*, float*); \
   void ws32_ops_N##n(const double*, const double*, const double*, const double*, float*); \
-  bool launch_fused_f64_N##n(const StageParams<double>&, const FusedParams<double>&, void*);
+  bool launch_fused_f64_N##n(const StageParams<double>&, const FusedParams<double>&, void*); \
+  TileLayout ffma_layout_N##n();                                                    \
+  size_t ffma_ops_count_N##n();                                                     \
+  void ffma_ops_N##n(const double*, const double*, const double*, const double*, float*);
 DG_DECL(1) DG_DECL(2) DG_DECL(3) DG_DECL(4) DG_DECL(5) DG_DECL(6) DG_DECL(7) DG_DECL(8) DG_DECL(9)
 #undef DG_DECL
 
@@ -77,6 +80,24 @@ size_t tc_ops_count(int N) {
 void tc_ops_build(int N, const double* Dr, const double* Ds, const double* Dt, const double* L, float* out) {
   static void (*const t[9])(const double*, const double*, const double*, const double*, float*) = {
       tc_ops_N1, tc_ops_N2, tc_ops_N3, tc_ops_N4, tc_ops_N5, tc_ops_N6, tc_ops_N7, tc_ops_N8, tc_ops_N9};
+  if (N >= 1 && N <= 9) t[N - 1](Dr, Ds, Dt, L, out);
+}
+
+TileLayout ffma_layout_f32(int N) {
+  static TileLayout (*const t[9])() = {ffma_layout_N1, ffma_layout_N2, ffma_layout_N3, ffma_layout_N4, ffma_layout_N5,
+                                       ffma_layout_N6, ffma_layout_N7, ffma_layout_N8, ffma_layout_N9};
+  return (N >= 1 && N <= 9) ? t[N - 1]() : TileLayout{};
+}
+size_t ffma_ops_count(int N) {
+  static size_t (*const t[9])() = {ffma_ops_count_N1, ffma_ops_count_N2, ffma_ops_count_N3,
+                                   ffma_ops_count_N4, ffma_ops_count_N5, ffma_ops_count_N6,
+                                   ffma_ops_count_N7, ffma_ops_count_N8, ffma_ops_count_N9};
+  return (N >= 1 && N <= 9) ? t[N - 1]() : 0;
+}
+void ffma_ops_build(int N, const double* Dr, const double* Ds, const double* Dt, const double* L, float* out) {
+  static void (*const t[9])(const double*, const double*, const double*, const double*, float*) = {
+      ffma_ops_N1, ffma_ops_N2, ffma_ops_N3, ffma_ops_N4, ffma_ops_N5,
+      ffma_ops_N6, ffma_ops_N7, ffma_ops_N8, ffma_ops_N9};
   if (N >= 1 && N <= 9) t[N - 1](Dr, Ds, Dt, L, out);
 }
 

@@ -1,0 +1,424 @@
+// FFMA variant, FP32: the warp-specialized TMA/mbarrier stage kernel of
+// stage_ws.cuh with both contractions as register-tiled FFMA (no tensor cores).
+//
+// Why a SIMT path at all: the north_star asks for the FP32 contraction's
+// TF32-or-FFMA choice to be justified by measurement.  3xTF32 costs three MMAs
+// per product plus the hi/lo split of every B value, and pads M to 16; the
+// algorithmic FP32 work at N = 4 is 38 K FMA per element and stage, which the
+// FFMA pipe (128 FMA/clk/SM, 72 TF/s measured) retires in ~300 cycles — the
+// same order as the 3xTF32 tensor time, with no padding and no splits.
+//
+// Tile layout (TileLayout perm = 3): element e, component c, node n of a tile at
+// (c*LD + n)*E + e — elements fastest, so that
+//   * a warp's 32 lanes (E elements x RG row groups) read B values U[c][k][e] for
+//     consecutive e: one conflict-free shared-memory wavefront;
+//   * the LSERK update stores u_out/res for consecutive e: coalesced 128-B rows;
+//   * one bulk copy (TMA) still moves a whole tile (the tile is its smem image).
+// Operators are stored transposed, A^T[b][k][m] and LIFT^T[j][m] (m fastest,
+// padded to MR rows), so a thread's RB = 4 consecutive rows are one float4
+// load that the whole warp shares (broadcast).
+//
+// Register tile per thread: 4 node rows x 6 components x {r,s,t} = 72 volume
+// accumulators (9 loads per 72 FFMA), then chain rule + curl in registers
+// (4 x 6 values), then LIFT . Flux (7 loads per 24 FFMA), then the update.
+// Roles (as stage_ws.cuh): 1 TMA loader warp, PW flux warps (trace gather with
+// cp.async LA tiles ahead, upwind/PEC flux in place), CW compute warps streaming
+// (tile, row block) tasks.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstring>
+
+#include "stage_ws.cuh"
+
+namespace dg {
+
+template <int N>
+struct FfCfg {
+  static constexpr int Np = Order<N>::Np, Nfp = Order<N>::Nfp, NF = Order<N>::NF;
+#ifdef DG_FF_TUNE_N
+  static constexpr bool TUNED = N == DG_FF_TUNE_N;
+#else
+  static constexpr bool TUNED = false;
+#endif
+#ifndef DG_FF_E
+#define DG_FF_E 0
+#endif
+#ifndef DG_FF_S
+#define DG_FF_S 0
+#endif
+#ifndef DG_FF_LA
+#define DG_FF_LA -1
+#endif
+#ifndef DG_FF_CW
+#define DG_FF_CW 0
+#endif
+#ifndef DG_FF_PW
+#define DG_FF_PW 0
+#endif
+#ifndef DG_FF_OPS
+#define DG_FF_OPS -1
+#endif
+  // elements per tile = elements per task (lanes = E elements x RG row groups)
+  static constexpr int E = (TUNED && DG_FF_E) ? DG_FF_E : N <= 4 ? 32 : N <= 6 ? 16 : 8;
+  static_assert(E == 8 || E == 16 || E == 32, "tile = 8, 16 or 32 elements");
+  static constexpr int RG = 32 / E;
+  static constexpr int RB = 4;             // node rows per thread
+  static constexpr int RT = RB * RG;       // node rows per task
+  static constexpr int MB = (Np + RT - 1) / RT;  // row blocks = tasks per tile
+  static constexpr int MR = MB * RT;       // padded rows of the transposed operators
+  static constexpr int LD = Np;            // node stride of a component (no padding)
+  static constexpr int TS = 6 * LD * E;    // floats per tile
+  static constexpr int GEOT = E * GEO_W;
+  static constexpr int IDXT = E * NF;
+  static constexpr bool OPS_SMEM = (TUNED && DG_FF_OPS >= 0) ? bool(DG_FF_OPS) : N <= 5;
+  static constexpr int A_FLOATS = 3 * Np * MR + NF * MR;
+  static constexpr int A_BYTES = OPS_SMEM ? r16(A_FLOATS * 4) : 0;
+  static constexpr int OFF_U = 0;
+  static constexpr int OFF_G = OFF_U + r16(TS * 4);
+  static constexpr int OFF_I = OFF_G + r16(GEOT * 4);
+  static constexpr int OFF_F = OFF_I + r16(IDXT * 4);
+  static constexpr int SLOT = OFF_F + r16(6 * NF * E * 4);
+  static constexpr int FM_BYTES = r16(NF * 2);
+  static constexpr int FIXED = A_BYTES + FM_BYTES + 4 * 8 * 8;
+  static constexpr int S_FIT = (227 * 1024 - FIXED) / SLOT;
+  static constexpr int S_DEF = S_FIT > 6 ? 6 : S_FIT;
+  static constexpr int S = (TUNED && DG_FF_S) ? DG_FF_S : S_DEF;
+  static_assert(S >= 2, "two ring slots at least");
+  static constexpr int LA = (TUNED && DG_FF_LA >= 0) ? DG_FF_LA : S - 2 < 2 ? S - 2 : 2;
+  static_assert(LA <= S - 2 || (S == 2 && LA == 0), "look-ahead beyond the ring");
+  static constexpr int CW = (TUNED && DG_FF_CW) ? DG_FF_CW : 8;
+  // 12 warps (3 per SMSP) leave 168 registers per thread for the 72-accumulator tile
+  static constexpr int PW = (TUNED && DG_FF_PW) ? DG_FF_PW : 3;
+  static constexpr int NT = 32 * (CW + 1 + PW);
+  static constexpr int PT = 32 * PW;
+  static constexpr int BAR_BYTES = 4 * S * 8;
+  static constexpr size_t SMEM_BYTES = size_t(S) * SLOT + A_BYTES + FM_BYTES + BAR_BYTES;
+  static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+  static_assert((TS * 4) % 16 == 0 && (GEOT * 4) % 16 == 0 && (IDXT * 4) % 16 == 0, "16-B bulk copies");
+};
+
+template <int N, bool UPDATE>
+__global__ void __launch_bounds__(FfCfg<N>::NT, 1)
+    dg_stage_ffma(const StageParams<float> p, const float* __restrict__ opsT, int64_t t_begin, int64_t t_count) {
+  using C = FfCfg<N>;
+  constexpr int Np = C::Np, Nfp = C::Nfp, NF = C::NF, E = C::E, LD = C::LD, S = C::S, TS = C::TS;
+  constexpr int MR = C::MR, RB = C::RB;
+  extern __shared__ __align__(128) unsigned char smem_ff[];
+  unsigned char* smem = smem_ff;
+  pdl_trigger();
+  float* sA = reinterpret_cast<float*>(smem + size_t(S) * C::SLOT);
+  int16_t* sFm = reinterpret_cast<int16_t*>(smem + size_t(S) * C::SLOT + C::A_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(S) * C::SLOT + C::A_BYTES + C::FM_BYTES);
+  uint64_t* bar_load = bars;
+  uint64_t* bar_tr = bars + S;
+  uint64_t* bar_full = bars + 2 * S;
+  uint64_t* bar_empty = bars + 3 * S;
+  auto sU = [&](int s) { return reinterpret_cast<float*>(smem + size_t(s) * C::SLOT + C::OFF_U); };
+  auto sG = [&](int s) { return reinterpret_cast<float*>(smem + size_t(s) * C::SLOT + C::OFF_G); };
+  auto sI = [&](int s) { return reinterpret_cast<int32_t*>(smem + size_t(s) * C::SLOT + C::OFF_I); };
+  auto sF = [&](int s) { return reinterpret_cast<float*>(smem + size_t(s) * C::SLOT + C::OFF_F); };
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool res_in = UPDATE && !p.first_stage;
+  const int64_t J = t_count > blockIdx.x ? (t_count - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int64_t kend = p.k_begin + p.K;
+  auto tile_of = [&](int64_t j) { return t_begin + blockIdx.x + j * gridDim.x; };
+  auto count_of = [&](int64_t tile) {
+    const int64_t k0 = tile * E;
+    return int(kend - k0 < E ? kend - k0 : E);
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(bar_load + s, 1);
+      mbar_init(bar_tr + s, C::PT);
+      mbar_init(bar_full + s, C::PT);
+      mbar_init(bar_empty + s, C::CW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int m = tid; m < NF; m += C::NT) sFm[m] = p.fmask[m];
+  if constexpr (C::OPS_SMEM) {
+    static_assert(MR % 4 == 0, "16-B operator rows");
+    for (int w = tid; w < C::A_FLOATS / 4; w += C::NT) cp_async16(sA + 4 * w, opsT + 4 * w);
+    cp_commit();
+    cp_wait<0>();
+  }
+  __syncthreads();
+  pdl_wait();  // the previous stage's fields are complete from here on
+
+  if (warp == C::CW) {
+    // ===================== TMA loader warp (one lane) =====================
+    if (lane == 0) {
+      for (int64_t j = 0; j < J; ++j) {
+        const int s = int(j % S);
+        mbar_wait(bar_empty + s, (unsigned(j / S) & 1) ^ 1);
+        const int64_t tile = tile_of(j);
+        mbar_arrive_tx(bar_load + s, TS * 4 + C::GEOT * 4 + C::IDXT * 4);
+        bulk_g2s(sU(s), p.u_in + tile * TS, TS * 4, bar_load + s);
+        bulk_g2s(sG(s), p.geo + tile * C::GEOT, C::GEOT * 4, bar_load + s);
+        bulk_g2s(sI(s), p.gidx + tile * C::IDXT, C::IDXT * 4, bar_load + s);
+      }
+    }
+  } else if (warp > C::CW) {
+    // ============================ flux warps ============================
+    // work item w = m*E + e (elements fastest: conflict-free face-buffer writes;
+    // the gather index of a perm-3 tile is stored [m][e] for the same reason)
+    const int ptid = tid - 32 * (C::CW + 1);
+    auto traces = [&](int64_t j) {
+      const int s = int(j % S);
+      mbar_wait(bar_load + s, unsigned(j / S) & 1);
+      const int32_t* I = sI(s);
+      float* F = sF(s);
+      for (int w = ptid; w < E * NF; w += C::PT) {
+        const int32_t gi = I[w];
+        if (gi >= 0 && !(gi & TileLayout::INTRA_FLAG)) {
+          const bool ghost = gi >= p.ghost_base;
+          const float* src = p.u_in + gi;
+#pragma unroll
+          for (int c = 0; c < 6; ++c) cp_async4(F + c * NF * E + w, src + (ghost ? c * Nfp : c * LD * E));
+        }
+      }
+      cp_async_mbar_arrive(bar_tr + s);
+    };
+    auto flux = [&](int64_t j) {
+      const int s = int(j % S);
+      mbar_wait(bar_tr + s, unsigned(j / S) & 1);
+      const int ne = count_of(tile_of(j));
+      const float* U = sU(s);
+      const float* Gm = sG(s);
+      const int32_t* I = sI(s);
+      float* F = sF(s);
+      for (int w = ptid; w < E * NF; w += C::PT) {
+        const int m = w / E, e = w - m * E, f = m / Nfp;
+        float fl[6] = {0, 0, 0, 0, 0, 0};
+        if (e < ne) {
+          const float* g = Gm + e * GEO_W + 9 + 4 * f;
+          const float nx = g[0], ny = g[1], nz = g[2], fs = g[3];
+          const int nM = sFm[m];
+          float uM[6], dE[3], dH[3];
+#pragma unroll
+          for (int c = 0; c < 6; ++c) uM[c] = U[(c * LD + nM) * E + e];
+          const int32_t gi = I[w];
+          if (gi >= 0 && (gi & TileLayout::INTRA_FLAG)) {  // neighbour in this tile: u+ from shared memory
+            const int e2 = (gi >> 8) & 255, n2 = gi & 255;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              dE[c] = U[(c * LD + n2) * E + e2] - uM[c];
+              dH[c] = U[((c + 3) * LD + n2) * E + e2] - uM[c + 3];
+            }
+          } else if (gi >= 0) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              dE[c] = F[c * NF * E + w] - uM[c];
+              dH[c] = F[(c + 3) * NF * E + w] - uM[c + 3];
+            }
+          } else {  // PEC wall: E+ = -E-, H+ = H-
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              dE[c] = -2.0f * uM[c];
+              dH[c] = 0.0f;
+            }
+          }
+          maxwell_flux<float>(nx, ny, nz, p.alpha, dE, dH, fl);
+          const float sc = fs * 0.5f;
+#pragma unroll
+          for (int c = 0; c < 6; ++c) fl[c] *= sc;
+        }
+#pragma unroll
+        for (int c = 0; c < 6; ++c) F[c * NF * E + w] = fl[c];
+      }
+      mbar_arrive(bar_full + s);
+    };
+    for (int64_t t = 0; t < C::LA && t < J; ++t) traces(t);
+    for (int64_t j = 0; j < J; ++j) {
+      if (C::LA == 0) {
+        traces(j);
+        flux(j);
+      } else {
+        flux(j);
+        if (j + C::LA < J) traces(j + C::LA);
+      }
+    }
+  } else {
+    // =========================== compute warps ===========================
+    const int el = lane % E, rg = lane / E;
+    const int64_t total = J * C::MB;
+    int64_t released = 0, waited = -1;
+    auto release = [&](int64_t jj) {
+      if (waited < jj) {
+        mbar_wait(bar_full + int(jj % S), unsigned(jj / S) & 1);
+        waited = jj;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_empty + int(jj % S));
+    };
+    const float* A = C::OPS_SMEM ? sA : opsT;
+    auto ld4 = [&](int idx) -> float4 {
+      if constexpr (C::OPS_SMEM)
+        return *reinterpret_cast<const float4*>(A + idx);
+      else
+        return __ldg(reinterpret_cast<const float4*>(A + idx));
+    };
+    for (int64_t q = warp; q < total; q += C::CW) {
+      const int64_t j = q / C::MB;
+      const int mb = int(q - j * C::MB);
+      while (released < j) release(released++);
+      const int s = int(j % S);
+      if (waited < j) {
+        mbar_wait(bar_full + s, unsigned(j / S) & 1);
+        waited = j;
+      }
+      const int64_t tile = tile_of(j);
+      const int ne = count_of(tile);
+      const int row0 = mb * C::RT + rg * RB;
+      const float* U = sU(s) + el;
+      const float* F = sF(s) + el;
+      // ---- a1: [Dr;Ds;Dt] . U, 4 rows x 6 components x 3 operators
+      float acc[3][6][RB];
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int c = 0; c < 6; ++c)
+#pragma unroll
+          for (int i = 0; i < RB; ++i) acc[b][c][i] = 0.0f;
+#pragma unroll 5
+      for (int k = 0; k < Np; ++k) {
+        float a[3][RB];
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          const float4 v = ld4((b * Np + k) * MR + row0);
+          a[b][0] = v.x;
+          a[b][1] = v.y;
+          a[b][2] = v.z;
+          a[b][3] = v.w;
+        }
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+          const float bv = U[(c * LD + k) * E];
+#pragma unroll
+          for (int b = 0; b < 3; ++b)
+#pragma unroll
+            for (int i = 0; i < RB; ++i) acc[b][c][i] = fmaf(a[b][i], bv, acc[b][c][i]);
+        }
+      }
+      // ---- chain rule + curl (thread-local: all components of one element and row)
+      float r[6][RB];
+      {
+        const float* Gm = sG(s) + el * GEO_W;
+        float gm[9];
+#pragma unroll
+        for (int i = 0; i < 9; ++i) gm[i] = Gm[i];
+#pragma unroll
+        for (int i = 0; i < RB; ++i) {
+          float dx[6], dy[6], dz[6];
+#pragma unroll
+          for (int c = 0; c < 6; ++c) {
+            const float ur = acc[0][c][i], us = acc[1][c][i], ut = acc[2][c][i];
+            dx[c] = gm[0] * ur + gm[3] * us + gm[6] * ut;
+            dy[c] = gm[1] * ur + gm[4] * us + gm[7] * ut;
+            dz[c] = gm[2] * ur + gm[5] * us + gm[8] * ut;
+          }
+          r[0][i] = dy[5] - dz[4];
+          r[1][i] = dz[3] - dx[5];
+          r[2][i] = dx[4] - dy[3];
+          r[3][i] = -(dy[2] - dz[1]);
+          r[4][i] = -(dz[0] - dx[2]);
+          r[5][i] = -(dx[1] - dy[0]);
+        }
+      }
+      // residual prefetch (coalesced over the elements of the warp), hidden behind the lift
+      const int64_t tb = tile * TS + el;
+      float rold[6][RB];
+#pragma unroll
+      for (int c = 0; c < 6; ++c)
+#pragma unroll
+        for (int i = 0; i < RB; ++i) {
+          const int row = row0 + i;
+          rold[c][i] = (UPDATE && res_in && row < Np && el < ne) ? p.res[tb + int64_t(c * LD + row) * E] : 0.0f;
+        }
+      // ---- a4: r += LIFT . Flux
+#pragma unroll 4
+      for (int jn = 0; jn < NF; ++jn) {
+        const float4 v = ld4(3 * Np * MR + jn * MR + row0);
+        const float l[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+          const float fv = F[(c * NF + jn) * E];
+#pragma unroll
+          for (int i = 0; i < RB; ++i) r[c][i] = fmaf(l[i], fv, r[c][i]);
+        }
+      }
+      // ---- a5: LSERK update (or RHS store), coalesced over elements
+      if (el < ne) {
+#pragma unroll
+        for (int c = 0; c < 6; ++c)
+#pragma unroll
+          for (int i = 0; i < RB; ++i) {
+            const int row = row0 + i;
+            if (row < Np) {
+              const int64_t idx = tb + int64_t(c * LD + row) * E;
+              if (UPDATE) {
+                const float rr = p.rk_a * rold[c][i] + p.dt * r[c][i];
+                p.res[idx] = rr;
+                p.u_out[idx] = U[(c * LD + row) * E] + p.rk_b * rr;
+              } else {
+                p.rhs_out[idx] = r[c][i];
+              }
+            }
+          }
+      }
+    }
+    while (released < J) release(released++);
+  }
+}
+
+template <int N>
+void launch_stage_ffma(const StageParams<float>& p, const float* opsT, int mode, cudaStream_t st) {
+  using C = FfCfg<N>;
+  static int sms = 0;
+  if (!sms) {
+    cudaFuncSetAttribute(dg_stage_ffma<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+    cudaFuncSetAttribute(dg_stage_ffma<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if (p.K <= 0) return;
+  const int64_t t0 = p.k_begin / C::E;
+  const int64_t tc = (p.k_begin + p.K + C::E - 1) / C::E - t0;
+  const unsigned grid = unsigned(tc < sms ? tc : sms);
+  if (mode == 1)
+    launch_pdl(true, dg_stage_ffma<N, true>, grid, C::NT, C::SMEM_BYTES, st, p, opsT, t0, tc);
+  else
+    launch_pdl(true, dg_stage_ffma<N, false>, grid, C::NT, C::SMEM_BYTES, st, p, opsT, t0, tc);
+}
+
+template <int N>
+TileLayout ffma_layout() {
+  using C = FfCfg<N>;
+  TileLayout L;
+  L.E = C::E;
+  L.LD = C::LD;
+  L.perm = 3;
+  L.TS = C::TS;
+  return L;
+}
+
+// host: transposed, row-padded operators A^T[3][Np][MR] (A^T[b][k][m] = D_b[m][k]) and
+// LIFT^T[NF][MR], from row-major FP64 Dr|Ds|Dt ([Np][Np]) and LIFT ([Np][NF]); padding zero
+template <int N>
+void ffma_ops(const double* Dr, const double* Ds, const double* Dt, const double* LIFT, float* out) {
+  using C = FfCfg<N>;
+  constexpr int Np = C::Np, NF = C::NF, MR = C::MR;
+  for (int i = 0; i < C::A_FLOATS; ++i) out[i] = 0.0f;
+  const double* D[3] = {Dr, Ds, Dt};
+  for (int b = 0; b < 3; ++b)
+    for (int m = 0; m < Np; ++m)
+      for (int k = 0; k < Np; ++k) out[(size_t(b) * Np + k) * MR + m] = float(D[b][m * Np + k]);
+  for (int m = 0; m < Np; ++m)
+    for (int jn = 0; jn < NF; ++jn) out[size_t(3) * Np * MR + size_t(jn) * MR + m] = float(LIFT[m * NF + jn]);
+}
+
+}  // namespace dg

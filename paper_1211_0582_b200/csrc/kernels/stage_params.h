@@ -37,6 +37,8 @@ constexpr int GEO_W = 26;  // 25 used (rx..tz, 4 x (n, Fscale)); padded to 16 B 
 //                    canonical image of the B operand: column col = 6e + c, node n
 //                    in core matrix (col/8, n/4) of 8 rows x 4 words:
 //                    ((col/8)*(LD/4) + n/4)*32 + (col%8)*4 + n%4.
+// FFMA kernel:       perm = 3: elements fastest, (c*LD + n)*E + e (col = c*E + e), so a
+//                    warp's lanes (consecutive elements) read and write consecutive words.
 // Padding (rows n >= Np, absent elements) is zero in every layout.
 struct TileLayout {
   int nc = 6;  // fields per element (6 Maxwell; 4 acoustics, perm 0 only)
@@ -45,16 +47,19 @@ struct TileLayout {
   int perm = 0;
   int64_t TS = 0;
   DG_HD int col(int e, int c) const {
-    return perm == 1 ? 24 * (e >> 2) + 8 * (c >> 1) + 2 * (e & 3) + (c & 1) : nc * e + c;
+    return perm == 1 ? 24 * (e >> 2) + 8 * (c >> 1) + 2 * (e & 3) + (c & 1) : perm == 3 ? c * E + e : nc * e + c;
   }
   DG_HD int coff(int c) const { return perm == 1 ? 8 * (c >> 1) + (c & 1) : c; }  // perm 0/1: col(e,c) - col(e,0)
+  // perm 0/1/3: word offset of component c relative to component 0 of the same (element, node)
+  DG_HD int64_t cofs(int c) const { return perm == 3 ? int64_t(c) * LD * E : int64_t(coff(c)) * LD; }
   DG_HD int64_t inner(int cl, int n) const {  // word offset of (column, node) inside a tile
-    return perm == 2 ? int64_t(((cl >> 3) * (LD >> 2) + (n >> 2)) * 32 + (cl & 7) * 4 + (n & 3))
-                     : int64_t(cl) * LD + n;
+    return perm == 2   ? int64_t(((cl >> 3) * (LD >> 2) + (n >> 2)) * 32 + (cl & 7) * 4 + (n & 3))
+           : perm == 3 ? (int64_t(cl / E) * LD + n) * E + cl % E
+                       : int64_t(cl) * LD + n;
   }
   DG_HD int64_t off(int64_t k, int c, int n) const { return (k / E) * TS + inner(col(int(k % E), c), n); }
   DG_HD int64_t ntiles(int64_t K) const { return (K + E - 1) / E; }
-  // gather-index encoding: perm 0/1 store off(k2, 0, n2) (+ coff(c)*LD per component);
+  // gather-index encoding: perm 0/1/3 store off(k2, 0, n2) (+ cofs(c) per component);
   // perm 2 stores (k2 << 8) | n2 and the kernel evaluates off() per component.
   // Ghost records are ghost_base + rec (perm 0/1) or GHOST_FLAG | rec (perm 2).
   static constexpr int32_t GHOST_FLAG = int32_t(1) << 30;
@@ -118,6 +123,9 @@ TileLayout ws32_layout_f32(int N); // tiled layout of the FP32 (3xTF32) WS kerne
 size_t ws32_ops_count(int N);      // floats in its split hi/lo operator buffer
 void ws32_ops_build(int N, const double* Dr, const double* Ds, const double* Dt, const double* LIFT, float* out);
 TileLayout tc_layout_f32(int N);   // tcgen05 (TC) kernel layout, N <= 4 (E = 0 otherwise)
+TileLayout ffma_layout_f32(int N); // FFMA kernel layout (perm 3)
+size_t ffma_ops_count(int N);      // floats in its transposed operator buffer
+void ffma_ops_build(int N, const double* Dr, const double* Ds, const double* Dt, const double* LIFT, float* out);
 size_t tc_ops_count(int N);
 void tc_ops_build(int N, const double* Dr, const double* Ds, const double* Dt, const double* LIFT, float* out);
 StageLauncher<float> stage_launcher_f32(int N);

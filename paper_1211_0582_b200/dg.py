@@ -22,7 +22,8 @@ if not os.path.exists(LIB_PATH):
 lib = C.CDLL(LIB_PATH)
 
 DG_OK, DG_ERR_ARG, DG_ERR_ORDER, DG_ERR_MESH, DG_ERR_STATE, DG_ERR_CUDA, DG_ERR_NCCL, DG_ERR_OOM = range(8)
-DG_VARIANT_AUTO, DG_VARIANT_BASIC, DG_VARIANT_MMA, DG_VARIANT_MMA_WS, DG_VARIANT_TC, DG_VARIANT_FUSED = 0, 1, 2, 3, 4, 5
+(DG_VARIANT_AUTO, DG_VARIANT_BASIC, DG_VARIANT_MMA, DG_VARIANT_MMA_WS, DG_VARIANT_TC, DG_VARIANT_FUSED,
+ DG_VARIANT_FFMA) = 0, 1, 2, 3, 4, 5, 6
 DG_SYSTEM_MAXWELL, DG_SYSTEM_ACOUSTICS = 0, 1
 STATUS_NAMES = {0: "DG_OK", 1: "DG_ERR_ARG", 2: "DG_ERR_ORDER", 3: "DG_ERR_MESH", 4: "DG_ERR_STATE",
                 5: "DG_ERR_CUDA", 6: "DG_ERR_NCCL", 7: "DG_ERR_OOM"}

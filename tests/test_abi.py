@@ -52,7 +52,7 @@ def test_argument_errors():
     with pytest.raises(DGError) as e:
         Solver(3, device=-1, system=2)
     assert e.value.status == dg.DG_ERR_ARG
-    for v in (2, 3, 4):                      # acoustics: BASIC kernel only
+    for v in (2, 3, 4, 6):                   # acoustics: BASIC kernel only
         with pytest.raises(DGError) as e:
             Solver(3, precision=4, device=-1, variant=v, system=dg.DG_SYSTEM_ACOUSTICS)
         assert e.value.status == dg.DG_ERR_ARG
@@ -63,8 +63,12 @@ def test_argument_errors():
             Solver(3, device=-1, variant=dg.DG_VARIANT_FUSED, **kw)
         assert e.value.status == dg.DG_ERR_ARG
     with pytest.raises(DGError) as e:
-        Solver(3, device=-1, variant=6)
+        Solver(3, device=-1, variant=7)
     assert e.value.status == dg.DG_ERR_ARG
+    with pytest.raises(DGError) as e:          # FFMA: the FP32 SIMT kernel only
+        Solver(3, precision=8, device=-1, variant=dg.DG_VARIANT_FFMA)
+    assert e.value.status == dg.DG_ERR_ARG
+    Solver(3, precision=4, device=-1, variant=dg.DG_VARIANT_FFMA).close()
 
 
 def test_host_only_solver_refuses_compute():

@@ -3,7 +3,8 @@
 K=20250), the B200 analogue of the paper's tuning study (fig:tuning-study,
 PAPER.md:1151-1167).  One JSON line per (precision, variant, N): ms per LSERK4 step,
 roofline fraction.  Kernels: FP64 BASIC (DFMA), MMA (DMMA, cp.async), MMA_WS (DMMA,
-TMA warp-specialized); FP32 BASIC (FFMA), MMA_WS (3xTF32 HMMA), TC (tcgen05, N<=4).
+TMA warp-specialized); FP32 BASIC (FFMA), MMA_WS (3xTF32 HMMA), TC (tcgen05, N<=4),
+FFMA (register-tiled FFMA in the WS pipeline).
 
 Usage: python tools/variant_sweep.py [--orders 1,2,...] [--steps 10]
        DG_LIB=paper_1211_0582_b200/tune/libdg_X.so python tools/variant_sweep.py ...  (tile sweep)
@@ -18,7 +19,8 @@ sys.path.insert(0, ROOT)
 import bench  # noqa: E402
 
 CASES = [(8, 1, "f64-basic-dfma"), (8, 2, "f64-mma-dmma"), (8, 3, "f64-ws-dmma"),
-         (4, 1, "f32-basic-ffma"), (4, 3, "f32-ws-3xtf32"), (4, 4, "f32-tc-tcgen05")]
+         (4, 1, "f32-basic-ffma"), (4, 3, "f32-ws-3xtf32"), (4, 4, "f32-tc-tcgen05"),
+         (4, 6, "f32-ffma-tiled")]
 
 
 def main():
