@@ -181,9 +181,10 @@ void release_device(dg_solver* s) {
 // DG_VARIANT_AUTO: the measured-best kernel per (precision, order) on the bench
 // config (NEXT-4 sweep, tools/variant_sweep.py, profiles/r1_pdl_sweep.jsonl):
 // FP64 -> MMA_WS for every N; FP32 -> BASIC at N = 1 (HBM-bound, smallest tiles win),
-// MMA_WS (3xTF32) otherwise.
+// FFMA (register-tiled SIMT) at N = 2, 3 and 9, MMA_WS (3xTF32 HMMA) at N = 4..8.
 int auto_variant(bool fp64, int N) {
   if (!fp64 && N == 1) return DG_VARIANT_BASIC;
+  if (!fp64 && (N == 2 || N == 3 || N == 9)) return DG_VARIANT_FFMA;
   return DG_VARIANT_MMA_WS;
 }
 
@@ -365,7 +366,7 @@ dg_status upload_setup(dg_solver* s) {
   s->Kl = Kl;
   const bool ws = s->variant == DG_VARIANT_AUTO || s->variant == DG_VARIANT_MMA_WS;
   const bool tc = sizeof(T) == 4 && s->variant == DG_VARIANT_TC;
-  const bool ff = sizeof(T) == 4 && s->variant == DG_VARIANT_FFMA;
+  const bool ff = sizeof(T) == 4 && s->variant == DG_VARIANT_FFMA;  // (AUTO resolved at create)
   if (ff) {
     s->lay = dg::ffma_layout_f32(s->N);
   } else if (sizeof(T) == 8 && ws) {

@@ -20,7 +20,9 @@
 //
 // Register tile per thread: 4 node rows x 6 components x {r,s,t} = 72 volume
 // accumulators (9 loads per 72 FFMA), then chain rule + curl in registers
-// (4 x 6 values), then LIFT . Flux (7 loads per 24 FFMA), then the update.
+// (4 x 6 values), then LIFT . Flux (7 loads per 24 FFMA), then the update.  The
+// residual is cp.async'ed into a per-warp staging buffer at task start (its
+// latency hides behind the contractions without holding 24 registers).
 // Roles (as stage_ws.cuh): 1 TMA loader warp, PW flux warps (trace gather with
 // cp.async LA tiles ahead, upwind/PEC flux in place), CW compute warps streaming
 // (tile, row block) tasks.
@@ -59,8 +61,11 @@ struct FfCfg {
 #ifndef DG_FF_OPS
 #define DG_FF_OPS -1
 #endif
-  // elements per tile = elements per task (lanes = E elements x RG row groups)
-  static constexpr int E = (TUNED && DG_FF_E) ? DG_FF_E : N <= 4 ? 32 : N <= 6 ? 16 : 8;
+  // elements per tile = elements per task (lanes = E elements x RG row groups); measured
+  // (tools/gpu_ffma_tune.sh): smaller tiles win where they cost little row padding, since
+  // 20 250 / (E x 148) tiles per CTA sets the tail imbalance and the ring depth
+  static constexpr int E = (TUNED && DG_FF_E) ? DG_FF_E
+                           : (N == 1 || N == 3) ? 32 : (N == 2 || N == 4 || N == 6) ? 16 : 8;
   static_assert(E == 8 || E == 16 || E == 32, "tile = 8, 16 or 32 elements");
   static constexpr int RG = 32 / E;
   static constexpr int RB = 4;             // node rows per thread
@@ -80,20 +85,36 @@ struct FfCfg {
   static constexpr int OFF_F = OFF_I + r16(IDXT * 4);
   static constexpr int SLOT = OFF_F + r16(6 * NF * E * 4);
   static constexpr int FM_BYTES = r16(NF * 2);
-  static constexpr int FIXED = A_BYTES + FM_BYTES + 4 * 8 * 8;
+  // residual staging: each compute warp cp.async's its task's residual (6 x RB values per
+  // lane) into shared memory at task start, so no registers are held across the contractions
+  static constexpr int STG_FLOATS = 6 * RB * 32;
+  static constexpr int STG_BYTES = 8 * STG_FLOATS * 4;  // up to 8 compute warps (CW <= 8)
+  static constexpr int FIXED = A_BYTES + FM_BYTES + STG_BYTES + 4 * 8 * 8;
   static constexpr int S_FIT = (227 * 1024 - FIXED) / SLOT;
   static constexpr int S_DEF = S_FIT > 6 ? 6 : S_FIT;
   static constexpr int S = (TUNED && DG_FF_S) ? DG_FF_S : S_DEF;
   static_assert(S >= 2, "two ring slots at least");
   static constexpr int LA = (TUNED && DG_FF_LA >= 0) ? DG_FF_LA : S - 2 < 2 ? S - 2 : 2;
   static_assert(LA <= S - 2 || (S == 2 && LA == 0), "look-ahead beyond the ring");
-  static constexpr int CW = (TUNED && DG_FF_CW) ? DG_FF_CW : 8;
-  // 12 warps (3 per SMSP) leave 168 registers per thread for the 72-accumulator tile
-  static constexpr int PW = (TUNED && DG_FF_PW) ? DG_FF_PW : 3;
+#ifndef DG_FF_SPLIT
+#define DG_FF_SPLIT -1
+#endif
+  // Register split (setmaxnreg): 16 warps = 4 warpgroups; the two compute warpgroups grow
+  // to REG_HI registers, the producer warpgroups (loader + 7 flux warps) shrink to REG_LO.
+  // Without it, 12 warps (3 per SMSP) leave 168 registers for the 72-accumulator tile but
+  // only 3 flux warps, which cannot keep up at N <= 4 (ncu: compute warps wait on full[s]).
+  // measured (profiles/r1_ffma_tune.jsonl): N = 1, 2, 3 gain 11-18 %, N = 4 is even, N >= 5 lose 1-5 %
+  static constexpr bool SPLIT = (TUNED && DG_FF_SPLIT >= 0) ? bool(DG_FF_SPLIT) : N <= 4;
+  static constexpr int REG_HI = 192, REG_LO = 64;
+  static constexpr int CW = SPLIT ? 8 : (TUNED && DG_FF_CW) ? DG_FF_CW : 8;
+  static constexpr int PW = SPLIT ? 7 : (TUNED && DG_FF_PW) ? DG_FF_PW : 3;
+  static_assert(!SPLIT || (CW % 4 == 0 && (CW + 1 + PW) % 4 == 0 &&
+                           (CW * REG_HI + (1 + PW) * REG_LO) * 32 <= 65536), "warpgroup register split");
   static constexpr int NT = 32 * (CW + 1 + PW);
   static constexpr int PT = 32 * PW;
   static constexpr int BAR_BYTES = 4 * S * 8;
-  static constexpr size_t SMEM_BYTES = size_t(S) * SLOT + A_BYTES + FM_BYTES + BAR_BYTES;
+  static_assert(CW <= 8, "residual staging sized for 8 compute warps");
+  static constexpr size_t SMEM_BYTES = size_t(S) * SLOT + A_BYTES + FM_BYTES + STG_BYTES + BAR_BYTES;
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   static_assert((TS * 4) % 16 == 0 && (GEOT * 4) % 16 == 0 && (IDXT * 4) % 16 == 0, "16-B bulk copies");
 };
@@ -109,7 +130,9 @@ __global__ void __launch_bounds__(FfCfg<N>::NT, 1)
   pdl_trigger();
   float* sA = reinterpret_cast<float*>(smem + size_t(S) * C::SLOT);
   int16_t* sFm = reinterpret_cast<int16_t*>(smem + size_t(S) * C::SLOT + C::A_BYTES);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(S) * C::SLOT + C::A_BYTES + C::FM_BYTES);
+  float* sStg = reinterpret_cast<float*>(smem + size_t(S) * C::SLOT + C::A_BYTES + C::FM_BYTES);
+  uint64_t* bars =
+      reinterpret_cast<uint64_t*>(smem + size_t(S) * C::SLOT + C::A_BYTES + C::FM_BYTES + C::STG_BYTES);
   uint64_t* bar_load = bars;
   uint64_t* bar_tr = bars + S;
   uint64_t* bar_full = bars + 2 * S;
@@ -148,6 +171,10 @@ __global__ void __launch_bounds__(FfCfg<N>::NT, 1)
   __syncthreads();
   pdl_wait();  // the previous stage's fields are complete from here on
 
+  // role branches: producers (loader + flux warps) first, so that each warpgroup executes one
+  // and the same setmaxnreg instruction (.aligned) and ptxas sees every role's register limit
+  if (warp >= C::CW) {
+  if constexpr (C::SPLIT) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(C::REG_LO));
   if (warp == C::CW) {
     // ===================== TMA loader warp (one lane) =====================
     if (lane == 0) {
@@ -182,52 +209,70 @@ __global__ void __launch_bounds__(FfCfg<N>::NT, 1)
       }
       cp_async_mbar_arrive(bar_tr + s);
     };
+    // flux of IT items per thread at once, branch-free, so the shared-memory loads of
+    // independent items overlap (a single flux warp per SMSP is latency-bound otherwise).
+    // u+ comes from the tile (intra-tile face), the gathered face buffer, or — on a PEC
+    // wall — u- itself with the E jump negated (E+ = -E-, H+ = H-).  Items of elements
+    // beyond the launch range are computed too (harmless: the compute warps skip them).
     auto flux = [&](int64_t j) {
+      constexpr int IT = 2;
+      constexpr int NIT = (E * NF + C::PT - 1) / C::PT;
       const int s = int(j % S);
       mbar_wait(bar_tr + s, unsigned(j / S) & 1);
-      const int ne = count_of(tile_of(j));
       const float* U = sU(s);
       const float* Gm = sG(s);
       const int32_t* I = sI(s);
       float* F = sF(s);
-      for (int w = ptid; w < E * NF; w += C::PT) {
-        const int m = w / E, e = w - m * E, f = m / Nfp;
-        float fl[6] = {0, 0, 0, 0, 0, 0};
-        if (e < ne) {
-          const float* g = Gm + e * GEO_W + 9 + 4 * f;
-          const float nx = g[0], ny = g[1], nz = g[2], fs = g[3];
+#pragma unroll 1
+      for (int it = 0; it < NIT; it += IT) {
+        float uM[IT][6], uP[IT][6], g[IT][4], sE[IT];
+        int wv[IT];
+#pragma unroll
+        for (int q = 0; q < IT; ++q) {
+          const int w0 = ptid + (it + q) * C::PT;
+          const bool ok = (it + q < NIT) && w0 < E * NF;
+          const int w = ok ? w0 : ptid;
+          wv[q] = ok ? w : -1;
+          const int m = w / E, e = w - m * E, f = m / Nfp;
           const int nM = sFm[m];
-          float uM[6], dE[3], dH[3];
-#pragma unroll
-          for (int c = 0; c < 6; ++c) uM[c] = U[(c * LD + nM) * E + e];
           const int32_t gi = I[w];
-          if (gi >= 0 && (gi & TileLayout::INTRA_FLAG)) {  // neighbour in this tile: u+ from shared memory
-            const int e2 = (gi >> 8) & 255, n2 = gi & 255;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              dE[c] = U[(c * LD + n2) * E + e2] - uM[c];
-              dH[c] = U[((c + 3) * LD + n2) * E + e2] - uM[c + 3];
-            }
-          } else if (gi >= 0) {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              dE[c] = F[c * NF * E + w] - uM[c];
-              dH[c] = F[(c + 3) * NF * E + w] - uM[c + 3];
-            }
-          } else {  // PEC wall: E+ = -E-, H+ = H-
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              dE[c] = -2.0f * uM[c];
-              dH[c] = 0.0f;
+          const float* pm = U + nM * E + e;
+          const float* pp = pm;
+          int cs = LD * E;
+          sE[q] = -1.0f;
+          if (gi >= 0) {
+            sE[q] = 1.0f;
+            if (gi & TileLayout::INTRA_FLAG) {
+              pp = U + (gi & 255) * E + ((gi >> 8) & 255);
+            } else {
+              pp = F + w;
+              cs = NF * E;
             }
           }
-          maxwell_flux<float>(nx, ny, nz, p.alpha, dE, dH, fl);
-          const float sc = fs * 0.5f;
 #pragma unroll
-          for (int c = 0; c < 6; ++c) fl[c] *= sc;
+          for (int c = 0; c < 6; ++c) {
+            uM[q][c] = pm[c * LD * E];
+            uP[q][c] = pp[c * cs];
+          }
+          const float* gp = Gm + e * GEO_W + 9 + 4 * f;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) g[q][i] = gp[i];
         }
 #pragma unroll
-        for (int c = 0; c < 6; ++c) F[c * NF * E + w] = fl[c];
+        for (int q = 0; q < IT; ++q) {
+          float dE[3], dH[3], fl[6];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            dE[c] = sE[q] * uP[q][c] - uM[q][c];
+            dH[c] = uP[q][c + 3] - uM[q][c + 3];
+          }
+          maxwell_flux<float>(g[q][0], g[q][1], g[q][2], p.alpha, dE, dH, fl);
+          const float sc = g[q][3] * 0.5f;
+          if (wv[q] >= 0) {
+#pragma unroll
+            for (int c = 0; c < 6; ++c) F[c * NF * E + wv[q]] = fl[c] * sc;
+          }
+        }
       }
       mbar_arrive(bar_full + s);
     };
@@ -241,7 +286,9 @@ __global__ void __launch_bounds__(FfCfg<N>::NT, 1)
         if (j + C::LA < J) traces(j + C::LA);
       }
     }
+  }
   } else {
+    if constexpr (C::SPLIT) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::REG_HI));
     // =========================== compute warps ===========================
     const int el = lane % E, rg = lane / E;
     const int64_t total = J * C::MB;
@@ -275,6 +322,18 @@ __global__ void __launch_bounds__(FfCfg<N>::NT, 1)
       const int row0 = mb * C::RT + rg * RB;
       const float* U = sU(s) + el;
       const float* F = sF(s) + el;
+      const int64_t tb = tile * TS + el;
+      float* stg = sStg + warp * C::STG_FLOATS + lane;  // [c][i][lane]
+      if (UPDATE && res_in) {  // residual -> staging (coalesced over elements), consumed by the update
+        if (el < ne) {
+#pragma unroll
+          for (int c = 0; c < 6; ++c)
+#pragma unroll
+            for (int i = 0; i < RB; ++i)
+              if (row0 + i < Np) cp_async4(stg + (c * RB + i) * 32, p.res + tb + int64_t(c * LD + row0 + i) * E);
+        }
+        cp_commit();
+      }
       // ---- a1: [Dr;Ds;Dt] . U, 4 rows x 6 components x 3 operators
       float acc[3][6][RB];
 #pragma unroll
@@ -328,16 +387,6 @@ __global__ void __launch_bounds__(FfCfg<N>::NT, 1)
           r[5][i] = -(dx[1] - dy[0]);
         }
       }
-      // residual prefetch (coalesced over the elements of the warp), hidden behind the lift
-      const int64_t tb = tile * TS + el;
-      float rold[6][RB];
-#pragma unroll
-      for (int c = 0; c < 6; ++c)
-#pragma unroll
-        for (int i = 0; i < RB; ++i) {
-          const int row = row0 + i;
-          rold[c][i] = (UPDATE && res_in && row < Np && el < ne) ? p.res[tb + int64_t(c * LD + row) * E] : 0.0f;
-        }
       // ---- a4: r += LIFT . Flux
 #pragma unroll 4
       for (int jn = 0; jn < NF; ++jn) {
@@ -351,6 +400,7 @@ __global__ void __launch_bounds__(FfCfg<N>::NT, 1)
         }
       }
       // ---- a5: LSERK update (or RHS store), coalesced over elements
+      if (UPDATE && res_in) cp_wait<0>();
       if (el < ne) {
 #pragma unroll
         for (int c = 0; c < 6; ++c)
@@ -360,7 +410,8 @@ __global__ void __launch_bounds__(FfCfg<N>::NT, 1)
             if (row < Np) {
               const int64_t idx = tb + int64_t(c * LD + row) * E;
               if (UPDATE) {
-                const float rr = p.rk_a * rold[c][i] + p.dt * r[c][i];
+                const float rold = res_in ? stg[(c * RB + i) * 32] : 0.0f;
+                const float rr = p.rk_a * rold + p.dt * r[c][i];
                 p.res[idx] = rr;
                 p.u_out[idx] = U[(c * LD + row) * E] + p.rk_b * rr;
               } else {
