@@ -69,7 +69,7 @@ typedef enum {
 
 typedef enum {
   DG_VARIANT_AUTO = 0,   /* measured best per (precision, N): MMA_WS, except FP32 N=1 -> BASIC,
-                            FP32 N=2,3,9 -> FFMA (tools/variant_sweep.py) */
+                            FP32 N=2,3,9 and FP64 N=1 -> FFMA (tools/variant_sweep.py) */
   DG_VARIANT_BASIC = 1,  /* one fused element-tile kernel per stage, FMA contractions */
   DG_VARIANT_MMA = 2,    /* FP64: DMMA contractions, cp.async-pipelined persistent kernel
                             (FP32: same as BASIC) */
@@ -81,9 +81,10 @@ typedef enum {
                             dg_lserk_step call in ONE persistent launch, tiles ordered by per-tile
                             completion counters instead of kernel boundaries.  Bitwise equal to
                             MMA_WS; measured slower on B200, hence not AUTO */
-  DG_VARIANT_FFMA = 6    /* FP32: the warp-specialized TMA pipeline with both contractions as
-                            register-tiled FFMA (no tensor cores): the FFMA side of the
-                            TF32-or-FFMA comparison */
+  DG_VARIANT_FFMA = 6    /* the warp-specialized TMA pipeline with both contractions as
+                            register-tiled FFMA (FP32) / DFMA (FP64), no tensor cores: the
+                            SIMT side of the TF32-or-FFMA and DMMA-or-DFMA comparisons
+                             */
 } dg_variant;
 
 /* The linear hyperbolic system u_t + div F(u) = 0 the operator is

@@ -180,9 +180,11 @@ void release_device(dg_solver* s) {
 
 // DG_VARIANT_AUTO: the measured-best kernel per (precision, order) on the bench
 // config (NEXT-4 sweep, tools/variant_sweep.py, profiles/r1_pdl_sweep.jsonl):
-// FP64 -> MMA_WS for every N; FP32 -> BASIC at N = 1 (HBM-bound, smallest tiles win),
-// FFMA (register-tiled SIMT) at N = 2, 3 and 9, MMA_WS (3xTF32 HMMA) at N = 4..8.
+// FP64 -> FFMA (register-tiled DFMA) at N = 1, MMA_WS (DMMA) otherwise; FP32 -> BASIC at
+// N = 1 (HBM-bound, smallest tiles win), FFMA (register-tiled SIMT) at N = 2, 3 and 9,
+// MMA_WS (3xTF32 HMMA) at N = 4..8.
 int auto_variant(bool fp64, int N) {
+  if (fp64 && N == 1) return DG_VARIANT_FFMA;
   if (!fp64 && N == 1) return DG_VARIANT_BASIC;
   if (!fp64 && (N == 2 || N == 3 || N == 9)) return DG_VARIANT_FFMA;
   return DG_VARIANT_MMA_WS;
@@ -366,9 +368,9 @@ dg_status upload_setup(dg_solver* s) {
   s->Kl = Kl;
   const bool ws = s->variant == DG_VARIANT_AUTO || s->variant == DG_VARIANT_MMA_WS;
   const bool tc = sizeof(T) == 4 && s->variant == DG_VARIANT_TC;
-  const bool ff = sizeof(T) == 4 && s->variant == DG_VARIANT_FFMA;  // (AUTO resolved at create)
+  const bool ff = s->variant == DG_VARIANT_FFMA;  // (AUTO resolved at create)
   if (ff) {
-    s->lay = dg::ffma_layout_f32(s->N);
+    s->lay = sizeof(T) == 8 ? dg::ffma_layout_f64(s->N) : dg::ffma_layout_f32(s->N);
   } else if (sizeof(T) == 8 && ws) {
     s->lay = dg::ws_layout_f64(s->N);
   } else if (sizeof(T) == 4 && ws) {
@@ -429,7 +431,14 @@ dg_status upload_setup(dg_solver* s) {
     for (int j = 0; j < NF; ++j) ops[size_t(3) * Np * Np + size_t(i) * NF + j] = T(s->ref.LIFT(i, j));
   CK(cudaMalloc(&s->d_ops, ops.size() * wb));
   CK(cudaMemcpy(s->d_ops, ops.data(), ops.size() * wb, cudaMemcpyHostToDevice));
-  if (sizeof(T) == 8) {
+  if (sizeof(T) == 8 && s->lay.perm == 3) {
+    // FFMA (DFMA) kernel: transposed, row-padded operators (stage_ffma.cuh)
+    std::vector<double> pad(dg::ffma64_ops_count(s->N));
+    dg::ffma64_ops_build(s->N, s->ref.Dr.a.data(), s->ref.Ds.a.data(), s->ref.Dt.a.data(), s->ref.LIFT.a.data(),
+                         pad.data());
+    CK(cudaMalloc(&s->d_ops_pad, pad.size() * sizeof(double)));
+    CK(cudaMemcpy(s->d_ops_pad, pad.data(), pad.size() * sizeof(double), cudaMemcpyHostToDevice));
+  } else if (sizeof(T) == 8) {
     // [3][M8][KV] + [M8][NF], zero padding (stage_mma.cuh)
     const int M8 = (Np + 7) / 8 * 8, KV = (Np + 3) / 4 * 4;
     std::vector<T> pad(size_t(3) * M8 * KV + size_t(M8) * NF, T(0));
@@ -650,8 +659,6 @@ dg_status dg_create(const dg_config* cfg, dg_solver** out) {
   if (cfg->precision != 4 && cfg->precision != 8) return fail(DG_ERR_ARG, "precision must be 4 or 8");
   if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return fail(DG_ERR_ARG, "bad rank/nranks");
   if (cfg->variant < 0 || cfg->variant > 6) return fail(DG_ERR_ARG, "bad variant");
-  if (cfg->variant == DG_VARIANT_FFMA && cfg->precision != 4)
-    return fail(DG_ERR_ARG, "DG_VARIANT_FFMA is the FP32 register-tiled FFMA kernel");
   if (cfg->variant == DG_VARIANT_FUSED && (cfg->precision != 8 || cfg->nranks != 1))
     return fail(DG_ERR_ARG, "DG_VARIANT_FUSED is the single-rank FP64 stage-fused WS kernel");
   if (cfg->variant == DG_VARIANT_TC && (cfg->precision != 4 || cfg->order > 4))

@@ -8,6 +8,8 @@ namespace dg {
 void launch_stage_f64_N2(const StageParams<double>& p, int mode, int variant, void* st) {
   if (variant == 1)       // DG_VARIANT_BASIC
     launch_stage_basic<double, 2>(p, mode, static_cast<cudaStream_t>(st));
+  else if (variant == 6)  // DG_VARIANT_FFMA: register-tiled DFMA WS kernel
+    launch_stage_ffma<double, 2>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
   else if (variant == 2)  // DG_VARIANT_MMA: DMMA, cp.async-pipelined, element-major layout
     launch_stage_mma<2>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
   else                    // AUTO / DG_VARIANT_MMA_WS: DMMA, warp-specialized TMA pipeline, tiled layout
@@ -18,17 +20,22 @@ void launch_stage_f32_N2(const StageParams<float>& p, int mode, int variant, voi
   if (variant == 1 || variant == 2)  // BASIC (MMA has no FP32 kernel of its own)
     launch_stage_basic<float, 2>(p, mode, static_cast<cudaStream_t>(st));
   else if (variant == 6)             // FFMA: register-tiled FFMA WS kernel
-    launch_stage_ffma<2>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
+    launch_stage_ffma<float, 2>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
   else if (variant == 4)             // TC: tcgen05 kind::tf32 (3xTF32), TMEM accumulators
     launch_stage_tc<2>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
   else                               // MMA_WS: 3xTF32 mma.sync WS kernel
     launch_stage_ws32<2>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
 }
 
-TileLayout ffma_layout_N2() { return ffma_layout<2>(); }
-size_t ffma_ops_count_N2() { return FfCfg<2>::A_FLOATS; }
+TileLayout ffma_layout_N2() { return ffma_layout<float, 2>(); }
+size_t ffma_ops_count_N2() { return FfCfg<float, 2>::A_FLOATS; }
 void ffma_ops_N2(const double* Dr, const double* Ds, const double* Dt, const double* L, float* out) {
-  ffma_ops<2>(Dr, Ds, Dt, L, out);
+  ffma_ops<float, 2>(Dr, Ds, Dt, L, out);
+}
+TileLayout ffma64_layout_N2() { return ffma_layout<double, 2>(); }
+size_t ffma64_ops_count_N2() { return FfCfg<double, 2>::A_FLOATS; }
+void ffma64_ops_N2(const double* Dr, const double* Ds, const double* Dt, const double* L, double* out) {
+  ffma_ops<double, 2>(Dr, Ds, Dt, L, out);
 }
 TileLayout ws32_layout_N2() { return ws32_layout<2>(); }
 TileLayout tc_layout_N2() { return tc_layout<2>(); }

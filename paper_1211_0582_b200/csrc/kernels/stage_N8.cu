@@ -8,6 +8,8 @@ namespace dg {
 void launch_stage_f64_N8(const StageParams<double>& p, int mode, int variant, void* st) {
   if (variant == 1)       // DG_VARIANT_BASIC
     launch_stage_basic<double, 8>(p, mode, static_cast<cudaStream_t>(st));
+  else if (variant == 6)  // DG_VARIANT_FFMA: register-tiled DFMA WS kernel
+    launch_stage_ffma<double, 8>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
   else if (variant == 2)  // DG_VARIANT_MMA: DMMA, cp.async-pipelined, element-major layout
     launch_stage_mma<8>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
   else                    // AUTO / DG_VARIANT_MMA_WS: DMMA, warp-specialized TMA pipeline, tiled layout
@@ -18,15 +20,20 @@ void launch_stage_f32_N8(const StageParams<float>& p, int mode, int variant, voi
   if (variant == 1 || variant == 2)  // BASIC (MMA has no FP32 kernel of its own)
     launch_stage_basic<float, 8>(p, mode, static_cast<cudaStream_t>(st));
   else if (variant == 6)             // FFMA: register-tiled FFMA WS kernel
-    launch_stage_ffma<8>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
+    launch_stage_ffma<float, 8>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
   else                               // AUTO / MMA_WS: 3xTF32 tensor-core WS kernel
     launch_stage_ws32<8>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
 }
 
-TileLayout ffma_layout_N8() { return ffma_layout<8>(); }
-size_t ffma_ops_count_N8() { return FfCfg<8>::A_FLOATS; }
+TileLayout ffma_layout_N8() { return ffma_layout<float, 8>(); }
+size_t ffma_ops_count_N8() { return FfCfg<float, 8>::A_FLOATS; }
 void ffma_ops_N8(const double* Dr, const double* Ds, const double* Dt, const double* L, float* out) {
-  ffma_ops<8>(Dr, Ds, Dt, L, out);
+  ffma_ops<float, 8>(Dr, Ds, Dt, L, out);
+}
+TileLayout ffma64_layout_N8() { return ffma_layout<double, 8>(); }
+size_t ffma64_ops_count_N8() { return FfCfg<double, 8>::A_FLOATS; }
+void ffma64_ops_N8(const double* Dr, const double* Ds, const double* Dt, const double* L, double* out) {
+  ffma_ops<double, 8>(Dr, Ds, Dt, L, out);
 }
 TileLayout ws32_layout_N8() { return ws32_layout<8>(); }
 TileLayout tc_layout_N8() { return TileLayout{}; }  // TC covers N <= 4

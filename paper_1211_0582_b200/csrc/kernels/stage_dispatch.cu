@@ -16,7 +16,10 @@ namespace dg {
   bool launch_fused_f64_N##n(const StageParams<double>&, const FusedParams<double>&, void*); \
   TileLayout ffma_layout_N##n();                                                    \
   size_t ffma_ops_count_N##n();                                                     \
-  void ffma_ops_N##n(const double*, const double*, const double*, const double*, float*);
+  void ffma_ops_N##n(const double*, const double*, const double*, const double*, float*); \
+  TileLayout ffma64_layout_N##n();                                                  \
+  size_t ffma64_ops_count_N##n();                                                   \
+  void ffma64_ops_N##n(const double*, const double*, const double*, const double*, double*);
 DG_DECL(1) DG_DECL(2) DG_DECL(3) DG_DECL(4) DG_DECL(5) DG_DECL(6) DG_DECL(7) DG_DECL(8) DG_DECL(9)
 #undef DG_DECL
 
@@ -98,6 +101,25 @@ void ffma_ops_build(int N, const double* Dr, const double* Ds, const double* Dt,
   static void (*const t[9])(const double*, const double*, const double*, const double*, float*) = {
       ffma_ops_N1, ffma_ops_N2, ffma_ops_N3, ffma_ops_N4, ffma_ops_N5,
       ffma_ops_N6, ffma_ops_N7, ffma_ops_N8, ffma_ops_N9};
+  if (N >= 1 && N <= 9) t[N - 1](Dr, Ds, Dt, L, out);
+}
+
+TileLayout ffma_layout_f64(int N) {
+  static TileLayout (*const t[9])() = {ffma64_layout_N1, ffma64_layout_N2, ffma64_layout_N3,
+                                       ffma64_layout_N4, ffma64_layout_N5, ffma64_layout_N6,
+                                       ffma64_layout_N7, ffma64_layout_N8, ffma64_layout_N9};
+  return (N >= 1 && N <= 9) ? t[N - 1]() : TileLayout{};
+}
+size_t ffma64_ops_count(int N) {
+  static size_t (*const t[9])() = {ffma64_ops_count_N1, ffma64_ops_count_N2, ffma64_ops_count_N3,
+                                   ffma64_ops_count_N4, ffma64_ops_count_N5, ffma64_ops_count_N6,
+                                   ffma64_ops_count_N7, ffma64_ops_count_N8, ffma64_ops_count_N9};
+  return (N >= 1 && N <= 9) ? t[N - 1]() : 0;
+}
+void ffma64_ops_build(int N, const double* Dr, const double* Ds, const double* Dt, const double* L, double* out) {
+  static void (*const t[9])(const double*, const double*, const double*, const double*, double*) = {
+      ffma64_ops_N1, ffma64_ops_N2, ffma64_ops_N3, ffma64_ops_N4, ffma64_ops_N5,
+      ffma64_ops_N6, ffma64_ops_N7, ffma64_ops_N8, ffma64_ops_N9};
   if (N >= 1 && N <= 9) t[N - 1](Dr, Ds, Dt, L, out);
 }
 

@@ -26,6 +26,9 @@
 // Roles (as stage_ws.cuh): 1 TMA loader warp, PW flux warps (trace gather with
 // cp.async LA tiles ahead, upwind/PEC flux in place), CW compute warps streaming
 // (tile, row block) tasks.
+//
+// FP64 (DFMA) instance: the same kernel with T = double and RB = 2 rows per thread (one
+// 16-byte operator load still covers a thread's rows): 36 volume accumulators.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -35,11 +38,45 @@
 
 namespace dg {
 
-template <int N>
+// 16-byte vector of T (a thread's RB operator rows in one shared-memory load)
+template <typename T>
+struct V16;
+template <>
+struct V16<float> {
+  using type = float4;
+  static __device__ __forceinline__ void unpack(const float4& v, float (&a)[4]) {
+    a[0] = v.x;
+    a[1] = v.y;
+    a[2] = v.z;
+    a[3] = v.w;
+  }
+};
+template <>
+struct V16<double> {
+  using type = double2;
+  static __device__ __forceinline__ void unpack(const double2& v, double (&a)[2]) {
+    a[0] = v.x;
+    a[1] = v.y;
+  }
+};
+template <typename T>
+__device__ __forceinline__ void cp_async_w(T* dst, const T* src) {
+  if constexpr (sizeof(T) == 8)
+    cp_async8(dst, src);
+  else
+    cp_async4(dst, src);
+}
+
+template <typename T, int N>
 struct FfCfg {
+  static constexpr int W = int(sizeof(T));
+  static constexpr bool F64 = W == 8;
   static constexpr int Np = Order<N>::Np, Nfp = Order<N>::Nfp, NF = Order<N>::NF;
+#ifndef DG_FF_TUNE_W
+#define DG_FF_TUNE_W 4
+#endif
 #ifdef DG_FF_TUNE_N
-  static constexpr bool TUNED = N == DG_FF_TUNE_N;
+  static constexpr bool TUNED = N == DG_FF_TUNE_N && W == DG_FF_TUNE_W;
 #else
   static constexpr bool TUNED = false;
 #endif
@@ -65,30 +102,32 @@ struct FfCfg {
   // (tools/gpu_ffma_tune.sh): smaller tiles win where they cost little row padding, since
   // 20 250 / (E x 148) tiles per CTA sets the tail imbalance and the ring depth
   static constexpr int E = (TUNED && DG_FF_E) ? DG_FF_E
-                           : (N == 1 || N == 3) ? 32 : (N == 2 || N == 4 || N == 6) ? 16 : 8;
-  static_assert(E == 8 || E == 16 || E == 32, "tile = 8, 16 or 32 elements");
+                           : F64 ? (N == 1 ? 32 : N <= 3 ? 16 : N <= 6 ? 8 : 4)
+                                 : (N == 1 || N == 3) ? 32 : (N == 2 || N == 4 || N == 6) ? 16 : 8;
+  static_assert(E == 4 || E == 8 || E == 16 || E == 32, "tile = 4, 8, 16 or 32 elements");
   static constexpr int RG = 32 / E;
-  static constexpr int RB = 4;             // node rows per thread
+  static constexpr int RB = 16 / W;        // node rows per thread (one 16-byte operator load)
   static constexpr int RT = RB * RG;       // node rows per task
   static constexpr int MB = (Np + RT - 1) / RT;  // row blocks = tasks per tile
   static constexpr int MR = MB * RT;       // padded rows of the transposed operators
   static constexpr int LD = Np;            // node stride of a component (no padding)
-  static constexpr int TS = 6 * LD * E;    // floats per tile
+  static constexpr int TS = 6 * LD * E;    // words per tile
   static constexpr int GEOT = E * GEO_W;
   static constexpr int IDXT = E * NF;
-  static constexpr bool OPS_SMEM = (TUNED && DG_FF_OPS >= 0) ? bool(DG_FF_OPS) : N <= 5;
-  static constexpr int A_FLOATS = 3 * Np * MR + NF * MR;
-  static constexpr int A_BYTES = OPS_SMEM ? r16(A_FLOATS * 4) : 0;
+  static constexpr int A_FLOATS = 3 * Np * MR + NF * MR;  // operator words
+  static constexpr bool OPS_SMEM =
+      (TUNED && DG_FF_OPS >= 0) ? bool(DG_FF_OPS) : (F64 ? A_FLOATS * W <= 64 * 1024 : N <= 5);
+  static constexpr int A_BYTES = OPS_SMEM ? r16(A_FLOATS * W) : 0;
   static constexpr int OFF_U = 0;
-  static constexpr int OFF_G = OFF_U + r16(TS * 4);
-  static constexpr int OFF_I = OFF_G + r16(GEOT * 4);
+  static constexpr int OFF_G = OFF_U + r16(TS * W);
+  static constexpr int OFF_I = OFF_G + r16(GEOT * W);
   static constexpr int OFF_F = OFF_I + r16(IDXT * 4);
-  static constexpr int SLOT = OFF_F + r16(6 * NF * E * 4);
+  static constexpr int SLOT = OFF_F + r16(6 * NF * E * W);
   static constexpr int FM_BYTES = r16(NF * 2);
   // residual staging: each compute warp cp.async's its task's residual (6 x RB values per
   // lane) into shared memory at task start, so no registers are held across the contractions
   static constexpr int STG_FLOATS = 6 * RB * 32;
-  static constexpr int STG_BYTES = 8 * STG_FLOATS * 4;  // up to 8 compute warps (CW <= 8)
+  static constexpr int STG_BYTES = 8 * STG_FLOATS * W;  // up to 8 compute warps (CW <= 8)
   static constexpr int FIXED = A_BYTES + FM_BYTES + STG_BYTES + 4 * 8 * 8;
   static constexpr int S_FIT = (227 * 1024 - FIXED) / SLOT;
   static constexpr int S_DEF = S_FIT > 6 ? 6 : S_FIT;
@@ -104,10 +143,11 @@ struct FfCfg {
   // Without it, 12 warps (3 per SMSP) leave 168 registers for the 72-accumulator tile but
   // only 3 flux warps, which cannot keep up at N <= 4 (ncu: compute warps wait on full[s]).
   // measured (profiles/r1_ffma_tune.jsonl): N = 1, 2, 3 gain 11-18 %, N = 4 is even, N >= 5 lose 1-5 %
-  static constexpr bool SPLIT = (TUNED && DG_FF_SPLIT >= 0) ? bool(DG_FF_SPLIT) : N <= 4;
+  // FP64 (RB = 2, 36 accumulators) fits 128 registers: 16 warps without a split.
+  static constexpr bool SPLIT = (TUNED && DG_FF_SPLIT >= 0) ? bool(DG_FF_SPLIT) : !F64 && N <= 4;
   static constexpr int REG_HI = 192, REG_LO = 64;
-  static constexpr int CW = SPLIT ? 8 : (TUNED && DG_FF_CW) ? DG_FF_CW : 8;
-  static constexpr int PW = SPLIT ? 7 : (TUNED && DG_FF_PW) ? DG_FF_PW : 3;
+  static constexpr int CW = SPLIT || F64 ? 8 : (TUNED && DG_FF_CW) ? DG_FF_CW : 8;
+  static constexpr int PW = SPLIT || F64 ? 7 : (TUNED && DG_FF_PW) ? DG_FF_PW : 3;
   static_assert(!SPLIT || (CW % 4 == 0 && (CW + 1 + PW) % 4 == 0 &&
                            (CW * REG_HI + (1 + PW) * REG_LO) * 32 <= 65536), "warpgroup register split");
   static constexpr int NT = 32 * (CW + 1 + PW);
@@ -116,31 +156,33 @@ struct FfCfg {
   static_assert(CW <= 8, "residual staging sized for 8 compute warps");
   static constexpr size_t SMEM_BYTES = size_t(S) * SLOT + A_BYTES + FM_BYTES + STG_BYTES + BAR_BYTES;
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
-  static_assert((TS * 4) % 16 == 0 && (GEOT * 4) % 16 == 0 && (IDXT * 4) % 16 == 0, "16-B bulk copies");
+  static_assert((TS * W) % 16 == 0 && (GEOT * W) % 16 == 0 && (IDXT * 4) % 16 == 0, "16-B bulk copies");
 };
 
-template <int N, bool UPDATE>
-__global__ void __launch_bounds__(FfCfg<N>::NT, 1)
-    dg_stage_ffma(const StageParams<float> p, const float* __restrict__ opsT, int64_t t_begin, int64_t t_count) {
-  using C = FfCfg<N>;
+template <typename T, int N, bool UPDATE>
+__global__ void __launch_bounds__(FfCfg<T, N>::NT, 1)
+    dg_stage_ffma(const StageParams<T> p, const T* __restrict__ opsT, int64_t t_begin, int64_t t_count) {
+  using C = FfCfg<T, N>;
+  using V = typename V16<T>::type;
+  constexpr int W = C::W;
   constexpr int Np = C::Np, Nfp = C::Nfp, NF = C::NF, E = C::E, LD = C::LD, S = C::S, TS = C::TS;
   constexpr int MR = C::MR, RB = C::RB;
   extern __shared__ __align__(128) unsigned char smem_ff[];
   unsigned char* smem = smem_ff;
   pdl_trigger();
-  float* sA = reinterpret_cast<float*>(smem + size_t(S) * C::SLOT);
+  T* sA = reinterpret_cast<T*>(smem + size_t(S) * C::SLOT);
   int16_t* sFm = reinterpret_cast<int16_t*>(smem + size_t(S) * C::SLOT + C::A_BYTES);
-  float* sStg = reinterpret_cast<float*>(smem + size_t(S) * C::SLOT + C::A_BYTES + C::FM_BYTES);
+  T* sStg = reinterpret_cast<T*>(smem + size_t(S) * C::SLOT + C::A_BYTES + C::FM_BYTES);
   uint64_t* bars =
       reinterpret_cast<uint64_t*>(smem + size_t(S) * C::SLOT + C::A_BYTES + C::FM_BYTES + C::STG_BYTES);
   uint64_t* bar_load = bars;
   uint64_t* bar_tr = bars + S;
   uint64_t* bar_full = bars + 2 * S;
   uint64_t* bar_empty = bars + 3 * S;
-  auto sU = [&](int s) { return reinterpret_cast<float*>(smem + size_t(s) * C::SLOT + C::OFF_U); };
-  auto sG = [&](int s) { return reinterpret_cast<float*>(smem + size_t(s) * C::SLOT + C::OFF_G); };
+  auto sU = [&](int s) { return reinterpret_cast<T*>(smem + size_t(s) * C::SLOT + C::OFF_U); };
+  auto sG = [&](int s) { return reinterpret_cast<T*>(smem + size_t(s) * C::SLOT + C::OFF_G); };
   auto sI = [&](int s) { return reinterpret_cast<int32_t*>(smem + size_t(s) * C::SLOT + C::OFF_I); };
-  auto sF = [&](int s) { return reinterpret_cast<float*>(smem + size_t(s) * C::SLOT + C::OFF_F); };
+  auto sF = [&](int s) { return reinterpret_cast<T*>(smem + size_t(s) * C::SLOT + C::OFF_F); };
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool res_in = UPDATE && !p.first_stage;
@@ -163,8 +205,9 @@ __global__ void __launch_bounds__(FfCfg<N>::NT, 1)
   }
   for (int m = tid; m < NF; m += C::NT) sFm[m] = p.fmask[m];
   if constexpr (C::OPS_SMEM) {
-    static_assert(MR % 4 == 0, "16-B operator rows");
-    for (int w = tid; w < C::A_FLOATS / 4; w += C::NT) cp_async16(sA + 4 * w, opsT + 4 * w);
+    constexpr int PER16 = 16 / W;
+    static_assert(MR % PER16 == 0, "16-B operator rows");
+    for (int w = tid; w < C::A_FLOATS / PER16; w += C::NT) cp_async16(sA + PER16 * w, opsT + PER16 * w);
     cp_commit();
     cp_wait<0>();
   }
@@ -182,9 +225,9 @@ __global__ void __launch_bounds__(FfCfg<N>::NT, 1)
         const int s = int(j % S);
         mbar_wait(bar_empty + s, (unsigned(j / S) & 1) ^ 1);
         const int64_t tile = tile_of(j);
-        mbar_arrive_tx(bar_load + s, TS * 4 + C::GEOT * 4 + C::IDXT * 4);
-        bulk_g2s(sU(s), p.u_in + tile * TS, TS * 4, bar_load + s);
-        bulk_g2s(sG(s), p.geo + tile * C::GEOT, C::GEOT * 4, bar_load + s);
+        mbar_arrive_tx(bar_load + s, TS * W + C::GEOT * W + C::IDXT * 4);
+        bulk_g2s(sU(s), p.u_in + tile * TS, TS * W, bar_load + s);
+        bulk_g2s(sG(s), p.geo + tile * C::GEOT, C::GEOT * W, bar_load + s);
         bulk_g2s(sI(s), p.gidx + tile * C::IDXT, C::IDXT * 4, bar_load + s);
       }
     }
@@ -197,14 +240,14 @@ __global__ void __launch_bounds__(FfCfg<N>::NT, 1)
       const int s = int(j % S);
       mbar_wait(bar_load + s, unsigned(j / S) & 1);
       const int32_t* I = sI(s);
-      float* F = sF(s);
+      T* F = sF(s);
       for (int w = ptid; w < E * NF; w += C::PT) {
         const int32_t gi = I[w];
         if (gi >= 0 && !(gi & TileLayout::INTRA_FLAG)) {
           const bool ghost = gi >= p.ghost_base;
-          const float* src = p.u_in + gi;
+          const T* src = p.u_in + gi;
 #pragma unroll
-          for (int c = 0; c < 6; ++c) cp_async4(F + c * NF * E + w, src + (ghost ? c * Nfp : c * LD * E));
+          for (int c = 0; c < 6; ++c) cp_async_w(F + c * NF * E + w, src + (ghost ? c * Nfp : c * LD * E));
         }
       }
       cp_async_mbar_arrive(bar_tr + s);
@@ -215,17 +258,17 @@ __global__ void __launch_bounds__(FfCfg<N>::NT, 1)
     // wall — u- itself with the E jump negated (E+ = -E-, H+ = H-).  Items of elements
     // beyond the launch range are computed too (harmless: the compute warps skip them).
     auto flux = [&](int64_t j) {
-      constexpr int IT = 2;
+      constexpr int IT = 2;  // (FP64: 16 warps x 128 registers also hold two items)
       constexpr int NIT = (E * NF + C::PT - 1) / C::PT;
       const int s = int(j % S);
       mbar_wait(bar_tr + s, unsigned(j / S) & 1);
-      const float* U = sU(s);
-      const float* Gm = sG(s);
+      const T* U = sU(s);
+      const T* Gm = sG(s);
       const int32_t* I = sI(s);
-      float* F = sF(s);
+      T* F = sF(s);
 #pragma unroll 1
       for (int it = 0; it < NIT; it += IT) {
-        float uM[IT][6], uP[IT][6], g[IT][4], sE[IT];
+        T uM[IT][6], uP[IT][6], g[IT][4], sE[IT];
         int wv[IT];
 #pragma unroll
         for (int q = 0; q < IT; ++q) {
@@ -236,12 +279,12 @@ __global__ void __launch_bounds__(FfCfg<N>::NT, 1)
           const int m = w / E, e = w - m * E, f = m / Nfp;
           const int nM = sFm[m];
           const int32_t gi = I[w];
-          const float* pm = U + nM * E + e;
-          const float* pp = pm;
+          const T* pm = U + nM * E + e;
+          const T* pp = pm;
           int cs = LD * E;
-          sE[q] = -1.0f;
+          sE[q] = T(-1);
           if (gi >= 0) {
-            sE[q] = 1.0f;
+            sE[q] = T(1);
             if (gi & TileLayout::INTRA_FLAG) {
               pp = U + (gi & 255) * E + ((gi >> 8) & 255);
             } else {
@@ -254,20 +297,20 @@ __global__ void __launch_bounds__(FfCfg<N>::NT, 1)
             uM[q][c] = pm[c * LD * E];
             uP[q][c] = pp[c * cs];
           }
-          const float* gp = Gm + e * GEO_W + 9 + 4 * f;
+          const T* gp = Gm + e * GEO_W + 9 + 4 * f;
 #pragma unroll
           for (int i = 0; i < 4; ++i) g[q][i] = gp[i];
         }
 #pragma unroll
         for (int q = 0; q < IT; ++q) {
-          float dE[3], dH[3], fl[6];
+          T dE[3], dH[3], fl[6];
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             dE[c] = sE[q] * uP[q][c] - uM[q][c];
             dH[c] = uP[q][c + 3] - uM[q][c + 3];
           }
-          maxwell_flux<float>(g[q][0], g[q][1], g[q][2], p.alpha, dE, dH, fl);
-          const float sc = g[q][3] * 0.5f;
+          maxwell_flux<T>(g[q][0], g[q][1], g[q][2], p.alpha, dE, dH, fl);
+          const T sc = g[q][3] * T(0.5);
           if (wv[q] >= 0) {
 #pragma unroll
             for (int c = 0; c < 6; ++c) F[c * NF * E + wv[q]] = fl[c] * sc;
@@ -301,12 +344,12 @@ __global__ void __launch_bounds__(FfCfg<N>::NT, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_empty + int(jj % S));
     };
-    const float* A = C::OPS_SMEM ? sA : opsT;
-    auto ld4 = [&](int idx) -> float4 {
+    const T* A = C::OPS_SMEM ? sA : opsT;
+    auto ld4 = [&](int idx) -> V {  // RB consecutive operator rows, 16 bytes
       if constexpr (C::OPS_SMEM)
-        return *reinterpret_cast<const float4*>(A + idx);
+        return *reinterpret_cast<const V*>(A + idx);
       else
-        return __ldg(reinterpret_cast<const float4*>(A + idx));
+        return __ldg(reinterpret_cast<const V*>(A + idx));
     };
     for (int64_t q = warp; q < total; q += C::CW) {
       const int64_t j = q / C::MB;
@@ -320,61 +363,55 @@ __global__ void __launch_bounds__(FfCfg<N>::NT, 1)
       const int64_t tile = tile_of(j);
       const int ne = count_of(tile);
       const int row0 = mb * C::RT + rg * RB;
-      const float* U = sU(s) + el;
-      const float* F = sF(s) + el;
+      const T* U = sU(s) + el;
+      const T* F = sF(s) + el;
       const int64_t tb = tile * TS + el;
-      float* stg = sStg + warp * C::STG_FLOATS + lane;  // [c][i][lane]
+      T* stg = sStg + warp * C::STG_FLOATS + lane;  // [c][i][lane]
       if (UPDATE && res_in) {  // residual -> staging (coalesced over elements), consumed by the update
         if (el < ne) {
 #pragma unroll
           for (int c = 0; c < 6; ++c)
 #pragma unroll
             for (int i = 0; i < RB; ++i)
-              if (row0 + i < Np) cp_async4(stg + (c * RB + i) * 32, p.res + tb + int64_t(c * LD + row0 + i) * E);
+              if (row0 + i < Np) cp_async_w(stg + (c * RB + i) * 32, p.res + tb + int64_t(c * LD + row0 + i) * E);
         }
         cp_commit();
       }
-      // ---- a1: [Dr;Ds;Dt] . U, 4 rows x 6 components x 3 operators
-      float acc[3][6][RB];
+      // ---- a1: [Dr;Ds;Dt] . U, RB rows x 6 components x 3 operators
+      T acc[3][6][RB];
 #pragma unroll
       for (int b = 0; b < 3; ++b)
 #pragma unroll
         for (int c = 0; c < 6; ++c)
 #pragma unroll
-          for (int i = 0; i < RB; ++i) acc[b][c][i] = 0.0f;
+          for (int i = 0; i < RB; ++i) acc[b][c][i] = T(0);
 #pragma unroll 5
       for (int k = 0; k < Np; ++k) {
-        float a[3][RB];
+        T a[3][RB];
 #pragma unroll
-        for (int b = 0; b < 3; ++b) {
-          const float4 v = ld4((b * Np + k) * MR + row0);
-          a[b][0] = v.x;
-          a[b][1] = v.y;
-          a[b][2] = v.z;
-          a[b][3] = v.w;
-        }
+        for (int b = 0; b < 3; ++b) V16<T>::unpack(ld4((b * Np + k) * MR + row0), a[b]);
 #pragma unroll
         for (int c = 0; c < 6; ++c) {
-          const float bv = U[(c * LD + k) * E];
+          const T bv = U[(c * LD + k) * E];
 #pragma unroll
           for (int b = 0; b < 3; ++b)
 #pragma unroll
-            for (int i = 0; i < RB; ++i) acc[b][c][i] = fmaf(a[b][i], bv, acc[b][c][i]);
+            for (int i = 0; i < RB; ++i) acc[b][c][i] = fma(a[b][i], bv, acc[b][c][i]);
         }
       }
       // ---- chain rule + curl (thread-local: all components of one element and row)
-      float r[6][RB];
+      T r[6][RB];
       {
-        const float* Gm = sG(s) + el * GEO_W;
-        float gm[9];
+        const T* Gm = sG(s) + el * GEO_W;
+        T gm[9];
 #pragma unroll
         for (int i = 0; i < 9; ++i) gm[i] = Gm[i];
 #pragma unroll
         for (int i = 0; i < RB; ++i) {
-          float dx[6], dy[6], dz[6];
+          T dx[6], dy[6], dz[6];
 #pragma unroll
           for (int c = 0; c < 6; ++c) {
-            const float ur = acc[0][c][i], us = acc[1][c][i], ut = acc[2][c][i];
+            const T ur = acc[0][c][i], us = acc[1][c][i], ut = acc[2][c][i];
             dx[c] = gm[0] * ur + gm[3] * us + gm[6] * ut;
             dy[c] = gm[1] * ur + gm[4] * us + gm[7] * ut;
             dz[c] = gm[2] * ur + gm[5] * us + gm[8] * ut;
@@ -390,13 +427,13 @@ __global__ void __launch_bounds__(FfCfg<N>::NT, 1)
       // ---- a4: r += LIFT . Flux
 #pragma unroll 4
       for (int jn = 0; jn < NF; ++jn) {
-        const float4 v = ld4(3 * Np * MR + jn * MR + row0);
-        const float l[4] = {v.x, v.y, v.z, v.w};
+        T l[RB];
+        V16<T>::unpack(ld4(3 * Np * MR + jn * MR + row0), l);
 #pragma unroll
         for (int c = 0; c < 6; ++c) {
-          const float fv = F[(c * NF + jn) * E];
+          const T fv = F[(c * NF + jn) * E];
 #pragma unroll
-          for (int i = 0; i < RB; ++i) r[c][i] = fmaf(l[i], fv, r[c][i]);
+          for (int i = 0; i < RB; ++i) r[c][i] = fma(l[i], fv, r[c][i]);
         }
       }
       // ---- a5: LSERK update (or RHS store), coalesced over elements
@@ -410,8 +447,8 @@ __global__ void __launch_bounds__(FfCfg<N>::NT, 1)
             if (row < Np) {
               const int64_t idx = tb + int64_t(c * LD + row) * E;
               if (UPDATE) {
-                const float rold = res_in ? stg[(c * RB + i) * 32] : 0.0f;
-                const float rr = p.rk_a * rold + p.dt * r[c][i];
+                const T rold = res_in ? stg[(c * RB + i) * 32] : T(0);
+                const T rr = p.rk_a * rold + p.dt * r[c][i];
                 p.res[idx] = rr;
                 p.u_out[idx] = U[(c * LD + row) * E] + p.rk_b * rr;
               } else {
@@ -425,13 +462,13 @@ __global__ void __launch_bounds__(FfCfg<N>::NT, 1)
   }
 }
 
-template <int N>
-void launch_stage_ffma(const StageParams<float>& p, const float* opsT, int mode, cudaStream_t st) {
-  using C = FfCfg<N>;
+template <typename T, int N>
+void launch_stage_ffma(const StageParams<T>& p, const T* opsT, int mode, cudaStream_t st) {
+  using C = FfCfg<T, N>;
   static int sms = 0;
   if (!sms) {
-    cudaFuncSetAttribute(dg_stage_ffma<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
-    cudaFuncSetAttribute(dg_stage_ffma<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+    cudaFuncSetAttribute(dg_stage_ffma<T, N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+    cudaFuncSetAttribute(dg_stage_ffma<T, N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -441,14 +478,14 @@ void launch_stage_ffma(const StageParams<float>& p, const float* opsT, int mode,
   const int64_t tc = (p.k_begin + p.K + C::E - 1) / C::E - t0;
   const unsigned grid = unsigned(tc < sms ? tc : sms);
   if (mode == 1)
-    launch_pdl(true, dg_stage_ffma<N, true>, grid, C::NT, C::SMEM_BYTES, st, p, opsT, t0, tc);
+    launch_pdl(true, dg_stage_ffma<T, N, true>, grid, C::NT, C::SMEM_BYTES, st, p, opsT, t0, tc);
   else
-    launch_pdl(true, dg_stage_ffma<N, false>, grid, C::NT, C::SMEM_BYTES, st, p, opsT, t0, tc);
+    launch_pdl(true, dg_stage_ffma<T, N, false>, grid, C::NT, C::SMEM_BYTES, st, p, opsT, t0, tc);
 }
 
-template <int N>
+template <typename T, int N>
 TileLayout ffma_layout() {
-  using C = FfCfg<N>;
+  using C = FfCfg<T, N>;
   TileLayout L;
   L.E = C::E;
   L.LD = C::LD;
@@ -459,17 +496,17 @@ TileLayout ffma_layout() {
 
 // host: transposed, row-padded operators A^T[3][Np][MR] (A^T[b][k][m] = D_b[m][k]) and
 // LIFT^T[NF][MR], from row-major FP64 Dr|Ds|Dt ([Np][Np]) and LIFT ([Np][NF]); padding zero
-template <int N>
-void ffma_ops(const double* Dr, const double* Ds, const double* Dt, const double* LIFT, float* out) {
-  using C = FfCfg<N>;
+template <typename T, int N>
+void ffma_ops(const double* Dr, const double* Ds, const double* Dt, const double* LIFT, T* out) {
+  using C = FfCfg<T, N>;
   constexpr int Np = C::Np, NF = C::NF, MR = C::MR;
-  for (int i = 0; i < C::A_FLOATS; ++i) out[i] = 0.0f;
+  for (int i = 0; i < C::A_FLOATS; ++i) out[i] = T(0);
   const double* D[3] = {Dr, Ds, Dt};
   for (int b = 0; b < 3; ++b)
     for (int m = 0; m < Np; ++m)
-      for (int k = 0; k < Np; ++k) out[(size_t(b) * Np + k) * MR + m] = float(D[b][m * Np + k]);
+      for (int k = 0; k < Np; ++k) out[(size_t(b) * Np + k) * MR + m] = T(D[b][m * Np + k]);
   for (int m = 0; m < Np; ++m)
-    for (int jn = 0; jn < NF; ++jn) out[size_t(3) * Np * MR + size_t(jn) * MR + m] = float(LIFT[m * NF + jn]);
+    for (int jn = 0; jn < NF; ++jn) out[size_t(3) * Np * MR + size_t(jn) * MR + m] = T(LIFT[m * NF + jn]);
 }
 
 }  // namespace dg

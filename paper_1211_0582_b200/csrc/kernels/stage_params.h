@@ -126,6 +126,9 @@ TileLayout tc_layout_f32(int N);   // tcgen05 (TC) kernel layout, N <= 4 (E = 0 
 TileLayout ffma_layout_f32(int N); // FFMA kernel layout (perm 3)
 size_t ffma_ops_count(int N);      // floats in its transposed operator buffer
 void ffma_ops_build(int N, const double* Dr, const double* Ds, const double* Dt, const double* LIFT, float* out);
+TileLayout ffma_layout_f64(int N); // FP64 (DFMA) instance of the FFMA kernel
+size_t ffma64_ops_count(int N);
+void ffma64_ops_build(int N, const double* Dr, const double* Ds, const double* Dt, const double* LIFT, double* out);
 size_t tc_ops_count(int N);
 void tc_ops_build(int N, const double* Dr, const double* Ds, const double* Dt, const double* LIFT, float* out);
 StageLauncher<float> stage_launcher_f32(int N);

@@ -65,10 +65,8 @@ def test_argument_errors():
     with pytest.raises(DGError) as e:
         Solver(3, device=-1, variant=7)
     assert e.value.status == dg.DG_ERR_ARG
-    with pytest.raises(DGError) as e:          # FFMA: the FP32 SIMT kernel only
-        Solver(3, precision=8, device=-1, variant=dg.DG_VARIANT_FFMA)
-    assert e.value.status == dg.DG_ERR_ARG
-    Solver(3, precision=4, device=-1, variant=dg.DG_VARIANT_FFMA).close()
+    for prec in (4, 8):                        # FFMA: the register-tiled SIMT kernel, both precisions
+        Solver(3, precision=prec, device=-1, variant=dg.DG_VARIANT_FFMA).close()
 
 
 def test_host_only_solver_refuses_compute():

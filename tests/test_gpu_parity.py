@@ -52,9 +52,10 @@ def setup(key, VX, E, N):
     return _SETUPS[k]
 
 
-# FP64 BASIC, MMA, MMA_WS (DMMA); FP32 BASIC, MMA_WS (3xTF32 HMMA), TC (tcgen05), FFMA (register-tiled SIMT)
-VARIANTS = [(8, 1), (8, 2), (8, 3), (4, 1), (4, 3), (4, 4), (4, 6)]
-VIDS = ["f64-basic", "f64-mma", "f64-ws", "f32-basic", "f32-ws", "f32-tc", "f32-ffma"]
+# FP64 BASIC, MMA, MMA_WS (DMMA), FFMA (register-tiled DFMA); FP32 BASIC, MMA_WS (3xTF32 HMMA),
+# TC (tcgen05), FFMA (register-tiled FFMA)
+VARIANTS = [(8, 1), (8, 2), (8, 3), (8, 6), (4, 1), (4, 3), (4, 4), (4, 6)]
+VIDS = ["f64-basic", "f64-mma", "f64-ws", "f64-ffma", "f32-basic", "f32-ws", "f32-tc", "f32-ffma"]
 
 
 def supported(N, prec, variant):

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import bench  # noqa: E402
 
-CASES = [(8, 1, "f64-basic-dfma"), (8, 2, "f64-mma-dmma"), (8, 3, "f64-ws-dmma"),
+CASES = [(8, 1, "f64-basic-dfma"), (8, 2, "f64-mma-dmma"), (8, 3, "f64-ws-dmma"), (8, 6, "f64-ffma-tiled"),
          (4, 1, "f32-basic-ffma"), (4, 3, "f32-ws-3xtf32"), (4, 4, "f32-tc-tcgen05"),
          (4, 6, "f32-ffma-tiled")]
 
