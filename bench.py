@@ -98,9 +98,9 @@ def ws_kind(N, prec, variant):
         return "tc"
     if variant == 6:
         return "ffma"
-    if (prec == 4 and N in (2, 3, 9)) or (prec == 8 and N == 1):
+    if (prec == 4 and N in (1, 2, 3, 9)) or (prec == 8 and N == 1):
         return "ffma"
-    return "basic" if (prec == 4 and N == 1) else "ws"
+    return "ws"
 
 
 def load_traffic(N, prec, variant, K):

@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(FfCfg<T, N>::NT, 1)
     // =========================== compute warps ===========================
     const int el = lane % E, rg = lane / E;
     const int64_t total = J * C::MB;
-    int64_t released = 0, waited = -1;
+    int64_t released = 0, waited = -1, lwaited = -1;
     auto release = [&](int64_t jj) {
       if (waited < jj) {
         mbar_wait(bar_full + int(jj % S), unsigned(jj / S) & 1);
@@ -356,9 +356,11 @@ __global__ void __launch_bounds__(FfCfg<T, N>::NT, 1)
       const int mb = int(q - j * C::MB);
       while (released < j) release(released++);
       const int s = int(j % S);
-      if (waited < j) {
-        mbar_wait(bar_full + s, unsigned(j / S) & 1);
-        waited = j;
+      // volume needs only the loaded tile (load[s]); the face buffer (full[s]) is waited for
+      // before the lift (see stage_ws.cuh)
+      if (lwaited < j) {
+        if (waited < j) mbar_wait(bar_load + s, unsigned(j / S) & 1);
+        lwaited = j;
       }
       const int64_t tile = tile_of(j);
       const int ne = count_of(tile);
@@ -423,6 +425,10 @@ __global__ void __launch_bounds__(FfCfg<T, N>::NT, 1)
           r[4][i] = -(dz[0] - dx[2]);
           r[5][i] = -(dx[1] - dy[0]);
         }
+      }
+      if (waited < j) {
+        mbar_wait(bar_full + s, unsigned(j / S) & 1);
+        waited = j;
       }
       // ---- a4: r += LIFT . Flux
 #pragma unroll 4

@@ -108,6 +108,10 @@ struct WsCfg {
   static constexpr bool RES_PREFETCH = !RES_SMEM && (N <= 5 || MW + 1 + PW <= 16);
   static constexpr int NT = 32 * (MW + 1 + PW);
   static constexpr int PT = 32 * PW;
+  // MMA warps start the volume contraction once the tile is loaded and wait for the flux
+  // only before the lift; measured (profiles/r1_early_volume.jsonl): N = 5 +4.6 %, N = 4
+  // +1.3 %, N = 3 -4.4 % (kept off there), others within noise
+  static constexpr bool EARLY_VOL = N != 3;
   static constexpr int G = E / 4;
   static constexpr int T = MT * G;  // tasks per tile
   static constexpr int TS = 6 * E * LD;
@@ -504,7 +508,7 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
     // ============================= MMA warps =============================
     const int gid = lane >> 2, tig = lane & 3;
     const int64_t total = JJ * C::T;
-    int64_t released = 0, waited = -1;
+    int64_t released = 0, waited = -1, lwaited = -1;
     auto release = [&](int64_t jj) {  // this warp is done with tile jj (waits for it to exist first)
       if (waited < jj) {
         mbar_wait(bar_full + int(jj % S), unsigned(jj / S) & 1);
@@ -522,15 +526,13 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
       const int task = int(q - j * C::T);
       while (released < j) release(released++);
       const int s = int(j % S);
-      if (waited < j) {
-        long long _tw = clock64();
-        mbar_wait(bar_full + s, unsigned(j / S) & 1);
-#ifdef DG_WS_PROFILE
-        if (lane == 0) atomicAdd(&g_ws_prof[5], (unsigned long long)(clock64() - _tw));
-#else
-        (void)_tw;
-#endif
-        waited = j;
+      // the volume contraction needs only the loaded tile (load[s]); the face buffer
+      // (full[s]) is waited for just before the lift, so the first tile of a stage
+      // overlaps its flux with the volume work.  (load[s] cannot be a phase ahead or
+      // behind: this warp has passed full[] of tile j-S and not released tile j.)
+      if (lwaited < j) {
+        if (waited < j) mbar_wait((C::EARLY_VOL ? bar_load : bar_full) + s, unsigned(j / S) & 1);
+        lwaited = j;
       }
 #ifdef DG_WS_PROFILE
       long long _tc = clock64();
@@ -611,6 +613,16 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
         r[1][1] = -(dy[2] - dz[1]);  // d_t Hx = -(curl E)_x
         r[2][0] = -(dz[0] - dx[2]);  // d_t Hy
         r[2][1] = -(dx[1] - dy[0]);  // d_t Hz
+      }
+      if (waited < j) {
+        long long _tw = clock64();
+        mbar_wait(bar_full + s, unsigned(j / S) & 1);
+#ifdef DG_WS_PROFILE
+        if (lane == 0) atomicAdd(&g_ws_prof[5], (unsigned long long)(clock64() - _tw));
+#else
+        (void)_tw;
+#endif
+        waited = j;
       }
       // lift: r += LIFT . Flux  (two accumulator sets: 6 independent DMMA chains)
       const double* fp = F + (24 * g + gid) * LDF + tig;

@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
     // ============================= MMA warps =============================
     const int gid = lane >> 2, tig = lane & 3;
     const int64_t total = J * C::T;
-    int64_t released = 0, waited = -1;
+    int64_t released = 0, waited = -1, lwaited = -1;
     auto release = [&](int64_t jj) {
       if (waited < jj) {
         mbar_wait(bar_full + int(jj % S), unsigned(jj / S) & 1);
@@ -323,9 +323,11 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
       const int task = int(q - j * C::T);
       while (released < j) release(released++);
       const int s = int(j % S);
-      if (waited < j) {
-        mbar_wait(bar_full + s, unsigned(j / S) & 1);
-        waited = j;
+      // volume needs only the loaded tile (load[s]); the face buffer (full[s]) is waited for
+      // before the lift (see stage_ws.cuh)
+      if (lwaited < j) {
+        if (waited < j) mbar_wait(bar_load + s, unsigned(j / S) & 1);
+        lwaited = j;
       }
       const int64_t tile = tile_of(j);
       const int ne = count_of(tile);
@@ -397,6 +399,10 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
           r[2][2 * h + 0] = -(dz[0] - dx[2]);
           r[2][2 * h + 1] = -(dx[1] - dy[0]);
         }
+      }
+      if (waited < j) {
+        mbar_wait(bar_full + s, unsigned(j / S) & 1);
+        waited = j;
       }
       // lift: r += LIFT . Flux  (3xTF32)
       const float* fp = F + (24 * g + gid) * LDF + tig;
