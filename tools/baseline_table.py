@@ -38,7 +38,9 @@ def main(path):
                    f"{x['gflops'] / 1e3:.2f} | {rr['bound']} | {100 * rr['frac']:.1f}% of {rr['peak']} {rr['unit']} |")
     out.append("")
     out.append("* The state at C2 is L2-resident for small N, and L2 is flushed before every timed step; C4 is the HBM-resident line.")
-    out.append("* FP64 contractions run on DMMA (WS kernel; MMA kernel at N=1); FP32 on 3xTF32 HMMA, except N=1 FP32 (FFMA BASIC).")
+    out.append("* Kernels (AUTO): FP64 on DMMA (WS kernel) except N=1 (register-tiled DFMA, FFMA kernel); FP32 on the "
+               "register-tiled FFMA kernel at N=1, 2, 3, 9 and on 3xTF32 HMMA (WS32 kernel) at N=4..8; the bound column "
+               "follows the kernel (alu = FFMA/DFMA peak, tensor = DMMA or TF32-mma/3 peak).")
     out.append("* Acoustics (NEXT-3) runs on the BASIC kernel.")
     out.append(f"* Raw JSON: `{path}`.")
     print("\n".join(out))
