@@ -94,7 +94,7 @@ typedef enum {
   DG_SYSTEM_ACOUSTICS = 1  /* 4 fields (p, v), rho0 = c = 1: p_t + div v = 0, v_t + grad p = 0;
                               upwind flux (-A_n + alpha |A_n|)[[u]]; rigid walls v.n = 0
                               (mirror p+ = p-, v+ = v- - 2 (n.v-) n); R16/R17.
-                              BASIC kernel only (AUTO selects it; MMA/MMA_WS/TC -> DG_ERR_ARG) */
+                              FFMA (AUTO) and BASIC kernels (MMA/MMA_WS/TC -> DG_ERR_ARG) */
 } dg_system;
 
 typedef struct {

@@ -369,6 +369,8 @@ dg_status upload_setup(dg_solver* s) {
   const bool ff = s->variant == DG_VARIANT_FFMA;  // (AUTO resolved at create)
   if (ff) {
     s->lay = sizeof(T) == 8 ? dg::ffma_layout_f64(s->N) : dg::ffma_layout_f32(s->N);
+    s->lay.nc = s->nc;  // acoustics: 4 fields per element (FfCfg<T, N, NC>::TS)
+    s->lay.TS = int64_t(s->nc) * s->lay.LD * s->lay.E;
   } else if (sizeof(T) == 8 && ws) {
     s->lay = dg::ws_layout_f64(s->N);
   } else if (sizeof(T) == 4 && ws) {
@@ -662,15 +664,17 @@ dg_status dg_create(const dg_config* cfg, dg_solver** out) {
   if (cfg->variant == DG_VARIANT_TC && (cfg->precision != 4 || cfg->order > 4))
     return fail(DG_ERR_ARG, "DG_VARIANT_TC is the FP32 tcgen05 kernel for N <= 4");
   if (cfg->system != DG_SYSTEM_MAXWELL && cfg->system != DG_SYSTEM_ACOUSTICS) return fail(DG_ERR_ARG, "bad system");
-  if (cfg->system == DG_SYSTEM_ACOUSTICS && cfg->variant != DG_VARIANT_AUTO && cfg->variant != DG_VARIANT_BASIC)
-    return fail(DG_ERR_ARG, "DG_SYSTEM_ACOUSTICS runs on the BASIC kernel only");
+  if (cfg->system == DG_SYSTEM_ACOUSTICS && cfg->variant != DG_VARIANT_AUTO && cfg->variant != DG_VARIANT_BASIC &&
+      cfg->variant != DG_VARIANT_FFMA)
+    return fail(DG_ERR_ARG, "DG_SYSTEM_ACOUSTICS runs on the BASIC and FFMA kernels only");
   std::unique_ptr<dg_solver> s(new dg_solver());
   s->cfg = *cfg;
   s->N = cfg->order;
   s->fp64 = cfg->precision == 8;
   s->wsize = s->fp64 ? 8 : 4;
   s->nc = cfg->system == DG_SYSTEM_ACOUSTICS ? 4 : 6;
-  s->variant = cfg->system == DG_SYSTEM_ACOUSTICS ? DG_VARIANT_BASIC
+  // acoustics (NEXT-3): AUTO -> the FFMA kernel (SYS = 1 instance), measured faster than BASIC
+  s->variant = cfg->system == DG_SYSTEM_ACOUSTICS ? (cfg->variant == DG_VARIANT_AUTO ? DG_VARIANT_FFMA : cfg->variant)
                : cfg->variant == DG_VARIANT_AUTO  ? auto_variant(cfg->precision == 8, cfg->order)
                : cfg->variant == DG_VARIANT_FUSED ? DG_VARIANT_MMA_WS  // same kernel and layout
                                                   : cfg->variant;

@@ -67,7 +67,7 @@ __device__ __forceinline__ void cp_async_w(T* dst, const T* src) {
     cp_async4(dst, src);
 }
 
-template <typename T, int N>
+template <typename T, int N, int NC = 6>
 struct FfCfg {
   static constexpr int W = int(sizeof(T));
   static constexpr bool F64 = W == 8;
@@ -111,7 +111,7 @@ struct FfCfg {
   static constexpr int MB = (Np + RT - 1) / RT;  // row blocks = tasks per tile
   static constexpr int MR = MB * RT;       // padded rows of the transposed operators
   static constexpr int LD = Np;            // node stride of a component (no padding)
-  static constexpr int TS = 6 * LD * E;    // words per tile
+  static constexpr int TS = NC * LD * E;   // words per tile (NC fields: 6 Maxwell, 4 acoustics)
   static constexpr int GEOT = E * GEO_W;
   static constexpr int IDXT = E * NF;
   static constexpr int A_FLOATS = 3 * Np * MR + NF * MR;  // operator words
@@ -122,11 +122,11 @@ struct FfCfg {
   static constexpr int OFF_G = OFF_U + r16(TS * W);
   static constexpr int OFF_I = OFF_G + r16(GEOT * W);
   static constexpr int OFF_F = OFF_I + r16(IDXT * 4);
-  static constexpr int SLOT = OFF_F + r16(6 * NF * E * W);
+  static constexpr int SLOT = OFF_F + r16(NC * NF * E * W);
   static constexpr int FM_BYTES = r16(NF * 2);
   // residual staging: each compute warp cp.async's its task's residual (6 x RB values per
   // lane) into shared memory at task start, so no registers are held across the contractions
-  static constexpr int STG_FLOATS = 6 * RB * 32;
+  static constexpr int STG_FLOATS = NC * RB * 32;
   static constexpr int STG_BYTES = 8 * STG_FLOATS * W;  // up to 8 compute warps (CW <= 8)
   static constexpr int FIXED = A_BYTES + FM_BYTES + STG_BYTES + 4 * 8 * 8;
   static constexpr int S_FIT = (227 * 1024 - FIXED) / SLOT;
@@ -159,10 +159,11 @@ struct FfCfg {
   static_assert((TS * W) % 16 == 0 && (GEOT * W) % 16 == 0 && (IDXT * 4) % 16 == 0, "16-B bulk copies");
 };
 
-template <typename T, int N, bool UPDATE>
-__global__ void __launch_bounds__(FfCfg<T, N>::NT, 1)
+template <typename T, int N, bool UPDATE, int SYS>
+__global__ void __launch_bounds__(FfCfg<T, N, System<SYS>::NC>::NT, 1)
     dg_stage_ffma(const StageParams<T> p, const T* __restrict__ opsT, int64_t t_begin, int64_t t_count) {
-  using C = FfCfg<T, N>;
+  constexpr int NC = System<SYS>::NC;
+  using C = FfCfg<T, N, NC>;
   using V = typename V16<T>::type;
   constexpr int W = C::W;
   constexpr int Np = C::Np, Nfp = C::Nfp, NF = C::NF, E = C::E, LD = C::LD, S = C::S, TS = C::TS;
@@ -247,7 +248,7 @@ __global__ void __launch_bounds__(FfCfg<T, N>::NT, 1)
           const bool ghost = gi >= p.ghost_base;
           const T* src = p.u_in + gi;
 #pragma unroll
-          for (int c = 0; c < 6; ++c) cp_async_w(F + c * NF * E + w, src + (ghost ? c * Nfp : c * LD * E));
+          for (int c = 0; c < NC; ++c) cp_async_w(F + c * NF * E + w, src + (ghost ? c * Nfp : c * LD * E));
         }
       }
       cp_async_mbar_arrive(bar_tr + s);
@@ -268,7 +269,7 @@ __global__ void __launch_bounds__(FfCfg<T, N>::NT, 1)
       T* F = sF(s);
 #pragma unroll 1
       for (int it = 0; it < NIT; it += IT) {
-        T uM[IT][6], uP[IT][6], g[IT][4], sE[IT];
+        T uM[IT][NC], uP[IT][NC], g[IT][4], sE[IT];
         int wv[IT];
 #pragma unroll
         for (int q = 0; q < IT; ++q) {
@@ -293,7 +294,7 @@ __global__ void __launch_bounds__(FfCfg<T, N>::NT, 1)
             }
           }
 #pragma unroll
-          for (int c = 0; c < 6; ++c) {
+          for (int c = 0; c < NC; ++c) {
             uM[q][c] = pm[c * LD * E];
             uP[q][c] = pp[c * cs];
           }
@@ -303,17 +304,30 @@ __global__ void __launch_bounds__(FfCfg<T, N>::NT, 1)
         }
 #pragma unroll
         for (int q = 0; q < IT; ++q) {
-          T dE[3], dH[3], fl[6];
+          T fl[NC];
+          if constexpr (SYS == 0) {
+            T dE[3], dH[3];
 #pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            dE[c] = sE[q] * uP[q][c] - uM[q][c];
-            dH[c] = uP[q][c + 3] - uM[q][c + 3];
+            for (int c = 0; c < 3; ++c) {
+              dE[c] = sE[q] * uP[q][c] - uM[q][c];
+              dH[c] = uP[q][c + 3] - uM[q][c + 3];
+            }
+            maxwell_flux<T>(g[q][0], g[q][1], g[q][2], p.alpha, dE, dH, fl);
+          } else {  // acoustics; rigid wall (sE = -1, u+ = u-): p+ = p-, v+ = v- - 2 (n.v-) n
+            const T nx = g[q][0], ny = g[q][1], nz = g[q][2];
+            const T wall = sE[q] < T(0) ? T(1) : T(0);
+            const T ndv = nx * uM[q][1] + ny * uM[q][2] + nz * uM[q][3];
+            const T dp = uP[q][0] - uM[q][0];
+            T dv[3];
+            dv[0] = uP[q][1] - uM[q][1] - wall * T(2) * ndv * nx;
+            dv[1] = uP[q][2] - uM[q][2] - wall * T(2) * ndv * ny;
+            dv[2] = uP[q][3] - uM[q][3] - wall * T(2) * ndv * nz;
+            acoustic_flux<T>(nx, ny, nz, p.alpha, dp, dv, fl);
           }
-          maxwell_flux<T>(g[q][0], g[q][1], g[q][2], p.alpha, dE, dH, fl);
           const T sc = g[q][3] * T(0.5);
           if (wv[q] >= 0) {
 #pragma unroll
-            for (int c = 0; c < 6; ++c) F[c * NF * E + wv[q]] = fl[c] * sc;
+            for (int c = 0; c < NC; ++c) F[c * NF * E + wv[q]] = fl[c] * sc;
           }
         }
       }
@@ -372,7 +386,7 @@ __global__ void __launch_bounds__(FfCfg<T, N>::NT, 1)
       if (UPDATE && res_in) {  // residual -> staging (coalesced over elements), consumed by the update
         if (el < ne) {
 #pragma unroll
-          for (int c = 0; c < 6; ++c)
+          for (int c = 0; c < NC; ++c)
 #pragma unroll
             for (int i = 0; i < RB; ++i)
               if (row0 + i < Np) cp_async_w(stg + (c * RB + i) * 32, p.res + tb + int64_t(c * LD + row0 + i) * E);
@@ -380,11 +394,11 @@ __global__ void __launch_bounds__(FfCfg<T, N>::NT, 1)
         cp_commit();
       }
       // ---- a1: [Dr;Ds;Dt] . U, RB rows x 6 components x 3 operators
-      T acc[3][6][RB];
+      T acc[3][NC][RB];
 #pragma unroll
       for (int b = 0; b < 3; ++b)
 #pragma unroll
-        for (int c = 0; c < 6; ++c)
+        for (int c = 0; c < NC; ++c)
 #pragma unroll
           for (int i = 0; i < RB; ++i) acc[b][c][i] = T(0);
 #pragma unroll 5
@@ -393,7 +407,7 @@ __global__ void __launch_bounds__(FfCfg<T, N>::NT, 1)
 #pragma unroll
         for (int b = 0; b < 3; ++b) V16<T>::unpack(ld4((b * Np + k) * MR + row0), a[b]);
 #pragma unroll
-        for (int c = 0; c < 6; ++c) {
+        for (int c = 0; c < NC; ++c) {
           const T bv = U[(c * LD + k) * E];
 #pragma unroll
           for (int b = 0; b < 3; ++b)
@@ -402,7 +416,7 @@ __global__ void __launch_bounds__(FfCfg<T, N>::NT, 1)
         }
       }
       // ---- chain rule + curl (thread-local: all components of one element and row)
-      T r[6][RB];
+      T r[NC][RB];
       {
         const T* Gm = sG(s) + el * GEO_W;
         T gm[9];
@@ -410,20 +424,27 @@ __global__ void __launch_bounds__(FfCfg<T, N>::NT, 1)
         for (int i = 0; i < 9; ++i) gm[i] = Gm[i];
 #pragma unroll
         for (int i = 0; i < RB; ++i) {
-          T dx[6], dy[6], dz[6];
+          T dx[NC], dy[NC], dz[NC];
 #pragma unroll
-          for (int c = 0; c < 6; ++c) {
+          for (int c = 0; c < NC; ++c) {
             const T ur = acc[0][c][i], us = acc[1][c][i], ut = acc[2][c][i];
             dx[c] = gm[0] * ur + gm[3] * us + gm[6] * ut;
             dy[c] = gm[1] * ur + gm[4] * us + gm[7] * ut;
             dz[c] = gm[2] * ur + gm[5] * us + gm[8] * ut;
           }
-          r[0][i] = dy[5] - dz[4];
-          r[1][i] = dz[3] - dx[5];
-          r[2][i] = dx[4] - dy[3];
-          r[3][i] = -(dy[2] - dz[1]);
-          r[4][i] = -(dz[0] - dx[2]);
-          r[5][i] = -(dx[1] - dy[0]);
+          if constexpr (SYS == 0) {  // d_t E = curl H, d_t H = -curl E
+            r[0][i] = dy[5] - dz[4];
+            r[1][i] = dz[3] - dx[5];
+            r[2][i] = dx[4] - dy[3];
+            r[3][i] = -(dy[2] - dz[1]);
+            r[4][i] = -(dz[0] - dx[2]);
+            r[5][i] = -(dx[1] - dy[0]);
+          } else {  // d_t p = -div v, d_t v = -grad p
+            r[0][i] = -(dx[1] + dy[2] + dz[3]);
+            r[1][i] = -dx[0];
+            r[2][i] = -dy[0];
+            r[3][i] = -dz[0];
+          }
         }
       }
       if (waited < j) {
@@ -436,7 +457,7 @@ __global__ void __launch_bounds__(FfCfg<T, N>::NT, 1)
         T l[RB];
         V16<T>::unpack(ld4(3 * Np * MR + jn * MR + row0), l);
 #pragma unroll
-        for (int c = 0; c < 6; ++c) {
+        for (int c = 0; c < NC; ++c) {
           const T fv = F[(c * NF + jn) * E];
 #pragma unroll
           for (int i = 0; i < RB; ++i) r[c][i] = fma(l[i], fv, r[c][i]);
@@ -446,7 +467,7 @@ __global__ void __launch_bounds__(FfCfg<T, N>::NT, 1)
       if (UPDATE && res_in) cp_wait<0>();
       if (el < ne) {
 #pragma unroll
-        for (int c = 0; c < 6; ++c)
+        for (int c = 0; c < NC; ++c)
 #pragma unroll
           for (int i = 0; i < RB; ++i) {
             const int row = row0 + i;
@@ -468,13 +489,15 @@ __global__ void __launch_bounds__(FfCfg<T, N>::NT, 1)
   }
 }
 
-template <typename T, int N>
-void launch_stage_ffma(const StageParams<T>& p, const T* opsT, int mode, cudaStream_t st) {
-  using C = FfCfg<T, N>;
+template <typename T, int N, int SYS>
+void launch_stage_ffma_sys(const StageParams<T>& p, const T* opsT, int mode, cudaStream_t st) {
+  using C = FfCfg<T, N, System<SYS>::NC>;
   static int sms = 0;
   if (!sms) {
-    cudaFuncSetAttribute(dg_stage_ffma<T, N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
-    cudaFuncSetAttribute(dg_stage_ffma<T, N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+    cudaFuncSetAttribute(dg_stage_ffma<T, N, true, SYS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(C::SMEM_BYTES));
+    cudaFuncSetAttribute(dg_stage_ffma<T, N, false, SYS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(C::SMEM_BYTES));
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -484,9 +507,18 @@ void launch_stage_ffma(const StageParams<T>& p, const T* opsT, int mode, cudaStr
   const int64_t tc = (p.k_begin + p.K + C::E - 1) / C::E - t0;
   const unsigned grid = unsigned(tc < sms ? tc : sms);
   if (mode == 1)
-    launch_pdl(true, dg_stage_ffma<T, N, true>, grid, C::NT, C::SMEM_BYTES, st, p, opsT, t0, tc);
+    launch_pdl(true, dg_stage_ffma<T, N, true, SYS>, grid, C::NT, C::SMEM_BYTES, st, p, opsT, t0, tc);
   else
-    launch_pdl(true, dg_stage_ffma<T, N, false>, grid, C::NT, C::SMEM_BYTES, st, p, opsT, t0, tc);
+    launch_pdl(true, dg_stage_ffma<T, N, false, SYS>, grid, C::NT, C::SMEM_BYTES, st, p, opsT, t0, tc);
+}
+
+// p.system selects the linear system (dg_system): 0 Maxwell, 1 acoustics (NEXT-3)
+template <typename T, int N>
+void launch_stage_ffma(const StageParams<T>& p, const T* opsT, int mode, cudaStream_t st) {
+  if (p.system == 1)
+    launch_stage_ffma_sys<T, N, 1>(p, opsT, mode, st);
+  else
+    launch_stage_ffma_sys<T, N, 0>(p, opsT, mode, st);
 }
 
 template <typename T, int N>

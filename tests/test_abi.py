@@ -52,7 +52,7 @@ def test_argument_errors():
     with pytest.raises(DGError) as e:
         Solver(3, device=-1, system=2)
     assert e.value.status == dg.DG_ERR_ARG
-    for v in (2, 3, 4, 6):                   # acoustics: BASIC kernel only
+    for v in (2, 3, 4):                      # acoustics: BASIC and FFMA kernels only
         with pytest.raises(DGError) as e:
             Solver(3, precision=4, device=-1, variant=v, system=dg.DG_SYSTEM_ACOUSTICS)
         assert e.value.status == dg.DG_ERR_ARG

@@ -378,15 +378,16 @@ from oracle import acoustics as oac  # noqa: E402
 from paper_1211_0582_b200.dg import DG_SYSTEM_ACOUSTICS  # noqa: E402
 
 
+@pytest.mark.parametrize("variant", [1, 6], ids=["basic", "ffma"])
 @pytest.mark.parametrize("prec", [8, 4])
 @pytest.mark.parametrize("N", range(1, 10))
-def test_acoustics_rhs_and_steps(N, prec):
-    # the second linear system through the same BASIC stage kernel (dg_system = 1):
+def test_acoustics_rhs_and_steps(N, prec, variant):
+    # the second linear system through the BASIC and FFMA stage kernels (dg_system = 1; AUTO = FFMA):
     # RHS and 2 LSERK4 steps vs the acoustics oracle on a shuffled/rotated/jittered mesh
     VX, E = mesh(3, 1, 2, 3)
     st = setup("m3", VX, E, N)
     U = di.random_fields(st.K, N, seed=2, nfields=4)
-    s = Solver(N, precision=prec, system=DG_SYSTEM_ACOUSTICS)
+    s = Solver(N, precision=prec, system=DG_SYSTEM_ACOUSTICS, variant=variant)
     s.mesh_upload(VX, E)
     s.fields_upload(U)
     assert relerr(s.rhs(), oac.rhs(st, U)) < TOL_RHS[prec]
