@@ -131,7 +131,9 @@ struct FfCfg {
   static constexpr int FIXED = A_BYTES + FM_BYTES + STG_BYTES + 4 * 8 * 8;
   static constexpr int S_FIT = (227 * 1024 - FIXED) / SLOT;
   static constexpr int S_DEF = S_FIT > 6 ? 6 : S_FIT;
-  static constexpr int S = (TUNED && DG_FF_S) ? DG_FF_S : S_DEF;
+  // FP32 N = 4: a 3-slot ring with look-ahead 1 beats 4 slots / look-ahead 2 (0.307 vs 0.326 ms,
+  // profiles/r1_ffma_tune.jsonl)
+  static constexpr int S = (TUNED && DG_FF_S) ? DG_FF_S : (!F64 && N == 4) ? 3 : S_DEF;
   static_assert(S >= 2, "two ring slots at least");
   static constexpr int LA = (TUNED && DG_FF_LA >= 0) ? DG_FF_LA : S - 2 < 2 ? S - 2 : 2;
   static_assert(LA <= S - 2 || (S == 2 && LA == 0), "look-ahead beyond the ring");
