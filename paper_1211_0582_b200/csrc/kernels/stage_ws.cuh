@@ -111,7 +111,11 @@ struct WsCfg {
   // MMA warps start the volume contraction once the tile is loaded and wait for the flux
   // only before the lift; measured (profiles/r1_early_volume.jsonl): N = 5 +4.6 %, N = 4
   // +1.3 %, N = 3 -4.4 % (kept off there), others within noise
+#ifdef DG_WS_EARLY
+  static constexpr bool EARLY_VOL = TUNED ? bool(DG_WS_EARLY) : N != 3;
+#else
   static constexpr bool EARLY_VOL = N != 3;
+#endif
   static constexpr int G = E / 4;
   static constexpr int T = MT * G;  // tasks per tile
   static constexpr int TS = 6 * E * LD;
