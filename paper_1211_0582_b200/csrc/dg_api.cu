@@ -393,7 +393,7 @@ dg_status upload_setup(dg_solver* s) {
   s->ghost_base = twords;
   s->ghost_words = P.n_ghost_faces * s->nc * Nfp;
   const int64_t uwords = s->ghost_base + s->ghost_words;
-  if (uwords >= (int64_t(1) << (s->lay.perm >= 1 ? 29 : 31)))
+  if (uwords >= (int64_t(1) << 31))
     return fail(DG_ERR_ARG, "local problem too large for 32-bit gather indices on one rank (partition further)");
   const size_t wb = sizeof(T);
   for (int i = 0; i < 2; ++i) {

@@ -125,7 +125,7 @@ void build_gather_index(const RefElem& ref, const MeshData& m, const Partition& 
         int64_t v;
         const int64_t l2 = g >= 0 ? -1 : P.g2l[k2];
         if (L.perm >= 1 && l2 >= 0 && l2 / L.E == l / L.E)
-          v = TileLayout::INTRA_FLAG | ((l2 % L.E) << 8) | ref.Fmask[f2 * Nfp + j];
+          v = TileLayout::intra(int(l2 % L.E), ref.Fmask[f2 * Nfp + j]);
         else if (L.perm == 2)
           v = g >= 0 ? (TileLayout::GHOST_FLAG | (g * L.nc * Nfp + j))
                      : ((P.g2l[k2] << 8) | ref.Fmask[f2 * Nfp + j]);

@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(FfCfg<T, N, System<SYS>::NC>::NT, 1)
       T* F = sF(s);
       for (int w = ptid; w < E * NF; w += C::PT) {
         const int32_t gi = I[w];
-        if (gi >= 0 && !(gi & TileLayout::INTRA_FLAG)) {
+        if (gi >= 0) {  // intra-tile faces (negative codes) need no gather
           const bool ghost = gi >= p.ghost_base;
           const T* src = p.u_in + gi;
 #pragma unroll
@@ -286,14 +286,13 @@ __global__ void __launch_bounds__(FfCfg<T, N, System<SYS>::NC>::NT, 1)
           const T* pp = pm;
           int cs = LD * E;
           sE[q] = T(-1);
-          if (gi >= 0) {
+          if (TileLayout::is_intra(gi)) {
             sE[q] = T(1);
-            if (gi & TileLayout::INTRA_FLAG) {
-              pp = U + (gi & 255) * E + ((gi >> 8) & 255);
-            } else {
-              pp = F + w;
-              cs = NF * E;
-            }
+            pp = U + TileLayout::intra_n(gi) * E + TileLayout::intra_e(gi);
+          } else if (gi >= 0) {
+            sE[q] = T(1);
+            pp = F + w;
+            cs = NF * E;
           }
 #pragma unroll
           for (int c = 0; c < NC; ++c) {

@@ -61,12 +61,17 @@ struct TileLayout {
   DG_HD int64_t ntiles(int64_t K) const { return (K + E - 1) / E; }
   // gather-index encoding: perm 0/1/3 store off(k2, 0, n2) (+ cofs(c) per component);
   // perm 2 stores (k2 << 8) | n2 and the kernel evaluates off() per component.
-  // Ghost records are ghost_base + rec (perm 0/1) or GHOST_FLAG | rec (perm 2).
+  // Ghost records are ghost_base + rec (perm 0/1/3) or GHOST_FLAG | rec (perm 2).
+  // -1 is a PEC wall.  Word offsets therefore reach 2^31 - 1 (17 GB of FP64 state per rank).
   static constexpr int32_t GHOST_FLAG = int32_t(1) << 30;
-  // tiled layouts (perm 1/2): a face whose neighbour sits in the SAME tile is encoded as
-  // INTRA_FLAG | (e2 << 8) | n2 — the kernel reads u+ from the tile already in shared
-  // memory instead of gathering it (the paper's flux-gather granularity).
-  static constexpr int32_t INTRA_FLAG = int32_t(1) << 29;
+  // tiled layouts (perm >= 1): a face whose neighbour sits in the SAME tile is encoded as the
+  // negative code intra(e2, n2) = -2 - ((e2 << 8) | n2) — the kernel reads u+ from the tile
+  // already in shared memory instead of gathering it (the paper's flux-gather granularity,
+  // PAPER.md:720-743).
+  static DG_HD int32_t intra(int e2, int n2) { return -2 - ((e2 << 8) | n2); }
+  static DG_HD bool is_intra(int32_t gi) { return gi < -1; }
+  static DG_HD int intra_e(int32_t gi) { return (-2 - gi) >> 8; }
+  static DG_HD int intra_n(int32_t gi) { return (-2 - gi) & 255; }
 };
 
 template <typename T>

@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
       for (int w = ptid; w < E * NF; w += C::PT) {  // element-fastest: <= 2-way bank conflicts
         const int m = w / E, e = w - m * E;
         const int32_t gi = I[e * NF + m];
-        if (gi >= 0 && !(gi & TileLayout::INTRA_FLAG)) {  // intra-tile faces need no gather
+        if (gi >= 0) {  // intra-tile faces (negative codes) need no gather
           if (gi & TileLayout::GHOST_FLAG) {
             const float* src = p.u_in + p.ghost_base + (gi & ~TileLayout::GHOST_FLAG);
 #pragma unroll
@@ -261,8 +261,8 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
 #pragma unroll
           for (int c = 0; c < 6; ++c) uM[c] = U[cm_off(6 * e + c, nM, KV)];
           const int32_t gi = I[e * NF + m];
-          if (gi >= 0 && (gi & TileLayout::INTRA_FLAG)) {  // neighbour in this tile: u+ from shared memory
-            const int e2 = (gi >> 8) & 255, n2 = gi & 255;
+          if (TileLayout::is_intra(gi)) {  // neighbour in this tile: u+ from shared memory
+            const int e2 = TileLayout::intra_e(gi), n2 = TileLayout::intra_n(gi);
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
               dE[c] = U[cm_off(6 * e2 + c, n2, KV)] - uM[c];

@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
       float* F = sF(s);
       for (int w = ptid; w < E * NF; w += C::PT) {
         const int32_t gi = I[w];
-        if (gi >= 0 && !(gi & TileLayout::INTRA_FLAG)) {  // intra-tile faces need no gather
+        if (gi >= 0) {  // intra-tile faces (negative codes) need no gather
           const int e = w / NF, m = w - e * NF;
           const bool ghost = gi >= p.ghost_base;
           const float* src = p.u_in + gi;
@@ -246,8 +246,8 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
 #pragma unroll
           for (int c = 0; c < 6; ++c) uM[c] = U[(cb + 8 * (c >> 1) + (c & 1)) * LD + nM];
           const int32_t gi = I[w];
-          if (gi >= 0 && (gi & TileLayout::INTRA_FLAG)) {  // neighbour in this tile: u+ from shared memory
-            const int e2 = (gi >> 8) & 255, n2 = gi & 255;
+          if (TileLayout::is_intra(gi)) {  // neighbour in this tile: u+ from shared memory
+            const int e2 = TileLayout::intra_e(gi), n2 = TileLayout::intra_n(gi);
             const int cb2 = 24 * (e2 >> 2) + 2 * (e2 & 3);
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
