@@ -300,6 +300,44 @@ def test_sampled_oracle_at_c4_size():
     s.close()
 
 
+def test_sampled_oracle_beyond_2pow29_words():
+    # maximum-size edge case: one rank whose state exceeds 2^29 words (FP32 N=9, Kuhn n=41,
+    # K=413,526: 5.46e8 words per copy), so the last elements' gather offsets need bits 29/30
+    # of the int32 index (intra-tile faces are negative codes).  Sampled elements, including
+    # the last one, against the oracle on their face-neighbourhood sub-mesh.
+    psutil = pytest.importorskip("psutil")
+    if psutil.virtual_memory().available < 40e9:
+        pytest.skip("needs ~40 GB of host memory for the FP64 host arrays")
+    N, n, prec = 9, 41, 4
+    VX, E = di.kuhn_box(n)
+    K = E.shape[0]
+    assert 6 * di.np_of(N) * K > 2 ** 29
+    s = Solver(N, precision=prec)
+    s.mesh_upload(VX, E)
+    EToE, _, _, _ = s.get_maps()
+    U0 = di.random_fields(K, N, seed=11)
+    s.fields_upload(U0)
+    R = s.rhs()
+    rng = np.random.default_rng(1)
+    samples = np.concatenate([[0, K - 1, K - 2], rng.integers(0, K, 3)])
+    keep, sVX, sE = _submesh(VX, E, EToE, samples, 1)
+    st = oracle.Setup(sVX, sE, N)
+    Rs = oracle.rhs(st, U0[:, keep])
+    pos = np.searchsorted(keep, samples)
+    assert relerr(R[:, samples], Rs[:, pos]) < TOL_RHS[prec]
+    del R
+    dt = di.dt_rule(VX, E, N)
+    s.lserk_step(dt, 1)
+    U1 = s.fields_download()
+    for k in (K - 1, samples[-1]):
+        keep, sVX, sE = _submesh(VX, E, EToE, [k], 6)
+        st = oracle.Setup(sVX, sE, N)
+        Us = oracle.lserk4(st, U0[:, keep], dt, 1)
+        p = np.searchsorted(keep, k)
+        assert relerr(U1[:, k], Us[:, p]) < TOL_STEP[prec]
+    s.close()
+
+
 @pytest.mark.parametrize("prec,variant", VARIANTS, ids=VIDS)
 @pytest.mark.parametrize("P,how", [(2, "slabs"), (3, "random"), (4, "random")])
 def test_partitioned_loopback_bitwise_equal_to_one_gpu(P, how, prec, variant):
