@@ -87,20 +87,8 @@ def load_peaks():
 
 
 def ws_kind(N, prec, variant):
-    """Which kernel the library runs for (N, precision, variant) — mirrors dg_api.cu auto_variant()."""
-    if variant == 1:
-        return "basic"
-    if variant == 2:
-        return "mma" if prec == 8 else "basic"
-    if variant == 3:
-        return "ws"
-    if variant == 4:
-        return "tc"
-    if variant == 6:
-        return "ffma"
-    if (prec == 4 and N in (1, 2, 3, 9)) or (prec == 8 and N == 1):
-        return "ffma"
-    return "ws"
+    """Kernel family of a RESOLVED dg_variant (Solver.kernel_variant(): the library resolves AUTO)."""
+    return {1: "basic", 2: "mma" if prec == 8 else "basic", 3: "ws", 4: "tc", 5: "ws", 6: "ffma"}.get(variant, "ws")
 
 
 def load_traffic(N, prec, variant, K):
@@ -263,6 +251,8 @@ def run_dg(args, N, prec, rank, world, local, dist, stream, flush, nccl_id, peak
            "ms_per_step": round(ms_step, 5), "dof_updates_per_s": dofs / (ms_step * 1e-3),
            "gflops": 5 * K_total * fpe / (ms_step * 1e-3) / 1e9,
            "launches_per_step": s.launches_per_step()}
+    kv = s.kernel_variant()  # the stage kernel actually in use (AUTO resolved by the library)
+    res["kernel"] = ws_kind(N, prec, kv)
     # dominant kernel: the fused stage kernel (5 launches per step, the step's only kernel at 1 GPU)
     kernel_ms = ms_step / 5 if world == 1 else s.time_stage_kernel(10)
     res["stage_kernel_ms"] = round(kernel_ms, 5)
@@ -272,7 +262,7 @@ def run_dg(args, N, prec, rank, world, local, dist, stream, flush, nccl_id, peak
         res["roofline"] = roofline(N, prec, Kl, kernel_ms, peaks, 1, None, fpe,
                                    bytes_per_elem_stage(N, 8 if prec == 8 else 4, 4))
     else:
-        res["roofline"] = roofline(N, prec, Kl, kernel_ms, peaks, args.variant,
+        res["roofline"] = roofline(N, prec, Kl, kernel_ms, peaks, kv,
                                    traffic=load_traffic(N, prec, args.variant, Kl) if world == 1 else None)
     if e2e:
         # end to end through the C ABI with HOST buffers, every step: H2D of the step's
@@ -441,7 +431,7 @@ def main():
                     "config": {"workload": workload, "K_total": head["K_total"], "order": N,
                                "precision": head["precision"], "parallelism": f"mesh z-slabs x{world}, NCCL halo",
                                "l2": "flushed before every timed step (256 MiB write, not timed)",
-                               "variant": args.variant, "kernel": ws_kind(N, prec, args.variant),
+                               "variant": args.variant, "kernel": head["kernel"],
                                "element_order": ("shuffled(seed %d)" % args.shuffle_seed
                                                  if args.shuffle_seed is not None else "natural")
                                                 + (" + Morton reorder" if args.reorder else "")},

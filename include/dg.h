@@ -217,6 +217,11 @@ DG_API dg_status dg_time_stage_kernel(dg_solver* s, int32_t reps, double* ms_per
 /* Number of kernel launches one LSERK4 step enqueues on this rank. */
 DG_API dg_status dg_launches_per_step(dg_solver* s, int32_t* n);
 
+/* The stage kernel this solver runs (dg_variant; DG_VARIANT_AUTO resolved at dg_create to the
+ * measured-best kernel for its precision, order and system; DG_VARIANT_FUSED reported as
+ * itself).  Valid for host-only solvers too.  DG_ERR_ARG on null pointers. */
+DG_API dg_status dg_kernel_variant(dg_solver* s, int32_t* variant);
+
 /* Thread-local description of the last error ("" if none). */
 DG_API const char* dg_last_error(void);
 /* Library version string (build id, ABI version, compiled arch). */

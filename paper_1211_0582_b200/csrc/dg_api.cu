@@ -1037,6 +1037,12 @@ dg_status dg_launches_per_step(dg_solver* s, int32_t* n) {
   return DG_OK;
 }
 
+dg_status dg_kernel_variant(dg_solver* s, int32_t* variant) {
+  if (!s || !variant) return fail(DG_ERR_ARG, "null argument");
+  *variant = s->cfg.variant == DG_VARIANT_FUSED ? int32_t(DG_VARIANT_FUSED) : int32_t(s->variant);
+  return DG_OK;
+}
+
 void dg_destroy(dg_solver* s) {
   if (!s) return;
   if (!s->host_only) {

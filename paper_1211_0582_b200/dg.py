@@ -65,6 +65,7 @@ _SIGS = {
     "dg_get_geometry": (C.c_int, [_P, _D, _D, _D]),
     "dg_time_stage_kernel": (C.c_int, [_P, C.c_int32, _D]),
     "dg_launches_per_step": (C.c_int, [_P, _I32]),
+    "dg_kernel_variant": (C.c_int, [_P, _I32]),
     "dg_last_error": (C.c_char_p, []),
     "dg_version": (C.c_char_p, []),
     "dg_destroy": (None, [_P]),
@@ -233,6 +234,12 @@ class Solver:
         ms = C.c_double()
         check(dg_time_stage_kernel(self.h, int(reps), C.byref(ms)), "dg_time_stage_kernel")
         return ms.value
+
+    def kernel_variant(self):
+        """The stage kernel in use (dg_variant; AUTO resolved by the library)."""
+        v = C.c_int32()
+        check(dg_kernel_variant(self.h, C.byref(v)), "dg_kernel_variant")
+        return v.value
 
     def launches_per_step(self):
         n = C.c_int32()

@@ -201,3 +201,27 @@ def test_morton_reorder_is_local_permutation():
         s.mesh_upload(VX, E)
         ids = s.local_elements()
         assert set(ids.tolist()) == {k for k in range(E.shape[0]) if (k * 2) // E.shape[0] == r}
+
+
+def test_kernel_variant_auto_resolution():
+    # DG_VARIANT_AUTO resolves at dg_create to the measured-best kernel (DESIGN.md §8 NEXT-4 table):
+    # FP64 -> FFMA (DFMA) at N=1, MMA_WS (DMMA) otherwise; FP32 -> FFMA at N=1,2,3,9, MMA_WS (3xTF32)
+    # at N=4..8; acoustics -> FFMA.  Explicit variants are reported as requested.
+    want = {8: {1: 6, **{n: 3 for n in range(2, 10)}},
+            4: {**{n: 6 for n in (1, 2, 3, 9)}, **{n: 3 for n in range(4, 9)}}}
+    for prec, table in want.items():
+        for N, v in table.items():
+            s = Solver(N, precision=prec, device=-1)
+            assert s.kernel_variant() == v, (prec, N)
+            s.close()
+    for prec in (4, 8):
+        s = Solver(4, precision=prec, device=-1, system=dg.DG_SYSTEM_ACOUSTICS)
+        assert s.kernel_variant() == dg.DG_VARIANT_FFMA
+        s.close()
+    for v in (1, 2, 3, 6):
+        s = Solver(3, precision=8, device=-1, variant=v)
+        assert s.kernel_variant() == v
+        s.close()
+    s = Solver(3, precision=8, device=-1, variant=dg.DG_VARIANT_FUSED)
+    assert s.kernel_variant() == dg.DG_VARIANT_FUSED
+    s.close()
