@@ -104,11 +104,21 @@ __device__ __forceinline__ unsigned tf32_rna(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return r;
 }
-// split x into tf32 hi + tf32 lo
+// split x into tf32 hi + lo: hi = x with the 13 low mantissa bits cleared (exactly a TF32
+// value, so the MMA's own operand conversion cannot alter it), lo = x - hi (exact in FP32,
+// |lo| < 2^-10 |x|; the MMA's TF32 conversion of lo costs at most 2^-20 |x|).  Two
+// instructions instead of cvt.rna + FADD + cvt.rna.
+#ifndef DG_W32_RNA_SPLIT
+__device__ __forceinline__ void tf32_split(float x, unsigned& hi, unsigned& lo) {
+  hi = __float_as_uint(x) & 0xffffe000u;
+  lo = __float_as_uint(x - __uint_as_float(hi));
+}
+#else
 __device__ __forceinline__ void tf32_split(float x, unsigned& hi, unsigned& lo) {
   hi = tf32_rna(x);
   lo = tf32_rna(x - __uint_as_float(hi));
 }
+#endif
 __device__ __forceinline__ void hmma_tf32(float (&c)[4], const unsigned (&a)[4], unsigned b0, unsigned b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
