@@ -250,7 +250,11 @@ def run_dg(args, N, prec, rank, world, local, dist, stream, flush, nccl_id, peak
     res = {"N": N, "precision": "f64" if prec == 8 else "f32", "K_total": K_total, "K_local": Kl,
            "ms_per_step": round(ms_step, 5), "dof_updates_per_s": dofs / (ms_step * 1e-3),
            "gflops": 5 * K_total * fpe / (ms_step * 1e-3) / 1e9,
-           "launches_per_step": s.launches_per_step()}
+           "launches_per_step": s.launches_per_step(),
+           # SURVEY §8(d) row fields: per-step spread (this rank), node updates, L2 residency
+           "ms_step_median": round(float(np.median(ms_steps)), 5), "ms_step_min": round(min(ms_steps), 5),
+           "ms_step_max": round(max(ms_steps), 5), "node_updates_per_s": Np * K_total / (ms_step * 1e-3),
+           "l2_resident": bool(3 * nf * Np * Kl * (8 if prec == 8 else 4) < 126e6)}
     kv = s.kernel_variant()  # the stage kernel actually in use (AUTO resolved by the library)
     res["kernel"] = ws_kind(N, prec, kv)
     # dominant kernel: the fused stage kernel (5 launches per step, the step's only kernel at 1 GPU)
