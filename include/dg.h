@@ -68,7 +68,7 @@ typedef enum {
 } dg_status;
 
 typedef enum {
-  DG_VARIANT_AUTO = 0,   /* measured best per (precision, N): MMA_WS, except FP32 N=1,2,3,9 and
+  DG_VARIANT_AUTO = 0,   /* measured best per (precision, N): MMA_WS, except FP32 N=1,2,3,6,9 and
                             FP64 N=1 -> FFMA (tools/variant_sweep.py) */
   DG_VARIANT_BASIC = 1,  /* one fused element-tile kernel per stage, FMA contractions */
   DG_VARIANT_MMA = 2,    /* FP64: DMMA contractions, cp.async-pipelined persistent kernel

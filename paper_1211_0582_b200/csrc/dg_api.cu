@@ -181,10 +181,10 @@ void release_device(dg_solver* s) {
 // DG_VARIANT_AUTO: the measured-best kernel per (precision, order) on the bench
 // config (NEXT-4 sweep, tools/variant_sweep.py, profiles/r1_pdl_sweep.jsonl):
 // FP64 -> FFMA (register-tiled DFMA) at N = 1, MMA_WS (DMMA) otherwise; FP32 -> FFMA
-// (register-tiled SIMT) at N = 1, 2, 3 and 9, MMA_WS (3xTF32 HMMA) at N = 4..8.
+// (register-tiled SIMT) at N = 1, 2, 3, 6 and 9, MMA_WS (3xTF32 HMMA) at N = 4, 5, 7, 8.
 int auto_variant(bool fp64, int N) {
   if (fp64 && N == 1) return DG_VARIANT_FFMA;
-  if (!fp64 && (N <= 3 || N == 9)) return DG_VARIANT_FFMA;
+  if (!fp64 && (N <= 3 || N == 6 || N == 9)) return DG_VARIANT_FFMA;
   return DG_VARIANT_MMA_WS;
 }
 

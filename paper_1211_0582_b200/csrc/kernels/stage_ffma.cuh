@@ -402,7 +402,11 @@ __global__ void __launch_bounds__(FfCfg<T, N, System<SYS>::NC>::NT, 1)
         for (int c = 0; c < NC; ++c)
 #pragma unroll
           for (int i = 0; i < RB; ++i) acc[b][c][i] = T(0);
-#pragma unroll 5
+#ifndef DG_FF_VUNROLL
+#define DG_FF_VUNROLL (C::OPS_SMEM ? 5 : 10)  // operators through L1/L2 (N >= 6): +10..18 %
+#endif
+constexpr int DG_FF_VUNROLL_V = DG_FF_VUNROLL;
+#pragma unroll DG_FF_VUNROLL_V
       for (int k = 0; k < Np; ++k) {
         T a[3][RB];
 #pragma unroll
@@ -453,7 +457,11 @@ __global__ void __launch_bounds__(FfCfg<T, N, System<SYS>::NC>::NT, 1)
         waited = j;
       }
       // ---- a4: r += LIFT . Flux
-#pragma unroll 4
+#ifndef DG_FF_LUNROLL
+#define DG_FF_LUNROLL (C::OPS_SMEM ? 4 : 8)
+#endif
+constexpr int DG_FF_LUNROLL_V = DG_FF_LUNROLL;
+#pragma unroll DG_FF_LUNROLL_V
       for (int jn = 0; jn < NF; ++jn) {
         T l[RB];
         V16<T>::unpack(ld4(3 * Np * MR + jn * MR + row0), l);

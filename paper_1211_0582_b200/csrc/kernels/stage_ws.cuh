@@ -585,7 +585,14 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
         }
       } else {
         const double* ap = opsA + size_t(row) * KV + tig;
-#pragma unroll 4
+        // operators streamed through L1/L2 (N >= 6): deeper unrolling keeps more operator loads in
+        // flight (profiles/r1_unroll_sweep.jsonl: N = 6 +4.5 %, 7 +7 %, 8 +10 %, 9 +4 % over 4/2)
+#ifndef DG_WS_GUNROLL
+        constexpr int GU = (N == 7 || N == 9) ? 16 : (N == 6 || N == 8) ? 12 : 4;
+#else
+        constexpr int GU = DG_WS_GUNROLL;
+#endif
+#pragma unroll GU
         for (int kk = 0; kk < KV; kk += 4) {
           const double ar = __ldg(ap + kk);
           const double as = __ldg(ap + size_t(M8) * KV + kk);
@@ -646,7 +653,12 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
         }
       } else {
         const double* lp = opsA + size_t(3) * M8 * KV + size_t(row) * KL + tig;
-#pragma unroll 2
+#ifndef DG_WS_LUNROLL
+        constexpr int LU = (N == 7 || N == 9) ? 8 : (N == 6 || N == 8) ? 6 : 2;
+#else
+        constexpr int LU = DG_WS_LUNROLL;
+#endif
+#pragma unroll LU
         for (int kk = 0; kk < KL; kk += 8) {
           const double a0 = __ldg(lp + kk);
           const double a1 = (kk + 4 < KL) ? __ldg(lp + kk + 4) : 0.0;

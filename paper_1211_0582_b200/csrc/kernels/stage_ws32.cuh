@@ -363,7 +363,11 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
                              : 0.0f;
       }
       const float* bp = U + (24 * g + gid) * LD + tig;
-#pragma unroll 2
+#ifndef DG_W32_GUNROLL
+#define DG_W32_GUNROLL (C::OPS_SMEM ? 2 : 4)  // operators through L1/L2: more loads in flight
+#endif
+constexpr int DG_W32_GUNROLL_V = DG_W32_GUNROLL;
+#pragma unroll DG_W32_GUNROLL_V
       for (int kk = 0; kk < KV; kk += 8) {
         unsigned bh[3][2], bl[3][2];
 #pragma unroll
@@ -416,7 +420,11 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
       }
       // lift: r += LIFT . Flux  (3xTF32)
       const float* fp = F + (24 * g + gid) * LDF + tig;
-#pragma unroll 2
+#ifndef DG_W32_LUNROLL
+#define DG_W32_LUNROLL (C::OPS_SMEM ? 2 : 4)
+#endif
+constexpr int DG_W32_LUNROLL_V = DG_W32_LUNROLL;
+#pragma unroll DG_W32_LUNROLL_V
       for (int kk = 0; kk < KL; kk += 8) {
         unsigned ah[4], al[4];
         ah[0] = __float_as_uint(ldA(Ahi, l0 + r0 * ldl + kk + tig));

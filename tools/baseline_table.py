@@ -39,7 +39,7 @@ def main(path):
     out.append("")
     out.append("* The state at C2 is L2-resident for small N, and L2 is flushed before every timed step; C4 is the HBM-resident line.")
     out.append("* Kernels (AUTO): FP64 on DMMA (WS kernel) except N=1 (register-tiled DFMA, FFMA kernel); FP32 on the "
-               "register-tiled FFMA kernel at N=1, 2, 3, 9 and on 3xTF32 HMMA (WS32 kernel) at N=4..8; the bound column "
+               "register-tiled FFMA kernel at N=1, 2, 3, 6, 9 and on 3xTF32 HMMA (WS32 kernel) at N=4, 5, 7, 8; the bound column "
                "follows the kernel (alu = FFMA/DFMA peak, tensor = DMMA or TF32-mma/3 peak).")
     out.append("* Acoustics (NEXT-3) runs on the FFMA kernel (SYS = 1 instance, AUTO).")
     out.append(f"* Raw JSON: `{path}`.")
