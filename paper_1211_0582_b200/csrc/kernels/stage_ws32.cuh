@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
       }
       const float* bp = U + (24 * g + gid) * LD + tig;
 #ifndef DG_W32_GUNROLL
-#define DG_W32_GUNROLL (C::OPS_SMEM ? 2 : 4)  // operators through L1/L2: more loads in flight
+#define DG_W32_GUNROLL (N == 8 ? 4 : 8)  // measured, profiles/r1_unroll_sweep.jsonl (2/2 before: N = 4 -3 %, N = 5 -2 %)
 #endif
 constexpr int DG_W32_GUNROLL_V = DG_W32_GUNROLL;
 #pragma unroll DG_W32_GUNROLL_V
@@ -421,7 +421,7 @@ constexpr int DG_W32_GUNROLL_V = DG_W32_GUNROLL;
       // lift: r += LIFT . Flux  (3xTF32)
       const float* fp = F + (24 * g + gid) * LDF + tig;
 #ifndef DG_W32_LUNROLL
-#define DG_W32_LUNROLL (C::OPS_SMEM ? 2 : 4)
+#define DG_W32_LUNROLL (N == 8 ? 4 : 8)
 #endif
 constexpr int DG_W32_LUNROLL_V = DG_W32_LUNROLL;
 #pragma unroll DG_W32_LUNROLL_V
