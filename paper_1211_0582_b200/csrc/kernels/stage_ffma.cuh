@@ -405,8 +405,8 @@ __global__ void __launch_bounds__(FfCfg<T, N, System<SYS>::NC>::NT, 1)
 #ifndef DG_FF_VUNROLL
 #define DG_FF_VUNROLL (C::OPS_SMEM ? 5 : 10)  // operators through L1/L2 (N >= 6): +10..18 %
 #endif
-constexpr int DG_FF_VUNROLL_V = DG_FF_VUNROLL;
-#pragma unroll DG_FF_VUNROLL_V
+      constexpr int kVolUnroll = DG_FF_VUNROLL;
+#pragma unroll kVolUnroll
       for (int k = 0; k < Np; ++k) {
         T a[3][RB];
 #pragma unroll
@@ -460,8 +460,8 @@ constexpr int DG_FF_VUNROLL_V = DG_FF_VUNROLL;
 #ifndef DG_FF_LUNROLL
 #define DG_FF_LUNROLL (C::OPS_SMEM ? 4 : 8)
 #endif
-constexpr int DG_FF_LUNROLL_V = DG_FF_LUNROLL;
-#pragma unroll DG_FF_LUNROLL_V
+      constexpr int kLiftUnroll = DG_FF_LUNROLL;
+#pragma unroll kLiftUnroll
       for (int jn = 0; jn < NF; ++jn) {
         T l[RB];
         V16<T>::unpack(ld4(3 * Np * MR + jn * MR + row0), l);

@@ -366,8 +366,8 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
 #ifndef DG_W32_GUNROLL
 #define DG_W32_GUNROLL (N == 8 ? 4 : 8)  // measured, profiles/r1_unroll_sweep.jsonl (2/2 before: N = 4 -3 %, N = 5 -2 %)
 #endif
-constexpr int DG_W32_GUNROLL_V = DG_W32_GUNROLL;
-#pragma unroll DG_W32_GUNROLL_V
+      constexpr int kVolUnroll = DG_W32_GUNROLL;
+#pragma unroll kVolUnroll
       for (int kk = 0; kk < KV; kk += 8) {
         unsigned bh[3][2], bl[3][2];
 #pragma unroll
@@ -423,8 +423,8 @@ constexpr int DG_W32_GUNROLL_V = DG_W32_GUNROLL;
 #ifndef DG_W32_LUNROLL
 #define DG_W32_LUNROLL (N == 8 ? 4 : 8)
 #endif
-constexpr int DG_W32_LUNROLL_V = DG_W32_LUNROLL;
-#pragma unroll DG_W32_LUNROLL_V
+      constexpr int kLiftUnroll = DG_W32_LUNROLL;
+#pragma unroll kLiftUnroll
       for (int kk = 0; kk < KL; kk += 8) {
         unsigned ah[4], al[4];
         ah[0] = __float_as_uint(ldA(Ahi, l0 + r0 * ldl + kk + tig));
