@@ -573,9 +573,29 @@ dg_status capture_step(dg_solver* s, int parity, double dt) {
   return DG_OK;
 }
 
+// DG_GRAPH=0 (environment): enqueue the five stage launches of each step directly instead of
+// launching the captured graph (A/B measurement of the step boundary, profiles/r1_graph_ab.jsonl).
+static bool graphs_enabled() {
+  static const int v = [] {
+    const char* e = std::getenv("DG_GRAPH");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
 template <typename T>
 dg_status lserk_steps(dg_solver* s, double dt, int nsteps) {
   if (sizeof(T) == 8 && s->fused) return fused_steps(s, dt, nsteps);
+  if (!graphs_enabled()) {
+    for (int n = 0; n < nsteps; ++n) {
+      for (int stage = 0; stage < 5; ++stage) {
+        dg_status st = enqueue_stage<T>(s, stage, dt, s->cur);
+        if (st != DG_OK) return st;
+        s->cur ^= 1;
+      }
+    }
+    return DG_OK;
+  }
   for (int n = 0; n < nsteps; ++n) {
     const int par = s->cur;
     if (!s->graph[par] || s->graph_dt[par] != dt) {
