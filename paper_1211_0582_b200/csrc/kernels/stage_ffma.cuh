@@ -105,7 +105,15 @@ struct FfCfg {
                            : F64 ? (N == 1 ? 32 : N <= 3 ? 16 : N <= 6 ? 8 : 4)
                                  : (N == 1 || N == 3) ? 32 : (N == 2 || N == 4 || N == 6) ? 16 : 8;
   static_assert(E == 4 || E == 8 || E == 16 || E == 32, "tile = 4, 8, 16 or 32 elements");
-  static constexpr int RG = 32 / E;
+#ifndef DG_FF_EPL
+#define DG_FF_EPL 0
+#endif
+  // elements per lane: 2 where the operators stream from L2 (FP32 N >= 6; ncu at N = 7: L1 hit rate 10 %,
+  // 41 % long-scoreboard stalls): each operator load then feeds twice the FFMAs
+  static constexpr int EPL = (TUNED && DG_FF_EPL) ? DG_FF_EPL : 1;
+  static constexpr int EL = E / EPL;       // distinct elements per warp (lanes = EL x RG)
+  static_assert(EL >= 4 && E % EPL == 0, "elements per lane");
+  static constexpr int RG = 32 / EL;
   static constexpr int RB = 16 / W;        // node rows per thread (one 16-byte operator load)
   static constexpr int RT = RB * RG;       // node rows per task
   static constexpr int MB = (Np + RT - 1) / RT;  // row blocks = tasks per tile
@@ -126,7 +134,7 @@ struct FfCfg {
   static constexpr int FM_BYTES = r16(NF * 2);
   // residual staging: each compute warp cp.async's its task's residual (6 x RB values per
   // lane) into shared memory at task start, so no registers are held across the contractions
-  static constexpr int STG_FLOATS = NC * RB * 32;
+  static constexpr int STG_FLOATS = EPL * NC * RB * 32;
   static constexpr int STG_BYTES = 8 * STG_FLOATS * W;  // up to 8 compute warps (CW <= 8)
   static constexpr int FIXED = A_BYTES + FM_BYTES + STG_BYTES + 4 * 8 * 8;
   static constexpr int S_FIT = (227 * 1024 - FIXED) / SLOT;
@@ -146,12 +154,18 @@ struct FfCfg {
   // only 3 flux warps, which cannot keep up at N <= 4 (ncu: compute warps wait on full[s]).
   // measured (profiles/r1_ffma_tune.jsonl): N = 1, 2, 3 gain 11-18 %, N = 4 is even, N >= 5 lose 1-5 %
   // FP64 (RB = 2, 36 accumulators) fits 128 registers: 16 warps without a split.
-  static constexpr bool SPLIT = (TUNED && DG_FF_SPLIT >= 0) ? bool(DG_FF_SPLIT) : !F64 && N <= 4;
-  static constexpr int REG_HI = 192, REG_LO = 64;
+  // EPL = 2 (twice the accumulators): 12 warps, compute warpgroups at 224 registers, loader + 3 flux at 64.
+  static constexpr bool SPLIT = (TUNED && DG_FF_SPLIT >= 0) ? bool(DG_FF_SPLIT) : (!F64 && N <= 4) || EPL == 2;
+  static constexpr int REG_HI = EPL == 2 ? 216 : 192, REG_LO = 64;
   static constexpr int CW = SPLIT || F64 ? 8 : (TUNED && DG_FF_CW) ? DG_FF_CW : 8;
-  static constexpr int PW = SPLIT || F64 ? 7 : (TUNED && DG_FF_PW) ? DG_FF_PW : 3;
+  static constexpr int PW = EPL == 2 ? 3 : SPLIT || F64 ? 7 : (TUNED && DG_FF_PW) ? DG_FF_PW : 3;
+  // setmaxnreg.inc blocks until the CTA's pool has the registers, and the pool is what the launch
+  // allocated: (warps x the launch-bound register count), so the split must fit inside it
+  static constexpr int LAUNCH_REGS = (65536 / (32 * (CW + 1 + PW)) / 8) * 8 > 255 ? 255
+                                     : (65536 / (32 * (CW + 1 + PW)) / 8) * 8;
   static_assert(!SPLIT || (CW % 4 == 0 && (CW + 1 + PW) % 4 == 0 &&
-                           (CW * REG_HI + (1 + PW) * REG_LO) * 32 <= 65536), "warpgroup register split");
+                           CW * REG_HI + (1 + PW) * REG_LO <= (CW + 1 + PW) * LAUNCH_REGS),
+                "warpgroup register split exceeds the launch allocation (setmaxnreg.inc would block)");
   static constexpr int NT = 32 * (CW + 1 + PW);
   static constexpr int PT = 32 * PW;
   static constexpr int BAR_BYTES = 4 * S * 8;
@@ -348,7 +362,8 @@ __global__ void __launch_bounds__(FfCfg<T, N, System<SYS>::NC>::NT, 1)
   } else {
     if constexpr (C::SPLIT) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::REG_HI));
     // =========================== compute warps ===========================
-    const int el = lane % E, rg = lane / E;
+    constexpr int EPL = C::EPL, EL = C::EL;
+    const int el = lane % EL, rg = lane / EL;  // elements el + ep * EL, ep < EPL
     const int64_t total = J * C::MB;
     int64_t released = 0, waited = -1, lwaited = -1;
     auto release = [&](int64_t jj) {
@@ -383,25 +398,31 @@ __global__ void __launch_bounds__(FfCfg<T, N, System<SYS>::NC>::NT, 1)
       const T* U = sU(s) + el;
       const T* F = sF(s) + el;
       const int64_t tb = tile * TS + el;
-      T* stg = sStg + warp * C::STG_FLOATS + lane;  // [c][i][lane]
+      T* stg = sStg + warp * C::STG_FLOATS + lane;  // [ep][c][i][lane]
       if (UPDATE && res_in) {  // residual -> staging (coalesced over elements), consumed by the update
-        if (el < ne) {
+#pragma unroll
+        for (int ep = 0; ep < EPL; ++ep)
+          if (el + ep * EL < ne) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+#pragma unroll
+              for (int i = 0; i < RB; ++i)
+                if (row0 + i < Np)
+                  cp_async_w(stg + ((ep * NC + c) * RB + i) * 32,
+                             p.res + tb + ep * EL + int64_t(c * LD + row0 + i) * E);
+          }
+        cp_commit();
+      }
+      // ---- a1: [Dr;Ds;Dt] . U, RB rows x 6 components x 3 operators, EPL elements
+      T acc[EPL][3][NC][RB];
+#pragma unroll
+      for (int ep = 0; ep < EPL; ++ep)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
 #pragma unroll
           for (int c = 0; c < NC; ++c)
 #pragma unroll
-            for (int i = 0; i < RB; ++i)
-              if (row0 + i < Np) cp_async_w(stg + (c * RB + i) * 32, p.res + tb + int64_t(c * LD + row0 + i) * E);
-        }
-        cp_commit();
-      }
-      // ---- a1: [Dr;Ds;Dt] . U, RB rows x 6 components x 3 operators
-      T acc[3][NC][RB];
-#pragma unroll
-      for (int b = 0; b < 3; ++b)
-#pragma unroll
-        for (int c = 0; c < NC; ++c)
-#pragma unroll
-          for (int i = 0; i < RB; ++i) acc[b][c][i] = T(0);
+            for (int i = 0; i < RB; ++i) acc[ep][b][c][i] = T(0);
 #ifndef DG_FF_VUNROLL
 #define DG_FF_VUNROLL (C::OPS_SMEM ? 5 : 10)  // operators through L1/L2 (N >= 6): +10..18 %
 #endif
@@ -412,18 +433,21 @@ __global__ void __launch_bounds__(FfCfg<T, N, System<SYS>::NC>::NT, 1)
 #pragma unroll
         for (int b = 0; b < 3; ++b) V16<T>::unpack(ld4((b * Np + k) * MR + row0), a[b]);
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          const T bv = U[(c * LD + k) * E];
+        for (int ep = 0; ep < EPL; ++ep)
 #pragma unroll
-          for (int b = 0; b < 3; ++b)
+          for (int c = 0; c < NC; ++c) {
+            const T bv = U[(c * LD + k) * E + ep * EL];
 #pragma unroll
-            for (int i = 0; i < RB; ++i) acc[b][c][i] = fma(a[b][i], bv, acc[b][c][i]);
-        }
+            for (int b = 0; b < 3; ++b)
+#pragma unroll
+              for (int i = 0; i < RB; ++i) acc[ep][b][c][i] = fma(a[b][i], bv, acc[ep][b][c][i]);
+          }
       }
       // ---- chain rule + curl (thread-local: all components of one element and row)
-      T r[NC][RB];
-      {
-        const T* Gm = sG(s) + el * GEO_W;
+      T r[EPL][NC][RB];
+#pragma unroll
+      for (int ep = 0; ep < EPL; ++ep) {
+        const T* Gm = sG(s) + (el + ep * EL) * GEO_W;
         T gm[9];
 #pragma unroll
         for (int i = 0; i < 9; ++i) gm[i] = Gm[i];
@@ -432,23 +456,23 @@ __global__ void __launch_bounds__(FfCfg<T, N, System<SYS>::NC>::NT, 1)
           T dx[NC], dy[NC], dz[NC];
 #pragma unroll
           for (int c = 0; c < NC; ++c) {
-            const T ur = acc[0][c][i], us = acc[1][c][i], ut = acc[2][c][i];
+            const T ur = acc[ep][0][c][i], us = acc[ep][1][c][i], ut = acc[ep][2][c][i];
             dx[c] = gm[0] * ur + gm[3] * us + gm[6] * ut;
             dy[c] = gm[1] * ur + gm[4] * us + gm[7] * ut;
             dz[c] = gm[2] * ur + gm[5] * us + gm[8] * ut;
           }
           if constexpr (SYS == 0) {  // d_t E = curl H, d_t H = -curl E
-            r[0][i] = dy[5] - dz[4];
-            r[1][i] = dz[3] - dx[5];
-            r[2][i] = dx[4] - dy[3];
-            r[3][i] = -(dy[2] - dz[1]);
-            r[4][i] = -(dz[0] - dx[2]);
-            r[5][i] = -(dx[1] - dy[0]);
+            r[ep][0][i] = dy[5] - dz[4];
+            r[ep][1][i] = dz[3] - dx[5];
+            r[ep][2][i] = dx[4] - dy[3];
+            r[ep][3][i] = -(dy[2] - dz[1]);
+            r[ep][4][i] = -(dz[0] - dx[2]);
+            r[ep][5][i] = -(dx[1] - dy[0]);
           } else {  // d_t p = -div v, d_t v = -grad p
-            r[0][i] = -(dx[1] + dy[2] + dz[3]);
-            r[1][i] = -dx[0];
-            r[2][i] = -dy[0];
-            r[3][i] = -dz[0];
+            r[ep][0][i] = -(dx[1] + dy[2] + dz[3]);
+            r[ep][1][i] = -dx[0];
+            r[ep][2][i] = -dy[0];
+            r[ep][3][i] = -dz[0];
           }
         }
       }
@@ -466,32 +490,37 @@ __global__ void __launch_bounds__(FfCfg<T, N, System<SYS>::NC>::NT, 1)
         T l[RB];
         V16<T>::unpack(ld4(3 * Np * MR + jn * MR + row0), l);
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          const T fv = F[(c * NF + jn) * E];
+        for (int ep = 0; ep < EPL; ++ep)
 #pragma unroll
-          for (int i = 0; i < RB; ++i) r[c][i] = fma(l[i], fv, r[c][i]);
-        }
+          for (int c = 0; c < NC; ++c) {
+            const T fv = F[(c * NF + jn) * E + ep * EL];
+#pragma unroll
+            for (int i = 0; i < RB; ++i) r[ep][c][i] = fma(l[i], fv, r[ep][c][i]);
+          }
       }
       // ---- a5: LSERK update (or RHS store), coalesced over elements
       if (UPDATE && res_in) cp_wait<0>();
-      if (el < ne) {
 #pragma unroll
-        for (int c = 0; c < NC; ++c)
+      for (int ep = 0; ep < EPL; ++ep) {
+        if (el + ep * EL < ne) {
 #pragma unroll
-          for (int i = 0; i < RB; ++i) {
-            const int row = row0 + i;
-            if (row < Np) {
-              const int64_t idx = tb + int64_t(c * LD + row) * E;
-              if (UPDATE) {
-                const T rold = res_in ? stg[(c * RB + i) * 32] : T(0);
-                const T rr = p.rk_a * rold + p.dt * r[c][i];
-                p.res[idx] = rr;
-                p.u_out[idx] = U[(c * LD + row) * E] + p.rk_b * rr;
-              } else {
-                p.rhs_out[idx] = r[c][i];
+          for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int i = 0; i < RB; ++i) {
+              const int row = row0 + i;
+              if (row < Np) {
+                const int64_t idx = tb + ep * EL + int64_t(c * LD + row) * E;
+                if (UPDATE) {
+                  const T rold = res_in ? stg[((ep * NC + c) * RB + i) * 32] : T(0);
+                  const T rr = p.rk_a * rold + p.dt * r[ep][c][i];
+                  p.res[idx] = rr;
+                  p.u_out[idx] = U[(c * LD + row) * E + ep * EL] + p.rk_b * rr;
+                } else {
+                  p.rhs_out[idx] = r[ep][c][i];
+                }
               }
             }
-          }
+        }
       }
     }
     while (released < J) release(released++);
