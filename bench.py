@@ -206,6 +206,10 @@ def run_dg(args, N, prec, rank, world, local, dist, stream, flush, nccl_id, peak
     import torch
     from paper_1211_0582_b200.dg import Solver
 
+    if world > 1:
+        # a fresh ncclUniqueId per solver: an id's bootstrap root serves one communicator only
+        nccl_id = nccl_unique_id(rank, dist)
+
     n = args.mesh_n
     VX, E = di.kuhn_box(n, nz=n * world)
     if args.shuffle_seed is not None:
@@ -319,6 +323,28 @@ def run_dg(args, N, prec, rank, world, local, dist, stream, flush, nccl_id, peak
     return res
 
 
+def oracle_rhs_rate(N, n, budget_s=2.0):
+    """Bounded oracle sample for the order sweep: whole RHS evaluations (numpy FP64, C2
+    mesh) for about budget_s; one LSERK4 step = 5 RHS + the stage updates, so
+    DOF-updates/s is quoted as 6 Np K / (5 t_rhs) (an upper bound: the updates are ignored)."""
+    import oracle
+    VX, E = di.kuhn_box(n)
+    st = oracle.Setup(VX, E, N)
+    U = di.random_fields(st.K, N, seed=0)
+    oracle.rhs(st, U)
+    reps = 0
+    t0 = time.perf_counter()
+    while True:
+        oracle.rhs(st, U)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el > budget_s:
+            break
+    t_rhs = el / reps
+    return {"N": N, "value": 6 * di.np_of(N) * st.K / (5 * t_rhs), "unit": "DOF-updates/s",
+            "rhs_s": round(t_rhs, 4), "rhs_evals": reps}
+
+
 def oracle_baseline(N, n, budget_s=20.0, max_steps=None):
     """The CPU oracle as it stands, timed on this host on the C2 mesh (FP64)."""
     import oracle
@@ -361,6 +387,7 @@ def main():
     ap.add_argument("--shuffle-seed", type=int, default=None, help="random element numbering (unstructured-like)")
     ap.add_argument("--reorder", action="store_true", help="library Morton renumbering of the elements")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end measurement")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
     if args.warmup < 3:
@@ -369,7 +396,13 @@ def main():
     rank, world, local, dist = dist_setup()
     N, prec = args.order, args.precision
     Np = di.np_of(N)
-    workload = f"C2: Kuhn box n={args.mesh_n} per GPU (K={6 * args.mesh_n ** 3}/GPU), N={N}, LSERK4, PEC cavity"
+    workload = (f"C2: Kuhn box n={args.mesh_n} per GPU (K={6 * args.mesh_n ** 3}/GPU), N={N}, LSERK4, "
+                f"PEC walls, upwind flux, U(-1,1) fields (seed 0)")
+
+    def config_of(K_total, precision, engine):
+        # identical keys for both arms, so the driver can match the workloads
+        return {"workload": workload, "K_total": K_total, "order": N, "precision": precision,
+                "parallelism": f"mesh z-slabs x{world}, NCCL halo", "engine": engine}
     base = {"metric": "DOF-updates/s per LSERK4 step (and GFLOP/s)", "unit": "DOF-updates/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "data": "synthetic (seeded U(-1,1) fields on a generated Kuhn tet box)"}
@@ -383,8 +416,7 @@ def main():
         out = dict(base)
         out.update({"impl": "reference", "value": cb["value"], "ms_per_step": cb["seconds"] / cb["steps"] * 1e3,
                     "dtype": "f64", "n_gpus": 1,
-                    "config": {"workload": workload, "K": K, "order": N, "precision": "f64",
-                               "engine": "CPU oracle (numpy, host cores)"},
+                    "config": config_of(K, "f64", "CPU oracle (numpy FP64, host cores)"),
                     "cpu_baseline": {"value": cb["value"], "unit": cb["unit"], "cores": cb["cores"],
                                      "kind": "oracle", "sample": cb["sample"]},
                     "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0,
@@ -397,11 +429,11 @@ def main():
     torch.cuda.set_device(local)
     stream = torch.cuda.Stream()
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
-    nccl_id = nccl_unique_id(rank, dist) if world > 1 else None
+    nccl_id = None  # run_dg bootstraps a fresh NCCL id per solver
     peaks = load_peaks()
 
     with ClockSampler(local) as clk:
-        head = run_dg(args, N, prec, rank, world, local, dist, stream, flush, nccl_id, peaks, e2e=True)
+        head = run_dg(args, N, prec, rank, world, local, dist, stream, flush, nccl_id, peaks, e2e=not args.no_e2e)
         sweep = []
         if not args.no_sweep:
             for p in (8, 4):
@@ -432,19 +464,21 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = oracle_baseline(N, args.mesh_n, budget_s=args.cpu_budget)
         cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        if not args.no_sweep:
+            # the oracle across the order sweep: bounded RHS samples (~2 s per order)
+            cpu["sweep"] = [oracle_rhs_rate(n_, args.mesh_n, 2.0) for n_ in range(1, 10)]
 
     if rank == 0:
         out = dict(base)
         out.update({"value": head["dof_updates_per_s"], "ms_per_step": head["ms_per_step"],
                     "gflops": round(head["gflops"], 2), "dtype": "f64" if prec == 8 else "f32",
-                    "config": {"workload": workload, "K_total": head["K_total"], "order": N,
-                               "precision": head["precision"], "parallelism": f"mesh z-slabs x{world}, NCCL halo",
+                    "config": {**config_of(head["K_total"], head["precision"], "libdg (sm_100a)"),
                                "l2": "flushed before every timed step (256 MiB write, not timed)",
                                "variant": args.variant, "kernel": head["kernel"],
                                "element_order": ("shuffled(seed %d)" % args.shuffle_seed
                                                  if args.shuffle_seed is not None else "natural")
                                                 + (" + Morton reorder" if args.reorder else "")},
-                    "roofline": head["roofline"], "e2e": head["e2e"],
+                    "roofline": head["roofline"], "e2e": head.get("e2e"),
                     "gpu_launches": head["launches_per_step"] * args.steps,
                     "stage_kernel_ms": head["stage_kernel_ms"],
                     "clocks": clocks, "cpu_baseline": cpu,

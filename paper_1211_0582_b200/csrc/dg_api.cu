@@ -102,6 +102,8 @@ struct dg_solver {
   double* d_stage64 = nullptr; // [nc][Kl][Np] FP64 host-layout staging
   void* d_geo = nullptr;
   int32_t* d_gidx = nullptr;
+  uint8_t* d_fcode = nullptr;  // TC kernel: compressed face connectivity (d_gidx holds the bases)
+  int16_t* d_ftab = nullptr;   // TC kernel: Fmask + orientation tables
   void* d_ops = nullptr;
   void* d_ops_pad = nullptr;   // FP64 MMA variant operators, zero-padded
   int16_t* d_fmask = nullptr;
@@ -161,6 +163,8 @@ void release_device(dg_solver* s) {
   void* p = s->d_stage64; free_dev(p); s->d_stage64 = nullptr;
   free_dev(s->d_geo);
   p = s->d_gidx; free_dev(p); s->d_gidx = nullptr;
+  p = s->d_fcode; free_dev(p); s->d_fcode = nullptr;
+  p = s->d_ftab; free_dev(p); s->d_ftab = nullptr;
   free_dev(s->d_ops);
   free_dev(s->d_ops_pad);
   p = s->d_fmask; free_dev(p); s->d_fmask = nullptr;
@@ -201,6 +205,8 @@ dg::StageParams<T> base_params(dg_solver* s) {
   dg::StageParams<T> p{};
   p.geo = static_cast<const T*>(s->d_geo);
   p.gidx = s->d_gidx;
+  p.fcode = s->d_fcode;
+  p.ftab = s->d_ftab;
   p.ops = static_cast<const T*>(s->d_ops);
   p.ops_pad = static_cast<const T*>(s->d_ops_pad);
   p.fmask = s->d_fmask;
@@ -377,7 +383,6 @@ dg_status upload_setup(dg_solver* s) {
     s->lay = dg::ws32_layout_f32(s->N);
   } else if (tc) {
     s->lay = dg::tc_layout_f32(s->N);
-    if (Kl >= (int64_t(1) << 22)) return fail(DG_ERR_ARG, "TC variant: more than 2^22 local elements");
   } else {
     s->lay = dg::TileLayout();
     s->lay.nc = s->nc;
@@ -415,7 +420,19 @@ dg_status upload_setup(dg_solver* s) {
   CK(cudaMalloc(&s->d_geo, geo.size() * wb));
   CK(cudaMemcpy(s->d_geo, geo.data(), geo.size() * wb, cudaMemcpyHostToDevice));
   std::vector<int32_t> gidx;
-  dg::build_gather_index(s->ref, m, P, s->lay, s->ghost_base, gidx);
+  if (s->lay.perm == 4) {
+    // TC kernel: per-face (neighbour base, f2*6 + orientation) + smem tables, 20 B per element
+    std::vector<uint8_t> fcode;
+    std::vector<int16_t> ftab;
+    dg::build_face_connectivity(s->ref, m, P, s->lay, gidx, fcode, ftab);
+    if (fcode.empty()) fcode.push_back(0);
+    CK(cudaMalloc((void**)&s->d_fcode, fcode.size()));
+    CK(cudaMemcpy(s->d_fcode, fcode.data(), fcode.size(), cudaMemcpyHostToDevice));
+    CK(cudaMalloc((void**)&s->d_ftab, ftab.size() * sizeof(int16_t)));
+    CK(cudaMemcpy(s->d_ftab, ftab.data(), ftab.size() * sizeof(int16_t), cudaMemcpyHostToDevice));
+  } else {
+    dg::build_gather_index(s->ref, m, P, s->lay, s->ghost_base, gidx);
+  }
   if (gidx.empty()) gidx.push_back(-1);
   CK(cudaMalloc((void**)&s->d_gidx, gidx.size() * sizeof(int32_t)));
   CK(cudaMemcpy(s->d_gidx, gidx.data(), gidx.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
@@ -453,7 +470,7 @@ dg_status upload_setup(dg_solver* s) {
   } else {
     // FP32 3xTF32: hi/lo split operators, zero-padded (stage_ws32.cuh / stage_tc.cuh);
     // FFMA: transposed, row-padded operators (stage_ffma.cuh)
-    const bool tcv = s->lay.perm == 2, ffv = s->lay.perm == 3;
+    const bool tcv = s->lay.perm == 4, ffv = s->lay.perm == 3;
     std::vector<float> pad(tcv ? dg::tc_ops_count(s->N) : ffv ? dg::ffma_ops_count(s->N) : dg::ws32_ops_count(s->N));
     if (ffv)
       dg::ffma_ops_build(s->N, s->ref.Dr.a.data(), s->ref.Ds.a.data(), s->ref.Dt.a.data(), s->ref.LIFT.a.data(),
@@ -681,8 +698,8 @@ dg_status dg_create(const dg_config* cfg, dg_solver** out) {
   if (cfg->variant < 0 || cfg->variant > 6) return fail(DG_ERR_ARG, "bad variant");
   if (cfg->variant == DG_VARIANT_FUSED && (cfg->precision != 8 || cfg->nranks != 1))
     return fail(DG_ERR_ARG, "DG_VARIANT_FUSED is the single-rank FP64 stage-fused WS kernel");
-  if (cfg->variant == DG_VARIANT_TC && (cfg->precision != 4 || cfg->order > 4))
-    return fail(DG_ERR_ARG, "DG_VARIANT_TC is the FP32 tcgen05 kernel for N <= 4");
+  if (cfg->variant == DG_VARIANT_TC && cfg->precision != 4)
+    return fail(DG_ERR_ARG, "DG_VARIANT_TC is the FP32 tcgen05 kernel");
   if (cfg->system != DG_SYSTEM_MAXWELL && cfg->system != DG_SYSTEM_ACOUSTICS) return fail(DG_ERR_ARG, "bad system");
   if (cfg->system == DG_SYSTEM_ACOUSTICS && cfg->variant != DG_VARIANT_AUTO && cfg->variant != DG_VARIANT_BASIC &&
       cfg->variant != DG_VARIANT_FFMA)

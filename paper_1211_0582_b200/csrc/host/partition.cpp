@@ -143,4 +143,37 @@ void build_gather_index(const RefElem& ref, const MeshData& m, const Partition& 
   }
 }
 
+void build_face_connectivity(const RefElem& ref, const MeshData& m, const Partition& P, const TileLayout& L,
+                             std::vector<int32_t>& fbase, std::vector<uint8_t>& fcode, std::vector<int16_t>& ftab) {
+  const int Nfp = ref.Nfp, NF = 4 * Nfp;
+  const int64_t Kpad = L.ntiles(P.K_local) * L.E;
+  fbase.assign(size_t(Kpad) * 4, -1);
+  fcode.assign(size_t(Kpad) * 4, 0);
+  for (int64_t l = 0; l < P.K_local; ++l) {
+    const int64_t k = P.local_ids[l];
+    for (int f = 0; f < 4; ++f) {
+      const int64_t k2 = m.EToE[4 * k + f];
+      const int f2 = m.EToF[4 * k + f];
+      if (k2 == k && f2 == f) continue;  // PEC wall
+      const int code = m.orient[4 * k + f];
+      const int64_t g = P.ghost_of[4 * l + f];
+      if (g >= 0) {
+        fbase[4 * l + f] = int32_t(TileLayout::GHOST_FLAG | (g * L.nc * Nfp));
+        fcode[4 * l + f] = uint8_t(code);
+      } else {
+        fbase[4 * l + f] = int32_t(L.off(P.g2l[k2], 0, 0));
+        fcode[4 * l + f] = uint8_t(f2 * 6 + code);
+      }
+    }
+  }
+  ftab.assign(size_t(NF) + 30 * Nfp, 0);
+  for (int i = 0; i < NF; ++i) ftab[i] = int16_t(ref.Fmask[i]);
+  for (int f2 = 0; f2 < 4; ++f2)
+    for (int o = 0; o < 6; ++o)
+      for (int i = 0; i < Nfp; ++i)
+        ftab[NF + (f2 * 6 + o) * Nfp + i] = int16_t(ref.Fmask[f2 * Nfp + m.fperm[o * Nfp + i]]);
+  for (int o = 0; o < 6; ++o)
+    for (int i = 0; i < Nfp; ++i) ftab[NF + 24 * Nfp + o * Nfp + i] = int16_t(m.fperm[o * Nfp + i]);
+}
+
 }  // namespace dg

@@ -53,4 +53,13 @@ std::string build_partition(const MeshData& m, int rank, int nranks, const int32
 void build_gather_index(const RefElem& ref, const MeshData& m, const Partition& P, const TileLayout& L,
                         int64_t ghost_base, std::vector<int32_t>& gidx);
 
+// Compressed face connectivity of the TC kernel (perm 4), per local (element, face):
+// fbase = L.off(k2_local, 0, 0) (word offset of the neighbour's node 0, component 0),
+// or GHOST_FLAG | g*nc*Nfp (its ghost record), or -1 (PEC); fcode = f2*6 + orientation
+// (ghost: orientation).  ftab = Fmask [4Nfp] | node of neighbour face node i, by
+// (f2*6 + orientation) [24][Nfp] | ghost-record position, by orientation [6][Nfp].
+// Together they rebuild exactly the nodes of build_gather_index (SURVEY §7 hard part 5).
+void build_face_connectivity(const RefElem& ref, const MeshData& m, const Partition& P, const TileLayout& L,
+                             std::vector<int32_t>& fbase, std::vector<uint8_t>& fcode, std::vector<int16_t>& ftab);
+
 }  // namespace dg

@@ -28,6 +28,9 @@ __global__ void k_cm_to_tiles(const S* __restrict__ src, T* __restrict__ dst, in
       const int e3 = int(r - q * L.E), c3 = int(q / L.LD);
       n = int(q - int64_t(c3) * L.LD);
       col = c3 * L.E + e3;
+    } else if (L.perm == 4) {  // n*(nc*E) + col
+      n = int(r / cols);
+      col = int(r - int64_t(n) * cols);
     } else {
       col = int(r / L.LD);
       n = int(r - int64_t(col) * L.LD);

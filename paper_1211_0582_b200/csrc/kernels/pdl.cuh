@@ -48,4 +48,21 @@ inline void launch_pdl(bool use, void (*kernel)(KArgs...), unsigned grid, unsign
   cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
+// One-time launcher setup per device: cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is
+// per device context, so a second solver on another device must run it again.
+struct PerDevice {
+  int sms[64] = {0};
+};
+template <typename F>
+inline int sms_for_device(PerDevice& pd, F&& setup) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& s = pd.sms[dev & 63];
+  if (!s) {
+    setup();
+    cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return s;
+}
+
 }  // namespace dg

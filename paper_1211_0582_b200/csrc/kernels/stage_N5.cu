@@ -1,61 +1,3 @@
-// Stage-kernel instantiations for order N=5 (stage_basic.cuh, stage_mma.cuh, stage_ws.cuh).
-#include "stage_ws32.cuh"
-
-#include "stage_ffma.cuh"
-
-namespace dg {
-
-void launch_stage_f64_N5(const StageParams<double>& p, int mode, int variant, void* st) {
-  if (variant == 1)       // DG_VARIANT_BASIC
-    launch_stage_basic<double, 5>(p, mode, static_cast<cudaStream_t>(st));
-  else if (variant == 6)  // DG_VARIANT_FFMA: register-tiled DFMA WS kernel
-    launch_stage_ffma<double, 5>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
-  else if (variant == 2)  // DG_VARIANT_MMA: DMMA, cp.async-pipelined, element-major layout
-    launch_stage_mma<5>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
-  else                    // AUTO / DG_VARIANT_MMA_WS: DMMA, warp-specialized TMA pipeline, tiled layout
-    launch_stage_ws<5>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
-}
-
-void launch_stage_f32_N5(const StageParams<float>& p, int mode, int variant, void* st) {
-  if (variant == 1 || variant == 2)  // BASIC (MMA has no FP32 kernel of its own)
-    launch_stage_basic<float, 5>(p, mode, static_cast<cudaStream_t>(st));
-  else if (variant == 6)             // FFMA: register-tiled FFMA WS kernel
-    launch_stage_ffma<float, 5>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
-  else                               // AUTO / MMA_WS: 3xTF32 tensor-core WS kernel
-    launch_stage_ws32<5>(p, p.ops_pad, mode, static_cast<cudaStream_t>(st));
-}
-
-TileLayout ffma_layout_N5() { return ffma_layout<float, 5>(); }
-size_t ffma_ops_count_N5() { return FfCfg<float, 5>::A_FLOATS; }
-void ffma_ops_N5(const double* Dr, const double* Ds, const double* Dt, const double* L, float* out) {
-  ffma_ops<float, 5>(Dr, Ds, Dt, L, out);
-}
-TileLayout ffma64_layout_N5() { return ffma_layout<double, 5>(); }
-size_t ffma64_ops_count_N5() { return FfCfg<double, 5>::A_FLOATS; }
-void ffma64_ops_N5(const double* Dr, const double* Ds, const double* Dt, const double* L, double* out) {
-  ffma_ops<double, 5>(Dr, Ds, Dt, L, out);
-}
-TileLayout ws32_layout_N5() { return ws32_layout<5>(); }
-TileLayout tc_layout_N5() { return TileLayout{}; }  // TC covers N <= 4
-size_t tc_ops_count_N5() { return 0; }
-void tc_ops_N5(const double*, const double*, const double*, const double*, float*) {}
-size_t ws32_ops_count_N5() { return 2 * Ws32Cfg<5>::OPS_ONE; }
-void ws32_ops_N5(const double* Dr, const double* Ds, const double* Dt, const double* L, float* out) {
-  ws32_ops<5>(Dr, Ds, Dt, L, out);
-}
-
-TileLayout ws_layout_N5() { return ws_layout<5>(); }
-bool launch_fused_f64_N5(const StageParams<double>& p, const FusedParams<double>& fp, void* st) {
-  return launch_stage_ws_fused<5>(p, p.ops_pad, fp, static_cast<cudaStream_t>(st));
-}
-
-#ifdef DG_WS_PROFILE
-void ws_prof_N5(unsigned long long* out, int reset) {
-  if (reset)
-    ws_prof_reset();
-  else
-    ws_prof_read(out);
-}
-#endif
-
-}  // namespace dg
+// Stage kernels for order N=5 (all variants; see stage_inst.cuh).
+#define DG_N 5
+#include "stage_inst.cuh"

@@ -111,6 +111,7 @@ struct FfCfg {
   // elements per lane: 2 where the operators stream from L2 (FP32 N >= 6; ncu at N = 7: L1 hit rate 10 %,
   // 41 % long-scoreboard stalls): each operator load then feeds twice the FFMAs
   static constexpr int EPL = (TUNED && DG_FF_EPL) ? DG_FF_EPL : 1;
+  static_assert(!F64 || EPL == 1, "EPL = 2 is an FP32-only tuning option (FP64 would not fit 216 registers)");
   static constexpr int EL = E / EPL;       // distinct elements per warp (lanes = EL x RG)
   static_assert(EL >= 4 && E % EPL == 0, "elements per lane");
   static constexpr int RG = 32 / EL;
@@ -530,16 +531,13 @@ __global__ void __launch_bounds__(FfCfg<T, N, System<SYS>::NC>::NT, 1)
 template <typename T, int N, int SYS>
 void launch_stage_ffma_sys(const StageParams<T>& p, const T* opsT, int mode, cudaStream_t st) {
   using C = FfCfg<T, N, System<SYS>::NC>;
-  static int sms = 0;
-  if (!sms) {
-    cudaFuncSetAttribute(dg_stage_ffma<T, N, true, SYS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(C::SMEM_BYTES));
-    cudaFuncSetAttribute(dg_stage_ffma<T, N, false, SYS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(C::SMEM_BYTES));
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  static PerDevice pd;
+  const int sms = sms_for_device(pd, [] {
+      cudaFuncSetAttribute(dg_stage_ffma<T, N, true, SYS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(C::SMEM_BYTES));
+      cudaFuncSetAttribute(dg_stage_ffma<T, N, false, SYS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(C::SMEM_BYTES));
+  });
   if (p.K <= 0) return;
   const int64_t t0 = p.k_begin / C::E;
   const int64_t tc = (p.k_begin + p.K + C::E - 1) / C::E - t0;

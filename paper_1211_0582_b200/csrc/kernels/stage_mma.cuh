@@ -395,16 +395,16 @@ __global__ void __launch_bounds__(MmaCfg<N>::NT)
 template <int N>
 void launch_stage_mma(const StageParams<double>& p, const double* opsA, int mode, cudaStream_t st) {
   using C = MmaCfg<N>;
-  static int grid_max = 0;
-  if (!grid_max) {
+  static PerDevice pd;
+  static int blocks[64] = {0};  // resident CTAs per SM, per device (set with the smem attribute)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int sms = sms_for_device(pd, [&] {
     cudaFuncSetAttribute(dg_stage_mma<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
     cudaFuncSetAttribute(dg_stage_mma<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
-    int dev = 0, sms = 148, per = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, dg_stage_mma<N, true>, C::NT, C::SMEM_BYTES);
-    grid_max = sms * (per > 0 ? per : 1);
-  }
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks[dev & 63], dg_stage_mma<N, true>, C::NT, C::SMEM_BYTES);
+  });
+  const int grid_max = sms * (blocks[dev & 63] > 0 ? blocks[dev & 63] : 1);
   if (p.K <= 0) return;
   const int64_t ntiles = (p.K + C::E - 1) / C::E;
   const unsigned grid = unsigned(ntiles < grid_max ? ntiles : grid_max);

@@ -9,6 +9,10 @@
 //   gidx        int32 [Kl][4*Nfp]: offset of the exterior trace u+ of face node m
 //               (component 0); component stride Np for element nodes, Nfp for ghost
 //               traces (offset >= ghost_base); -1 on a PEC boundary face
+//               TC kernel (perm 4): compressed per face instead, int32 [Kl][4] word offset
+//               of the neighbour's (node 0, component 0) or GHOST_FLAG | record offset or
+//               -1 (PEC), plus uint8 fcode [Kl][4] = f2*6 + orientation code; the face-node
+//               tables ftab rebuild the node (SURVEY §7 hard part 5)
 //   geo         [Kl][GEO_W]: rx ry rz sx sy sz tx ty tz, then 4 x (nx ny nz Fscale)
 //   ops         Dr | Ds | Dt ([Np][Np] each, row-major) | LIFT ([Np][4Nfp])
 //   fmask       int16 [4*Nfp]
@@ -39,6 +43,10 @@ constexpr int GEO_W = 26;  // 25 used (rx..tz, 4 x (n, Fscale)); padded to 16 B 
 //                    ((col/8)*(LD/4) + n/4)*32 + (col%8)*4 + n%4.
 // FFMA kernel:       perm = 3: elements fastest, (c*LD + n)*E + e (col = c*E + e), so a
 //                    warp's lanes (consecutive elements) read and write consecutive words.
+// TC kernel:         perm = 4: node-major tiles, n*(nc*E) + nc*e + c (col = nc*e + c): one
+//                    row of the tcgen05 accumulator per (element, component), so the
+//                    epilogue's lanes (consecutive rows) touch consecutive words, and a
+//                    node octet of a tile is one contiguous bulk copy.
 // Padding (rows n >= Np, absent elements) is zero in every layout.
 struct TileLayout {
   int nc = 6;  // fields per element (6 Maxwell; 4 acoustics, perm 0 only)
@@ -51,10 +59,13 @@ struct TileLayout {
   }
   DG_HD int coff(int c) const { return perm == 1 ? 8 * (c >> 1) + (c & 1) : c; }  // perm 0/1: col(e,c) - col(e,0)
   // perm 0/1/3: word offset of component c relative to component 0 of the same (element, node)
-  DG_HD int64_t cofs(int c) const { return perm == 3 ? int64_t(c) * LD * E : int64_t(coff(c)) * LD; }
+  DG_HD int64_t cofs(int c) const {
+    return perm == 3 ? int64_t(c) * LD * E : perm == 4 ? int64_t(c) : int64_t(coff(c)) * LD;
+  }
   DG_HD int64_t inner(int cl, int n) const {  // word offset of (column, node) inside a tile
     return perm == 2   ? int64_t(((cl >> 3) * (LD >> 2) + (n >> 2)) * 32 + (cl & 7) * 4 + (n & 3))
            : perm == 3 ? (int64_t(cl / E) * LD + n) * E + cl % E
+           : perm == 4 ? int64_t(n) * (nc * E) + cl
                        : int64_t(cl) * LD + n;
   }
   DG_HD int64_t off(int64_t k, int c, int n) const { return (k / E) * TS + inner(col(int(k % E), c), n); }
@@ -81,7 +92,9 @@ struct StageParams {
   T* res;              // LSERK residual (in place)
   T* rhs_out;          // RHS mode: d_t u in device layout
   const T* geo;
-  const int32_t* gidx;
+  const int32_t* gidx;  // TC kernel (perm 4): per (element, face) neighbour base instead (below)
+  const uint8_t* fcode;  // TC kernel: per (element, face) f2*6 + orientation (ghost: orientation)
+  const int16_t* ftab;   // TC kernel: Fmask [4Nfp] | neighbour node [24][Nfp] | ghost position [6][Nfp]
   const T* ops;
   const T* ops_pad;    // MMA variant: Dr|Ds|Dt as [3][M8][KV] + LIFT [M8][4Nfp], zero-padded
   const int16_t* fmask;

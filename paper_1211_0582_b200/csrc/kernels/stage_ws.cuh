@@ -708,15 +708,12 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
 template <int N>
 void launch_stage_ws(const StageParams<double>& p, const double* opsA, int mode, cudaStream_t st) {
   using C = WsCfg<N>;
-  static int sms = 0;
-  if (!sms) {
-    cudaFuncSetAttribute(dg_stage_ws<N, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
-    cudaFuncSetAttribute(dg_stage_ws<N, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
-    cudaFuncSetAttribute(dg_stage_ws<N, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  static PerDevice pd;
+  const int sms = sms_for_device(pd, [] {
+      cudaFuncSetAttribute(dg_stage_ws<N, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+      cudaFuncSetAttribute(dg_stage_ws<N, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+      cudaFuncSetAttribute(dg_stage_ws<N, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+  });
   if (p.K <= 0) return;
   // element range [k_begin, k_begin+K) must start on a tile boundary
   const int64_t t0 = p.k_begin / C::E;
@@ -736,13 +733,10 @@ template <int N>
 bool launch_stage_ws_fused(const StageParams<double>& p, const double* opsA, const FusedParams<double>& fp,
                            cudaStream_t st) {
   using C = WsCfg<N>;
-  static int sms = 0;
-  if (!sms) {
-    cudaFuncSetAttribute(dg_stage_ws<N, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  static PerDevice pd;
+  const int sms = sms_for_device(pd, [] {
+      cudaFuncSetAttribute(dg_stage_ws<N, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+  });
   if (p.K <= 0 || fp.nst <= 0) return true;
   const int64_t tc = (p.K + C::E - 1) / C::E;
   const unsigned grid = unsigned(tc < sms ? tc : sms);

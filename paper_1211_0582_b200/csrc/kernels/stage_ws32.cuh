@@ -483,14 +483,11 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
 template <int N>
 void launch_stage_ws32(const StageParams<float>& p, const float* opsA, int mode, cudaStream_t st) {
   using C = Ws32Cfg<N>;
-  static int sms = 0;
-  if (!sms) {
-    cudaFuncSetAttribute(dg_stage_ws32<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
-    cudaFuncSetAttribute(dg_stage_ws32<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  static PerDevice pd;
+  const int sms = sms_for_device(pd, [] {
+      cudaFuncSetAttribute(dg_stage_ws32<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+      cudaFuncSetAttribute(dg_stage_ws32<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+  });
   if (p.K <= 0) return;
   const int64_t t0 = p.k_begin / C::E;
   const int64_t tc = (p.k_begin + p.K + C::E - 1) / C::E - t0;

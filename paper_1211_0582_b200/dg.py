@@ -181,7 +181,10 @@ class Solver:
         check(dg_fields_upload_device(self.h, C.c_void_p(t.data_ptr())), "dg_fields_upload_device")
 
     def fields_download(self, out=None):
-        out = np.empty((self.nfields, self.K_local, self.Np)) if out is None else out
+        if out is None:
+            out = np.empty((self.nfields, self.K_local, self.Np))
+        assert out.dtype == np.float64 and out.flags.c_contiguous
+        assert out.shape == (self.nfields, self.K_local, self.Np), out.shape
         check(dg_fields_download(self.h, _ptr(out, _D)), "dg_fields_download")
         return out
 

@@ -59,8 +59,7 @@ VIDS = ["f64-basic", "f64-mma", "f64-ws", "f64-ffma", "f32-basic", "f32-ws", "f3
 
 
 def supported(N, prec, variant):
-    if variant == 4 and N > 4:
-        pytest.skip("the tcgen05 TC kernel covers N <= 4")
+    pass  # every variant covers N = 1..9
 
 
 @pytest.mark.parametrize("prec,variant", VARIANTS, ids=VIDS)

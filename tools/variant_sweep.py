@@ -3,7 +3,7 @@
 K=20250), the B200 analogue of the paper's tuning study (fig:tuning-study,
 PAPER.md:1151-1167).  One JSON line per (precision, variant, N): ms per LSERK4 step,
 roofline fraction.  Kernels: FP64 BASIC (DFMA), MMA (DMMA, cp.async), MMA_WS (DMMA,
-TMA warp-specialized); FP32 BASIC (FFMA), MMA_WS (3xTF32 HMMA), TC (tcgen05, N<=4),
+TMA warp-specialized); FP32 BASIC (FFMA), MMA_WS (3xTF32 HMMA), TC (tcgen05 3xTF32),
 FFMA (register-tiled FFMA in the WS pipeline).
 
 Usage: python tools/variant_sweep.py [--orders 1,2,...] [--steps 10]
@@ -41,8 +41,6 @@ def main():
         if a.cases and name not in a.cases.split(","):
             continue
         for N in [int(x) for x in a.orders.split(",")]:
-            if var == 4 and N > 4:
-                continue
             args.variant = var
             r = bench.run_dg(args, N, prec, 0, 1, 0, None, stream, flush, None, peaks)
             print(json.dumps({"lib": tag, "case": name, "N": N, "ms_per_step": r["ms_per_step"],
