@@ -102,8 +102,7 @@ struct dg_solver {
   double* d_stage64 = nullptr; // [nc][Kl][Np] FP64 host-layout staging
   void* d_geo = nullptr;
   int32_t* d_gidx = nullptr;
-  uint8_t* d_fcode = nullptr;  // TC kernel: compressed face connectivity (d_gidx holds the bases)
-  int16_t* d_ftab = nullptr;   // TC kernel: Fmask + orientation tables
+  int16_t* d_ftab = nullptr;   // TC kernel: Fmask + orientation tables (d_gidx holds the per-face connectivity)
   void* d_ops = nullptr;
   void* d_ops_pad = nullptr;   // FP64 MMA variant operators, zero-padded
   int16_t* d_fmask = nullptr;
@@ -163,7 +162,6 @@ void release_device(dg_solver* s) {
   void* p = s->d_stage64; free_dev(p); s->d_stage64 = nullptr;
   free_dev(s->d_geo);
   p = s->d_gidx; free_dev(p); s->d_gidx = nullptr;
-  p = s->d_fcode; free_dev(p); s->d_fcode = nullptr;
   p = s->d_ftab; free_dev(p); s->d_ftab = nullptr;
   free_dev(s->d_ops);
   free_dev(s->d_ops_pad);
@@ -205,7 +203,6 @@ dg::StageParams<T> base_params(dg_solver* s) {
   dg::StageParams<T> p{};
   p.geo = static_cast<const T*>(s->d_geo);
   p.gidx = s->d_gidx;
-  p.fcode = s->d_fcode;
   p.ftab = s->d_ftab;
   p.ops = static_cast<const T*>(s->d_ops);
   p.ops_pad = static_cast<const T*>(s->d_ops_pad);
@@ -410,24 +407,38 @@ dg_status upload_setup(dg_solver* s) {
   CK(cudaMalloc(&s->d_scratch, std::max<int64_t>(twords, 1) * wb));
   CK(cudaMemsetAsync(s->d_scratch, 0, std::max<int64_t>(twords, 1) * wb, s->stream));
   CK(cudaMalloc((void**)&s->d_stage64, std::max<int64_t>(s->nc * Kl * Np, 1) * sizeof(double)));
-  // geometry [Kpad][GEO_W] (padding elements zero)
-  std::vector<T> geo(size_t(std::max<int64_t>(Kpad, 1)) * dg::GEO_W, T(0));
+  // geometry [Kpad][GEO_W] (padding elements zero); TC kernel (perm 4): per tile [E][GEO_W]
+  // padded to TC_GEOT words, so one tile's record is one 16-B aligned bulk copy
+  const bool tcl = s->lay.perm == 4;
+  const int64_t gstride = tcl ? dg::TC_GEOT : s->lay.E * dg::GEO_W;
+  std::vector<T> geo(size_t(std::max<int64_t>(s->ntiles * gstride, 1)), T(0));
   for (int64_t l = 0; l < Kl; ++l) {
     const int64_t k = P.local_ids[l];
-    for (int i = 0; i < 9; ++i) geo[l * dg::GEO_W + i] = T(m.rst_x[9 * k + i]);
-    for (int i = 0; i < 16; ++i) geo[l * dg::GEO_W + 9 + i] = T(m.nrm[16 * k + i]);
+    const int64_t g0 = (l / s->lay.E) * gstride + (l % s->lay.E) * dg::GEO_W;
+    for (int i = 0; i < 9; ++i) geo[g0 + i] = T(m.rst_x[9 * k + i]);
+    for (int i = 0; i < 16; ++i) geo[g0 + 9 + i] = T(m.nrm[16 * k + i]);
   }
   CK(cudaMalloc(&s->d_geo, geo.size() * wb));
   CK(cudaMemcpy(s->d_geo, geo.data(), geo.size() * wb, cudaMemcpyHostToDevice));
   std::vector<int32_t> gidx;
-  if (s->lay.perm == 4) {
-    // TC kernel: per-face (neighbour base, f2*6 + orientation) + smem tables, 20 B per element
+  if (tcl) {
+    // TC kernel: per-face (neighbour base, f2*6 + orientation) + smem tables, 20 B per element,
+    // packed per tile as [E][4] bases | [E] x 4 codes (u8) | pad to TC_CONNT words
+    std::vector<int32_t> fbase;
     std::vector<uint8_t> fcode;
     std::vector<int16_t> ftab;
-    dg::build_face_connectivity(s->ref, m, P, s->lay, gidx, fcode, ftab);
-    if (fcode.empty()) fcode.push_back(0);
-    CK(cudaMalloc((void**)&s->d_fcode, fcode.size()));
-    CK(cudaMemcpy(s->d_fcode, fcode.data(), fcode.size(), cudaMemcpyHostToDevice));
+    dg::build_face_connectivity(s->ref, m, P, s->lay, fbase, fcode, ftab);
+    const int E = s->lay.E;
+    gidx.assign(size_t(s->ntiles) * dg::TC_CONNT, 0);
+    for (int64_t t = 0; t < s->ntiles; ++t)
+      for (int e = 0; e < E; ++e) {
+        uint32_t codes = 0;
+        for (int f = 0; f < 4; ++f) {
+          gidx[t * dg::TC_CONNT + 4 * e + f] = fbase[(t * E + e) * 4 + f];
+          codes |= uint32_t(fcode[(t * E + e) * 4 + f]) << (8 * f);
+        }
+        gidx[t * dg::TC_CONNT + 4 * E + e] = int32_t(codes);
+      }
     CK(cudaMalloc((void**)&s->d_ftab, ftab.size() * sizeof(int16_t)));
     CK(cudaMemcpy(s->d_ftab, ftab.data(), ftab.size() * sizeof(int16_t), cudaMemcpyHostToDevice));
   } else {

@@ -66,10 +66,13 @@ bool DG_FN(launch_fused_f64)(const StageParams<double>& p, const FusedParams<dou
 
 #ifdef DG_WS_PROFILE
 void DG_FN(ws_prof)(unsigned long long* out, int reset) {
-  if (reset)
+  if (reset) {
     ws_prof_reset();
-  else
+    tc_prof_reset();
+  } else {
     ws_prof_read(out);
+    tc_prof_read(out + 16);  // TC-kernel counters follow the WS ones
+  }
 }
 #endif
 

@@ -9,10 +9,11 @@
 //   gidx        int32 [Kl][4*Nfp]: offset of the exterior trace u+ of face node m
 //               (component 0); component stride Np for element nodes, Nfp for ghost
 //               traces (offset >= ghost_base); -1 on a PEC boundary face
-//               TC kernel (perm 4): compressed per face instead, int32 [Kl][4] word offset
-//               of the neighbour's (node 0, component 0) or GHOST_FLAG | record offset or
-//               -1 (PEC), plus uint8 fcode [Kl][4] = f2*6 + orientation code; the face-node
-//               tables ftab rebuild the node (SURVEY §7 hard part 5)
+//               TC kernel (perm 4): compressed per face instead, per tile [TC_CONNT] int32:
+//               [E][4] word offset of the neighbour's (node 0, component 0), or GHOST_FLAG |
+//               record offset, or -1 (PEC); then [E] x 4 packed u8 codes f2*6 + orientation
+//               (ghost: orientation); the face-node tables ftab rebuild the node (SURVEY §7
+//               hard part 5).  geo is per tile [E][GEO_W] padded to TC_GEOT.
 //   geo         [Kl][GEO_W]: rx ry rz sx sy sz tx ty tz, then 4 x (nx ny nz Fscale)
 //   ops         Dr | Ds | Dt ([Np][Np] each, row-major) | LIFT ([Np][4Nfp])
 //   fmask       int16 [4*Nfp]
@@ -30,6 +31,8 @@
 namespace dg {
 
 constexpr int GEO_W = 26;  // 25 used (rx..tz, 4 x (n, Fscale)); padded to 16 B for bulk copies
+constexpr int TC_GEOT = 548;   // TC kernel: geometry words per tile (21 x 26, padded to 16 B)
+constexpr int TC_CONNT = 128;  // TC kernel: connectivity words per tile
 
 // Field layout in device memory: element k, component c, node n lives at
 //   (k / E) * TS + col(k % E, c) * LD + n.
@@ -92,9 +95,8 @@ struct StageParams {
   T* res;              // LSERK residual (in place)
   T* rhs_out;          // RHS mode: d_t u in device layout
   const T* geo;
-  const int32_t* gidx;  // TC kernel (perm 4): per (element, face) neighbour base instead (below)
-  const uint8_t* fcode;  // TC kernel: per (element, face) f2*6 + orientation (ghost: orientation)
-  const int16_t* ftab;   // TC kernel: Fmask [4Nfp] | neighbour node [24][Nfp] | ghost position [6][Nfp]
+  const int32_t* gidx;  // TC kernel (perm 4): per-tile face connectivity [tile][TC_CONNT] instead (above)
+  const int16_t* ftab;  // TC kernel: Fmask [4Nfp] | neighbour node [24][Nfp] | ghost position [6][Nfp]
   const T* ops;
   const T* ops_pad;    // MMA variant: Dr|Ds|Dt as [3][M8][KV] + LIFT [M8][4Nfp], zero-padded
   const int16_t* fmask;

@@ -60,32 +60,53 @@ struct TcCfg {
   static constexpr int NFQ = (NF + 7) / 8;          // flux chunks
   static constexpr int NQ = NV + NFQ;
   static constexpr int TS = (ROWS * Np + 7) / 8 * 8;  // floats per tile (node-major)
+  static constexpr int GEOT = TC_GEOT;              // floats per tile of geometry (21 x 26, padded to 16 B)
+  static constexpr int CONNT = TC_CONNT;            // int32 per tile: fbase [21][4] | fcode [21] (4 x u8) | pad
+  static_assert(E * GEO_W <= GEOT && 5 * E <= CONNT, "per-tile records");
   static constexpr int SLABF = 1024;                // floats per slab slot (8 x 126 used)
   static constexpr int OPC = 2 * 8 * NP16;          // floats per operator chunk (hi | lo)
-  static constexpr int ACH = 2 * 128 * 8;           // floats per generated chunk (hi | lo)
-  static constexpr bool OP_RES = N <= 4;            // operators resident in shared memory
-  static constexpr int RB = OP_RES ? NQ : 4;
-  static constexpr int RS = 4;
-  static constexpr int RV = 8, RF = 6;
-  static constexpr int PW = 6;                      // flux warps (>= 168 items per chunk)
+  static constexpr int ITEMS = 8 * E;               // flux items (element, face-node slot) per chunk
+  static constexpr int PW = 6;                      // flux warps: one item per thread and chunk
+  static constexpr int FTH = 32 * PW;
+  static constexpr int LT = 4;                      // per-thread cp.async trace pipeline depth (chunks)
+  static constexpr int TRC = FTH * 12;              // floats per trace-staging chunk: [6 pairs][FTH][2]
+  static constexpr int LF = 6;                      // flux staging ring (chunks) [128 rows][8]
+  static constexpr int FSC = 128 * 8;
+  static constexpr int RS = 4, RM = 4;
+  static constexpr int WB = 3;                      // operand chunks per writer batch (one wait::st)
+  static constexpr int WUNR = NQ <= 36 ? (NQ + WB - 1) / WB : 1;
+  // generated operand G in TENSOR memory (kind::tf32 A operand: lane = row, one column per k):
+  // ring slots of 16 columns (8 G | 8 G_lo) after the two accumulators
+  static constexpr int A0 = 2 * NP16;
+  static constexpr int RA = (512 - A0) / 16 < 12 ? (512 - A0) / 16 : 12;
+  static constexpr int al1k(int b) { return (b + 1023) / 1024 * 1024; }
+  static constexpr int NTAB = NF + 24 * Nfp + 6 * Nfp + 8 * NFQ;  // int16: Fmask | node | ghost | chunk-slot tables
+  static constexpr int FIXED = RS * SLABF * 4 + RM * 2816 + LT * TRC * 4 + LF * FSC * 4 +
+                               (NTAB * 2 + 15) / 16 * 16 + 1024;
+  static constexpr bool OP_RES = FIXED + al1k(NQ * OPC * 4) <= 226 * 1024;  // operators resident in smem
+  static constexpr int RB_MAX = (226 * 1024 - FIXED) / (OPC * 4);
+  static constexpr int RB = OP_RES ? NQ : (RB_MAX < 12 ? RB_MAX : 12);
   // 16 warps: 4 per SMSP, so every thread can have 128 registers
   static constexpr int W_LD = 4, W_MMA = 5, W_VG0 = 6, W_FG0 = 10;
   static constexpr int NW = W_FG0 + PW;
   static constexpr int NT = 32 * NW;
-  static constexpr int TMEM_COLS = 2 * NP16 <= 32 ? 32 : 2 * NP16 <= 64 ? 64 : 2 * NP16 <= 128 ? 128
-                                   : 2 * NP16 <= 256 ? 256 : 512;
-  static constexpr int NTAB = NF + 24 * Nfp + 6 * Nfp;  // int16: Fmask | node table | ghost table
-  static constexpr int al1k(int b) { return (b + 1023) / 1024 * 1024; }
+  static constexpr int TMEM_COLS = 512;
   static constexpr int OFF_B = 0;
-  static constexpr int OFF_AV = OFF_B + al1k(RB * OPC * 4);
-  static constexpr int OFF_AF = OFF_AV + RV * ACH * 4;
-  static constexpr int OFF_S = OFF_AF + RF * ACH * 4;
-  static constexpr int OFF_T = OFF_S + RS * SLABF * 4;
+  static constexpr int OFF_S = OFF_B + al1k(RB * OPC * 4);
+  static constexpr int OFF_M = OFF_S + RS * SLABF * 4;   // meta ring: [RM][geo GEOT floats | conn CONNT ints]
+  static constexpr int OFF_TR = OFF_M + RM * 2816;      // trace staging ring [LT][TRC]
+  static constexpr int OFF_FS = OFF_TR + LT * TRC * 4;  // flux staging ring [LF][FSC]
+  static constexpr int OFF_T = OFF_FS + LF * FSC * 4;
   static constexpr int OFF_BAR = OFF_T + (NTAB * 2 + 15) / 16 * 16;
-  static constexpr int NBAR = 2 * RB + 2 * RV + 2 * RF + 2 * RS + 4;
+  static constexpr int NBAR = 2 * RB + 2 * RA + 2 * LF + 2 * RS + 2 * RM + 4;
   static constexpr size_t SMEM_BYTES = OFF_BAR + NBAR * 8 + 16;
+  static_assert(RA >= 4, "TMEM operand ring depth");
+  static_assert(Nfp <= 64 && Np <= 256, "chunk-slot table packing");
+  static_assert(RB >= 3, "operator ring depth");
+  static_assert(GEOT * 4 + CONNT * 4 <= 2816, "meta slot");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
-  static_assert(PW * 32 >= 8 * E, "one flux item per thread and chunk");
+  static_assert(FTH >= ITEMS, "one flux item per thread and chunk");
+  static_assert(ITEMS <= 2 * 32 * PW, "at most two flux items per thread and chunk");
   static constexpr size_t OPS_FLOATS = size_t(NQ) * OPC;
 };
 
@@ -105,50 +126,100 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
       "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
+__device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+}
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
+}
+// mbarrier wait with a suspend-time hint: a waiting warp sleeps until the phase completes
+// instead of spinning try_wait and stealing issue slots from the producer warps
+__device__ __forceinline__ void tc_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
 }
 __device__ __forceinline__ float tf32_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 // word offset of (row, kk) inside an 8-k chunk of the canonical K-major layout
 __host__ __device__ constexpr int tc_cm(int r, int kk) { return ((r >> 3) * 2 + (kk >> 2)) * 32 + (r & 7) * 4 + (kk & 3); }
 
+#ifdef DG_WS_PROFILE
+// per-role cycle counters (lane 0 of each warp, summed over CTAs; tools/tc_profile.py):
+// 0 epi wait acc_full | 1 epi work | 2 VG wait slab | 3 VG wait A slot | 4 VG work | 5 FG wait A slot |
+// 6 FG work (loads + flux) | 7 MMA wait V chunk | 8 MMA wait F chunk | 9 MMA wait operator chunk |
+// 10 MMA issue | 11 slab loader wait | 12 tiles (epilogue warp 0) | 13 CTA cycles (epilogue warp 0)
+__device__ unsigned long long g_tc_prof[16];
+#define TC_T(v) long long v = clock64()
+#define TC_A(i, t0) \
+  do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_tc_prof[i], (unsigned long long)(clock64() - (t0))); } while (0)
+inline void tc_prof_read(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_tc_prof, sizeof(g_tc_prof)); }
+inline void tc_prof_reset() {
+  static unsigned long long z[16] = {0};
+  cudaMemcpyToSymbol(g_tc_prof, z, sizeof(z));
+}
+#else
+#define TC_T(v) \
+  do {          \
+  } while (0)
+#define TC_A(i, t0) \
+  do {              \
+  } while (0)
+#endif
+
 template <int N, bool UPDATE>
 __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
-    dg_stage_tc(const StageParams<float> p, const float* __restrict__ ops, int64_t t_begin, int64_t t_count) {
+    dg_stage_tc(const StageParams<float> p, const float* __restrict__ ops, int t_begin64, int t_count64) {
+  // per-CTA counters and word offsets fit 32 bits (dg_mesh_upload bounds a rank's state below 2^31 words)
+  const int t_begin = int(t_begin64), t_count = int(t_count64);
   using C = TcCfg<N>;
   constexpr int Np = C::Np, Nfp = C::Nfp, NF = C::NF, E = C::E, ROWS = C::ROWS, NP16 = C::NP16;
   constexpr int NO = C::NO, NV = C::NV, NFQ = C::NFQ, NQ = C::NQ, TS = C::TS;
-  constexpr int RB = C::RB, RS = C::RS, RV = C::RV, RF = C::RF;
+  constexpr int RB = C::RB, RS = C::RS, RA = C::RA, LF = C::LF, RM = C::RM, LT = C::LT, ITEMS = C::ITEMS;
   extern __shared__ __align__(1024) unsigned char smem_tc[];
   unsigned char* smem = smem_tc;
   pdl_trigger();
   float* sB = reinterpret_cast<float*>(smem + C::OFF_B);
-  float* sAV = reinterpret_cast<float*>(smem + C::OFF_AV);
-  float* sAF = reinterpret_cast<float*>(smem + C::OFF_AF);
+  float* sFS = reinterpret_cast<float*>(smem + C::OFF_FS);
   float* sS = reinterpret_cast<float*>(smem + C::OFF_S);
+  float* sTR = reinterpret_cast<float*>(smem + C::OFF_TR);
   int16_t* sFm = reinterpret_cast<int16_t*>(smem + C::OFF_T);
   const int16_t* sNP = sFm + NF;          // [24][Nfp] neighbour node of face node i, by f2*6 + orientation
   const int16_t* sGP = sNP + 24 * Nfp;    // [6][Nfp]  ghost record position, by orientation
+  auto sGeo = [&](int j) { return reinterpret_cast<const float*>(smem + C::OFF_M + int(j % RM) * 2816); };
+  auto sConn = [&](int j) {
+    return reinterpret_cast<const int32_t*>(smem + C::OFF_M + int(j % RM) * 2816 + C::GEOT * 4);
+  };
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* b_full = bars;
   uint64_t* b_empty = b_full + RB;
-  uint64_t* av_full = b_empty + RB;
-  uint64_t* av_empty = av_full + RV;
-  uint64_t* af_full = av_empty + RV;
-  uint64_t* af_empty = af_full + RF;
-  uint64_t* s_full = af_empty + RF;
+  uint64_t* a_full = b_empty + RB;   // TMEM operand ring (writers -> MMA)
+  uint64_t* a_empty = a_full + RA;   // (MMA commit -> writers)
+  uint64_t* f_full = a_empty + RA;   // flux staging ring (flux warps -> writers)
+  uint64_t* f_empty = f_full + LF;   // (writers -> flux warps)
+  uint64_t* s_full = f_empty + LF;
   uint64_t* s_empty = s_full + RS;
-  uint64_t* acc_full = s_empty + RS;
+  uint64_t* m_full = s_empty + RS;
+  uint64_t* m_empty = m_full + RM;
+  uint64_t* acc_full = m_empty + RM;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBAR);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t J = t_count > blockIdx.x ? (t_count - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  const int64_t kend = p.k_begin + p.K;
-  auto tile_of = [&](int64_t j) { return t_begin + blockIdx.x + j * gridDim.x; };
-  auto count_of = [&](int64_t tile) {
-    const int64_t k0 = tile * E;
+  const int J = t_count > blockIdx.x ? (t_count - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int kend = int(p.k_begin + p.K);
+  auto tile_of = [&](int j) { return t_begin + blockIdx.x + j * gridDim.x; };
+  auto count_of = [&](int tile) {
+    const int k0 = tile * E;
     return int(kend - k0 < E ? kend - k0 : E);
   };
 
@@ -157,17 +228,21 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
       mbar_init(b_full + i, 1);
       mbar_init(b_empty + i, 1);
     }
-    for (int i = 0; i < RV; ++i) {
-      mbar_init(av_full + i, 4);
-      mbar_init(av_empty + i, 1);
+    for (int i = 0; i < RA; ++i) {
+      mbar_init(a_full + i, 4);
+      mbar_init(a_empty + i, 1);
     }
-    for (int i = 0; i < RF; ++i) {
-      mbar_init(af_full + i, C::PW);
-      mbar_init(af_empty + i, 1);
+    for (int i = 0; i < LF; ++i) {
+      mbar_init(f_full + i, C::PW);
+      mbar_init(f_empty + i, 4);
     }
     for (int i = 0; i < RS; ++i) {
       mbar_init(s_full + i, 1);
       mbar_init(s_empty + i, 4);
+    }
+    for (int i = 0; i < RM; ++i) {
+      mbar_init(m_full + i, 1);
+      mbar_init(m_empty + i, 4 + C::PW);  // operand writers + flux warps
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(acc_full + a, 1);
@@ -180,9 +255,11 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
                  "n"(C::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  // generated-operand rings start zeroed: rows 126, 127 are never written and must stay finite
-  for (int w = tid; w < (RV + RF) * C::ACH; w += C::NT) sAV[w] = 0.0f;
-  for (int w = tid; w < C::NTAB; w += C::NT) sFm[w] = p.ftab[w];
+  for (int w = tid; w < NF + 30 * Nfp; w += C::NT) sFm[w] = p.ftab[w];
+  for (int w = tid; w < 8 * NFQ; w += C::NT) {  // chunk slot w -> face node m = w: f | i << 2 | Fmask[m] << 8
+    const int f = w / Nfp, i = w - f * Nfp;
+    sFm[NF + 30 * Nfp + w] = int16_t(w < NF ? (f | (i << 2) | (int(p.ftab[w]) << 8)) : 0xffff);
+  }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -197,19 +274,20 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
     // behind the MMA / the previous group instead of serializing with the stores.
     const int r = 32 * warp + lane, e = r / 6;
     const bool res_in = UPDATE && !p.first_stage;
-    for (int64_t j = 0; j < J; ++j) {
+    TC_T(tcta);
+    for (int j = 0; j < J; ++j) {
       const int a = int(j & 1);
-      const int64_t tile = tile_of(j);
+      const int tile = tile_of(j);
       const bool valid = r < ROWS && e < count_of(tile);
-      const int64_t base = tile * TS + r;
+      const int base = tile * TS + r;
       auto ld_grp = [&](int c0, float (&uv)[16], float (&rv)[16]) {
+        const float* up = p.u_in + base + c0 * ROWS;
+        const float* rp = p.res + base + c0 * ROWS;
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const int n = c0 + i;
-          const bool ok = UPDATE && valid && n < Np;
-          const int64_t o = base + int64_t(ok ? n : 0) * ROWS;
-          uv[i] = ok ? __ldg(p.u_in + o) : 0.0f;
-          rv[i] = ok && res_in ? p.res[o] : 0.0f;
+          const bool ok = UPDATE && valid && c0 + i < Np;
+          uv[i] = ok ? __ldg(up + i * ROWS) : 0.0f;
+          rv[i] = ok && res_in ? rp[i * ROWS] : 0.0f;
         }
       };
       auto process = [&](int c0, const float (&uv)[16], const float (&rv)[16]) {
@@ -221,18 +299,18 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
             : "r"(tmem + (uint32_t(32 * warp) << 16) + uint32_t(a * NP16 + c0)));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (valid) {
+          float* rp = p.res + base + c0 * ROWS;
+          float* op = (UPDATE ? p.u_out : p.rhs_out) + base + c0 * ROWS;
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const int n = c0 + i;
-            if (n < Np) {
-              const int64_t o = base + int64_t(n) * ROWS;
+            if (c0 + i < Np) {
               const float d = __uint_as_float(v[i]);
               if (UPDATE) {
                 const float rr = p.rk_a * rv[i] + p.dt * d;
-                p.res[o] = rr;
-                p.u_out[o] = uv[i] + p.rk_b * rr;
+                rp[i * ROWS] = rr;
+                op[i * ROWS] = uv[i] + p.rk_b * rr;
               } else {
-                p.rhs_out[o] = d;
+                op[i * ROWS] = d;
               }
             }
           }
@@ -240,7 +318,10 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
       };
       float ua[16], ra[16], ub[16], rb[16];
       ld_grp(0, ua, ra);
-      mbar_wait(acc_full + a, unsigned(j >> 1) & 1);
+      TC_T(t0);
+      tc_wait(acc_full + a, unsigned(j >> 1) & 1);
+      TC_A(0, t0);
+      TC_T(t1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
       for (int c0 = 0; c0 < NP16; c0 += 32) {
@@ -254,92 +335,115 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty + a);
+      TC_A(1, t1);
+#ifdef DG_WS_PROFILE
+      if (tid == 0) atomicAdd(&g_tc_prof[12], 1ull);
+#endif
     }
+#ifdef DG_WS_PROFILE
+    if (tid == 0) atomicAdd(&g_tc_prof[13], (unsigned long long)(clock64() - tcta));
+#endif
   } else if (warp == C::W_LD) {
-    // ===================== slab loader (field tiles) =====================
     if (lane == 0) {
-      for (int64_t j = 0; j < J; ++j) {
-        const float* src = p.u_in + tile_of(j) * TS;
-        for (int o = 0; o < NO; ++o) {
-          const int64_t g = j * NO + o;
-          const int s = int(g % RS);
-          mbar_wait(s_empty + s, (unsigned(g / RS) & 1) ^ 1);
-          const int nodes = Np - 8 * o < 8 ? Np - 8 * o : 8;
-          unsigned bytes = unsigned(nodes * ROWS * 4);
-          bytes = (bytes + 15) & ~15u;  // an odd node count ends 8 B short; the tile padding covers it
-          mbar_arrive_tx(s_full + s, bytes);
-          bulk_g2s(sS + s * C::SLABF, src + 8 * o * ROWS, bytes, s_full + s);
-        }
-      }
-    } else if (lane == 1) {
-      // ====================== operator loader ======================
+      // ===== loader: one thread drives both copy streams with non-blocking barrier tests =====
+      // stream 1: per tile, geometry + connectivity (meta ring), then its node-octet slabs;
+      // stream 2: the operator chunks in MMA order (streamed orders; resident: one copy).
       if constexpr (C::OP_RES) {
         mbar_arrive_tx(b_full, unsigned(C::OPS_FLOATS * 4));
         bulk_g2s(sB, ops, unsigned(C::OPS_FLOATS * 4), b_full);
-      } else {
-        for (int64_t j = 0; j < J; ++j) {
-          for (int s = 0; s < NQ; ++s) {
-            const int64_t g = j * NQ + s;
-            const int b = int(g % RB);
-            mbar_wait(b_empty + b, (unsigned(g / RB) & 1) ^ 1);
-            mbar_arrive_tx(b_full + b, unsigned(C::OPC * 4));
-            bulk_g2s(sB + b * C::OPC, ops + int64_t(s) * C::OPC, unsigned(C::OPC * 4), b_full + b);
+      }
+      const int T2 = C::OP_RES ? 0 : J * NQ;
+      int j1 = 0, o1 = -1, g1 = 0, g2 = 0;
+      while (j1 < J || g2 < T2) {
+        bool moved = false;
+        if (j1 < J) {
+          const int tile = tile_of(j1);
+          if (o1 < 0) {
+            const int ms = j1 % RM;
+            if (mbar_test(m_empty + ms, (unsigned(j1 / RM) & 1) ^ 1)) {
+              mbar_arrive_tx(m_full + ms, unsigned(C::GEOT * 4 + C::CONNT * 4));
+              bulk_g2s(smem + C::OFF_M + ms * 2816, p.geo + tile * C::GEOT, unsigned(C::GEOT * 4), m_full + ms);
+              bulk_g2s(smem + C::OFF_M + ms * 2816 + C::GEOT * 4, p.gidx + tile * C::CONNT, unsigned(C::CONNT * 4),
+                       m_full + ms);
+              o1 = 0;
+              moved = true;
+            }
+          } else {
+            const int s = g1 % RS;
+            if (mbar_test(s_empty + s, (unsigned(g1 / RS) & 1) ^ 1)) {
+              const int nodes = Np - 8 * o1 < 8 ? Np - 8 * o1 : 8;
+              unsigned bytes = unsigned(nodes * ROWS * 4);
+              bytes = (bytes + 15) & ~15u;  // an odd node count ends 8 B short; the tile padding covers it
+              mbar_arrive_tx(s_full + s, bytes);
+              bulk_g2s(sS + s * C::SLABF, p.u_in + tile * TS + 8 * o1 * ROWS, bytes, s_full + s);
+              ++g1;
+              if (++o1 == NO) {
+                o1 = -1;
+                ++j1;
+              }
+              moved = true;
+            }
           }
         }
+        if (g2 < T2) {
+          const int b = g2 % RB;
+          if (mbar_test(b_empty + b, (unsigned(g2 / RB) & 1) ^ 1)) {
+            mbar_arrive_tx(b_full + b, unsigned(C::OPC * 4));
+            bulk_g2s(sB + b * C::OPC, ops + (g2 % NQ) * C::OPC, unsigned(C::OPC * 4), b_full + b);
+            ++g2;
+            moved = true;
+          }
+        }
+        if (!moved) __nanosleep(64);
       }
     }
   } else if (warp == C::W_MMA) {
     // ============================ MMA issuer ============================
     if (lane == 0) {
       constexpr uint32_t idesc = tc_idesc(128, NP16);
-      if constexpr (C::OP_RES) mbar_wait(b_full, 0);
-      int64_t gv = 0, gf = 0;
-      for (int64_t j = 0; j < J; ++j) {
+      if constexpr (C::OP_RES) tc_wait(b_full, 0);
+      int ga = 0;
+      for (int j = 0; j < J; ++j) {
         const int a = int(j & 1);
-        mbar_wait(acc_empty + a, (unsigned(j >> 1) & 1) ^ 1);
+        tc_wait(acc_empty + a, (unsigned(j >> 1) & 1) ^ 1);
         const uint32_t d = tmem + uint32_t(a * NP16);
-        int v = 0, f = 0;
-        for (int s = 0; s < NQ; ++s) {
-          const float* A;
-          uint64_t* rel;
-          if (tc_is_vol(v, f, NV, NFQ)) {
-            const int slot = int(gv % RV);
-            mbar_wait(av_full + slot, unsigned(gv / RV) & 1);
-            A = sAV + slot * C::ACH;
-            rel = av_empty + slot;
-            ++gv;
-            ++v;
-          } else {
-            const int slot = int(gf % RF);
-            mbar_wait(af_full + slot, unsigned(gf / RF) & 1);
-            A = sAF + slot * C::ACH;
-            rel = af_empty + slot;
-            ++gf;
-            ++f;
-          }
+        for (int s = 0; s < NQ; ++s, ++ga) {
+          const int slot = ga % RA;
+          TC_T(t0);
+          tc_wait(a_full + slot, unsigned(ga / RA) & 1);
+          TC_A(7, t0);
           const float* B;
           int b = 0;
           if constexpr (C::OP_RES) {
             B = sB + s * C::OPC;
           } else {
-            const int64_t g = j * NQ + s;
-            b = int(g % RB);
-            mbar_wait(b_full + b, unsigned(g / RB) & 1);
+            const int g = j * NQ + s;
+            b = g % RB;
+            TC_T(t2);
+            tc_wait(b_full + b, unsigned(g / RB) & 1);
+            TC_A(9, t2);
             B = sB + b * C::OPC;
           }
+          TC_T(t1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          tc_mma(d, tc_desc(A), tc_desc(B), idesc, s > 0 ? 1u : 0u);      // G . Op
-          tc_mma(d, tc_desc(A + 1024), tc_desc(B), idesc, 1u);            // G_lo . Op
-          tc_mma(d, tc_desc(A), tc_desc(B + 8 * NP16), idesc, 1u);        // G . Op_lo
-          tc_commit(rel);
+          const uint32_t ta = tmem + uint32_t(C::A0 + 16 * slot);  // G at ta, G_lo at ta + 8
+          tc_mma_ts(d, ta, tc_desc(B), idesc, s > 0 ? 1u : 0u);      // G . Op
+          tc_mma_ts(d, ta + 8, tc_desc(B), idesc, 1u);              // G_lo . Op
+          tc_mma_ts(d, ta, tc_desc(B + 8 * NP16), idesc, 1u);       // G . Op_lo
+          tc_commit(a_empty + slot);
           if constexpr (!C::OP_RES) tc_commit(b_empty + b);
+          TC_A(10, t1);
         }
         tc_commit(acc_full + a);
       }
     }
   } else if (warp < C::W_FG0) {
-    // ================== volume generators (a1 operand) ==================
-    const int r = tid - 32 * C::W_VG0, e = r / 6, out = r - 6 * (r / 6);
+    // ============ operand writers: G chunks into the TMEM ring, in MMA order ============
+    // Lane-owning warps (warp % 4 = TMEM lane quarter): row r = 32 (warp % 4) + lane.
+    // Volume chunk (octet o, derivative d) (a1): G = al_d u_f1 + be_d u_f2 from the slab;
+    // flux chunk (a2 + a3): G = the flux warps' values from the staging ring.  Written with
+    // tcgen05.st (no generic->async proxy fence on the path), G_lo = G - trunc_tf32(G).
+    const int r = 32 * (warp & 3) + lane, e = r / 6, out = r - 6 * (r / 6);
     // row -> (first field, its derivative direction, second field, its direction, sign):
     // rhsE = curl H, rhsH = -curl E;  out: Ex Ey Ez Hx Hy Hz
     const int f1 = out < 3 ? (out == 0 ? 5 : out == 1 ? 3 : 4) : (out == 3 ? 2 : out == 4 ? 0 : 1);
@@ -347,151 +451,249 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
     const int x1 = out % 3 == 0 ? 1 : out % 3 == 1 ? 2 : 0;  // curl_x = d_y(.) - d_z(.), cyclic
     const int x2 = out % 3 == 0 ? 2 : out % 3 == 1 ? 0 : 1;
     const float sg = out < 3 ? 1.0f : -1.0f;
-    for (int64_t j = 0; j < J; ++j) {
-      const int64_t tile = tile_of(j);
+    const uint32_t trow = tmem + (uint32_t(32 * (warp & 3)) << 16);
+    int ga = 0, gs = 0, gf = 0;
+    for (int j = 0; j < J; ++j) {
+      const int tile = tile_of(j);
       const bool valid = r < ROWS && e < count_of(tile);
+      static_assert(C::RA >= C::WB, "TMEM ring holds a writer batch");
       float al[3], be[3];
+      tc_wait(m_full + j % RM, unsigned(j / RM) & 1);
       {
-        const float* g = p.geo + (tile * E + (valid ? e : 0)) * GEO_W;
+        const float* g = sGeo(j) + (valid ? e : 0) * GEO_W;
 #pragma unroll
         for (int dd = 0; dd < 3; ++dd) {
-          al[dd] = valid ? sg * __ldg(g + 3 * dd + x1) : 0.0f;
-          be[dd] = valid ? -sg * __ldg(g + 3 * dd + x2) : 0.0f;
+          al[dd] = valid ? sg * g[3 * dd + x1] : 0.0f;
+          be[dd] = valid ? -sg * g[3 * dd + x2] : 0.0f;
         }
       }
-      for (int o = 0; o < NO; ++o) {
-        const int64_t gs = j * NO + o;
-        const int ss = int(gs % RS);
-        mbar_wait(s_full + ss, unsigned(gs / RS) & 1);
-        const float* sl = sS + ss * C::SLABF + 6 * e;
-        float u1[8], u2[8];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(m_empty + j % RM);
+      float u1[8], u2[8];
+      int v = 0, f = 0;
+      TC_T(t1);
+      // WB steps per batch: one tcgen05.wait::st for WB chunk stores.  For small NQ the whole
+      // tile schedule is unrolled, so the volume/flux interleave is resolved at compile time.
+#pragma unroll(C::WUNR)
+      for (int s0 = 0; s0 < NQ; s0 += C::WB) {
+        const int nb = NQ - s0 < C::WB ? NQ - s0 : C::WB;
+        float vv[C::WB][8];
 #pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-          const bool ok = valid && 8 * o + jj < Np;
-          u1[jj] = ok ? sl[jj * ROWS + f1] : 0.0f;
-          u2[jj] = ok ? sl[jj * ROWS + f2] : 0.0f;
+        for (int bq = 0; bq < C::WB; ++bq) {
+          if (bq < nb) {
+            if (tc_is_vol(v, f, NV, NFQ)) {
+              const int o = v / 3, dd = v - 3 * o;
+              if (dd == 0) {  // a new octet slab: its two fields for this row
+                const int ss = gs % RS;
+                TC_T(t0);
+                tc_wait(s_full + ss, unsigned(gs / RS) & 1);
+                TC_A(2, t0);
+                const float* sl = sS + ss * C::SLABF + 6 * e;
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                  const bool ok = valid && 8 * o + jj < Np;
+                  u1[jj] = ok ? sl[jj * ROWS + f1] : 0.0f;
+                  u2[jj] = ok ? sl[jj * ROWS + f2] : 0.0f;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(s_empty + ss);
+                ++gs;
+              }
+              const float a1 = dd == 0 ? al[0] : dd == 1 ? al[1] : al[2];
+              const float b1 = dd == 0 ? be[0] : dd == 1 ? be[1] : be[2];
+#pragma unroll
+              for (int jj = 0; jj < 8; ++jj) vv[bq][jj] = a1 * u1[jj] + b1 * u2[jj];
+              ++v;
+            } else {
+              const int fs = gf % LF;
+              TC_T(t0);
+              tc_wait(f_full + fs, unsigned(gf / LF) & 1);
+              TC_A(2, t0);
+              const float4* src = reinterpret_cast<const float4*>(sFS + fs * C::FSC + 8 * r);
+              const float4 x = src[0], y = src[1];
+              const bool ok = r < ROWS;  // rows 126, 127 of the MMA are padding: keep them zero
+              vv[bq][0] = ok ? x.x : 0.0f;
+              vv[bq][1] = ok ? x.y : 0.0f;
+              vv[bq][2] = ok ? x.z : 0.0f;
+              vv[bq][3] = ok ? x.w : 0.0f;
+              vv[bq][4] = ok ? y.x : 0.0f;
+              vv[bq][5] = ok ? y.y : 0.0f;
+              vv[bq][6] = ok ? y.z : 0.0f;
+              vv[bq][7] = ok ? y.w : 0.0f;
+              __syncwarp();
+              if (lane == 0) mbar_arrive(f_empty + fs);
+              ++gf;
+              ++f;
+            }
+          }
         }
+        TC_A(4, t1);
+        TC_T(t2);
+#pragma unroll
+        for (int bq = 0; bq < C::WB; ++bq) {
+          if (bq < nb) {
+            const int slot = (ga + bq) % RA;
+            tc_wait(a_empty + slot, (unsigned((ga + bq) / RA) & 1) ^ 1);
+            if (bq == 0) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            uint32_t w[16];
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+              w[jj] = __float_as_uint(vv[bq][jj]);
+              w[8 + jj] = __float_as_uint(tf32_lo(vv[bq][jj]));
+            }
+            asm volatile(
+                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::
+                    "r"(trow + uint32_t(C::A0 + 16 * slot)),
+                "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(w[8]),
+                "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15])
+                : "memory");
+          }
+        }
+        TC_A(3, t2);
+#ifdef DG_WS_PROFILE
+        t1 = clock64();
+#endif
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive(s_empty + ss);
-#pragma unroll
-        for (int dd = 0; dd < 3; ++dd) {
-          const int64_t gv = gs * 3 + dd;
-          const int slot = int(gv % RV);
-          mbar_wait(av_empty + slot, (unsigned(gv / RV) & 1) ^ 1);
-          float* A = sAV + slot * C::ACH;
-          float vv[8];
-#pragma unroll
-          for (int jj = 0; jj < 8; ++jj) vv[jj] = al[dd] * u1[jj] + be[dd] * u2[jj];
-          float4* h0 = reinterpret_cast<float4*>(A + tc_cm(r, 0));
-          float4* h1 = reinterpret_cast<float4*>(A + tc_cm(r, 4));
-          float4* l0 = reinterpret_cast<float4*>(A + 1024 + tc_cm(r, 0));
-          float4* l1 = reinterpret_cast<float4*>(A + 1024 + tc_cm(r, 4));
-          *h0 = make_float4(vv[0], vv[1], vv[2], vv[3]);
-          *h1 = make_float4(vv[4], vv[5], vv[6], vv[7]);
-          *l0 = make_float4(tf32_lo(vv[0]), tf32_lo(vv[1]), tf32_lo(vv[2]), tf32_lo(vv[3]));
-          *l1 = make_float4(tf32_lo(vv[4]), tf32_lo(vv[5]), tf32_lo(vv[6]), tf32_lo(vv[7]));
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tcgen05.mma operand
-          __syncwarp();
-          if (lane == 0) mbar_arrive(av_full + slot);
-        }
+        if (lane == 0)
+          for (int bq = 0; bq < nb; ++bq) mbar_arrive(a_full + (ga + bq) % RA);
+        ga += nb;
       }
+      TC_A(4, t1);
     }
   } else {
-    // ============== flux generators (a2 + a3: lift operand) ==============
+    // ============ flux (a2 + a3): upwind/PEC flux x Fscale/2 -> flux staging ============
+    // Item (element e, face-node slot kk) per thread and chunk.  Its traces u- and u+ are
+    // cp.async'ed LT - 1 chunks ahead into this thread's own staging slots (per-thread
+    // cp.async groups: no cross-thread synchronisation); the flux goes to the staging ring
+    // as plain shared stores, which the operand writers pick up.
     const int ft = tid - 32 * C::W_FG0;
     const int kk = ft & 7, e = ft >> 3;
-    const bool item = e < E;
-    for (int64_t j = 0; j < J; ++j) {
-      const int64_t tile = tile_of(j);
-      const bool act = item && e < count_of(tile);
-      const int64_t k = tile * E + (act ? e : 0);
-      float nrm[4][4];
-      int32_t fb[4];
-      int fcd[4];
-#pragma unroll
-      for (int f = 0; f < 4; ++f) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) nrm[f][i] = __ldg(p.geo + k * GEO_W + 9 + 4 * f + i);
-        fb[f] = act ? __ldg(p.gidx + 4 * k + f) : -1;
-        fcd[f] = __ldg(p.fcode + 4 * k + f);
+    const bool item = ft < ITEMS;
+    const int TOT = J * NFQ;
+    const uint16_t* sQ = reinterpret_cast<const uint16_t*>(sGP + 6 * Nfp);  // [NFQ][8]: f | i << 2 | Fmask << 8
+    float* const stg0 = sTR + 2 * ft;   // this thread's staging words: + (slot * 6 + pair) * 2 * FTH
+    constexpr int PST = 2 * C::FTH;     // floats between pairs
+    // issue side: (tile, chunk) = (ji, qi), staging slot si
+    int ji = 0, qi = 0, si = 0;
+    bool act_i = false;
+    const float* uT_i = p.u_in;
+    const int32_t* cn_i = nullptr;
+    int codes_i = 0;
+    auto issue = [&]() {
+      if (qi == 0) {
+        tc_wait(m_full + ji % RM, unsigned(ji / RM) & 1);
+        const int tile = tile_of(ji);
+        act_i = item && e < count_of(tile);
+        uT_i = p.u_in + tile * TS + 6 * e;
+        cn_i = sConn(ji) + 4 * e;
+        codes_i = sConn(ji)[4 * E + e];
       }
-      const float* uT = p.u_in + tile * TS + 6 * e;
-      // one face node's traces: u- from the element, u+ from the neighbour / ghost record / PEC mirror
-      auto load = [&](int q, float (&uM)[6], float (&uP)[6], int& kind) {
-        const int m = 8 * q + kk;
-        kind = 0;  // 0: nothing (padding / absent element), 1: PEC wall, 2: interior face
-        if (act && m < NF) {
-          const int f = m / Nfp, i = m - f * Nfp;
-          const float* src = uT + int(sFm[m]) * ROWS;
+      const int code = sQ[qi * 8 + kk];  // 0xffff: slot past the last face node
+      if (act_i && code != 0xffff) {
+        const int f = code & 3, i = (code >> 2) & 63;
+        float* d = stg0 + si * 6 * PST;
+        const float* src = uT_i + (code >> 8) * ROWS;
 #pragma unroll
-          for (int c = 0; c < 6; ++c) uM[c] = src[c];
-          const int32_t b = f == 0 ? fb[0] : f == 1 ? fb[1] : f == 2 ? fb[2] : fb[3];
-          const int cd = f == 0 ? fcd[0] : f == 1 ? fcd[1] : f == 2 ? fcd[2] : fcd[3];
-          if (b < 0) {
-            kind = 1;
-          } else if (b & TileLayout::GHOST_FLAG) {
+        for (int c = 0; c < 3; ++c) cp_async8(d + c * PST, src + 2 * c);
+        const int32_t b = cn_i[f];
+        const int cd = (codes_i >> (8 * f)) & 0xff;
+        if (b >= 0) {
+          if (b & TileLayout::GHOST_FLAG) {
             const float* g = p.u_in + p.ghost_base + (b & ~TileLayout::GHOST_FLAG) + sGP[cd * Nfp + i];
 #pragma unroll
-            for (int c = 0; c < 6; ++c) uP[c] = g[c * Nfp];
-            kind = 2;
+            for (int c = 0; c < 6; ++c) cp_async4(d + (3 + c / 2) * PST + (c & 1), g + c * Nfp);
           } else {
             const float* g = p.u_in + b + int(sNP[cd * Nfp + i]) * ROWS;
 #pragma unroll
-            for (int c = 0; c < 6; ++c) uP[c] = g[c];
-            kind = 2;
+            for (int c = 0; c < 3; ++c) cp_async8(d + (3 + c) * PST, g + 2 * c);
           }
-        }
-      };
-      auto emit = [&](int q, const float (&uM)[6], const float (&uP)[6], int kind) {
-        float fl[6] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
-        if (kind) {
-          const int f = (8 * q + kk) / Nfp;
-          const float nx = f == 0 ? nrm[0][0] : f == 1 ? nrm[1][0] : f == 2 ? nrm[2][0] : nrm[3][0];
-          const float ny = f == 0 ? nrm[0][1] : f == 1 ? nrm[1][1] : f == 2 ? nrm[2][1] : nrm[3][1];
-          const float nz = f == 0 ? nrm[0][2] : f == 1 ? nrm[1][2] : f == 2 ? nrm[2][2] : nrm[3][2];
-          const float fs = f == 0 ? nrm[0][3] : f == 1 ? nrm[1][3] : f == 2 ? nrm[2][3] : nrm[3][3];
-          float dE[3], dH[3];
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {  // PEC wall: E+ = -E-, H+ = H-
-            dE[c] = kind == 2 ? uP[c] - uM[c] : -2.0f * uM[c];
-            dH[c] = kind == 2 ? uP[c + 3] - uM[c + 3] : 0.0f;
-          }
-          maxwell_flux<float>(nx, ny, nz, p.alpha, dE, dH, fl);
-          const float sc = 0.5f * fs;
-#pragma unroll
-          for (int c = 0; c < 6; ++c) fl[c] *= sc;
-        }
-        const int64_t gq = j * NFQ + q;
-        const int slot = int(gq % RF);
-        mbar_wait(af_empty + slot, (unsigned(gq / RF) & 1) ^ 1);
-        float* A = sAF + slot * C::ACH;
-        if (item) {
-#pragma unroll
-          for (int c = 0; c < 6; ++c) {
-            const int o = tc_cm(6 * e + c, kk);
-            A[o] = fl[c];
-            A[1024 + o] = tf32_lo(fl[c]);
-          }
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(af_full + slot);
-      };
-      float xM[6], xP[6], yM[6], yP[6];
-      int xk = 0, yk = 0;
-#pragma unroll
-      for (int c = 0; c < 6; ++c) xM[c] = xP[c] = yM[c] = yP[c] = 0.0f;
-      load(0, xM, xP, xk);
-#pragma unroll 1
-      for (int q = 0; q < NFQ; q += 2) {
-        if (q + 1 < NFQ) load(q + 1, yM, yP, yk);
-        emit(q, xM, xP, xk);
-        if (q + 1 < NFQ) {
-          if (q + 2 < NFQ) load(q + 2, xM, xP, xk);
-          emit(q + 1, yM, yP, yk);
         }
       }
+      cp_commit();
+      if (++si == LT) si = 0;
+      if (++qi == NFQ) {
+        qi = 0;
+        ++ji;
+      }
+    };
+    TC_T(tw);
+    for (int G = 0; G < LT - 1; ++G) {  // always LT - 1 groups, so cp_wait<LT - 1> below covers chunk G
+      if (G < TOT)
+        issue();
+      else
+        cp_commit();
     }
+    int j = 0, q = 0, sc_ = 0, fsl = 0;
+    unsigned fph = 0;
+    bool act = false;
+    const float* gE = nullptr;
+    const int32_t* cn = nullptr;
+    for (int G = 0; G < TOT; ++G) {
+      if (q == 0) {
+        act = item && e < count_of(tile_of(j));
+        gE = sGeo(j) + e * GEO_W + 9;
+        cn = sConn(j) + 4 * e;
+      }
+      if (G + LT - 1 < TOT)
+        issue();
+      else
+        cp_commit();
+      cp_wait<LT - 1>();  // this thread's copies for chunk G have landed
+      const int code = sQ[q * 8 + kk];
+      float fl[6] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+      if (act && code != 0xffff) {
+        const int f = code & 3;
+        const float* gm = gE + 4 * f;
+        const float nx = gm[0], ny = gm[1], nz = gm[2], fs = gm[3];
+        const bool wall = cn[f] < 0;
+        const float* d = stg0 + sc_ * 6 * PST;
+        float uM[6], uP[6];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const float2 a2 = *reinterpret_cast<const float2*>(d + c * PST);
+          uM[2 * c] = a2.x;
+          uM[2 * c + 1] = a2.y;
+          const float2 b2 = *reinterpret_cast<const float2*>(d + (3 + c) * PST);
+          uP[2 * c] = b2.x;
+          uP[2 * c + 1] = b2.y;
+        }
+        float dE[3], dH[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {  // PEC wall: E+ = -E-, H+ = H-
+          dE[c] = wall ? -2.0f * uM[c] : uP[c] - uM[c];
+          dH[c] = wall ? 0.0f : uP[c + 3] - uM[c + 3];
+        }
+        maxwell_flux<float>(nx, ny, nz, p.alpha, dE, dH, fl);
+        const float sc = 0.5f * fs;
+#pragma unroll
+        for (int c = 0; c < 6; ++c) fl[c] *= sc;
+      }
+      if (++sc_ == LT) sc_ = 0;
+      TC_T(t0);
+      tc_wait(f_empty + fsl, fph ^ 1);
+      TC_A(5, t0);
+      if (item) {
+        float* F = sFS + fsl * C::FSC + 48 * e + kk;  // [row 6e + c][kk]
+#pragma unroll
+        for (int c = 0; c < 6; ++c) F[8 * c] = fl[c];
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(f_full + fsl);
+        if (q == NFQ - 1) mbar_arrive(m_empty + j % RM);  // done with this tile's meta slot
+      }
+      if (++fsl == LF) {
+        fsl = 0;
+        fph ^= 1;
+      }
+      if (++q == NFQ) {
+        q = 0;
+        ++j;
+      }
+    }
+    TC_A(6, tw);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();

@@ -1,5 +1,6 @@
 #!/usr/bin/env python
-"""Cycle breakdown of the tcgen05 TC stage kernel (profiling build, see tools/ws_profile.py)."""
+"""Cycle breakdown of the tcgen05 TC stage kernel (profiling build libdg_prof.so, `make prof`):
+per-role clock64 counters of stage_tc.cuh, cycles per tile per warp of the role."""
 import ctypes
 import os
 import sys
@@ -12,10 +13,9 @@ from paper_1211_0582_b200 import dg  # noqa: E402
 
 f = dg.lib.dg_debug_ws_profile
 f.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
-NAMES = ["load_wait_empty", "flux_wait_load", "flux_trace_issue", "flux_wait_traces", "flux_compute", "flux_lo_split",
-         "mma_wait_full", "mma_wait_acc_empty", "mma_issue", "epi_wait_acc_full", "epi_pass1", "epi_pass2",
-         "epi_store_release"]
-WARPS = [1, 4, 4, 4, 4, 4, 1, 1, 1, 4, 4, 4, 4]  # lane-0 counters per role
+NAMES = ["epi_wait_acc_full", "epi_work", "wr_wait_input", "wr_wait_tmem_slot", "wr_work", "flux_wait_slot",
+         "flux_total", "mma_wait_operand", "unused", "mma_wait_op", "mma_issue", "ldr_wait_slab_free"]
+WARPS = [4, 4, 4, 4, 4, 6, 6, 1, 1, 1, 1, 1]
 n = int(os.environ.get("MESH_N", "15"))
 for N in [int(a) for a in sys.argv[1:]] or [4]:
     VX, E = di.kuhn_box(n)
@@ -31,8 +31,9 @@ for N in [int(a) for a in sys.argv[1:]] or [4]:
     s.synchronize()
     f(N, buf, 0)
     v = list(buf)[16:]
-    tiles = max(v[13], 1)
-    print(f"N={N} tiles={tiles}  cycles per tile per warp of the role:")
+    tiles = max(v[12], 1)
+    ctas = 148
+    print(f"N={N} tiles={tiles}  CTA cycles per tile {v[13] / tiles:.0f}; cycles per tile per warp of the role:")
     for i, k in enumerate(NAMES):
         print(f"  {k:20s} {v[i] / tiles / WARPS[i]:10.0f}")
     s.close()
