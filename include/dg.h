@@ -68,15 +68,18 @@ typedef enum {
 } dg_status;
 
 typedef enum {
-  DG_VARIANT_AUTO = 0,   /* measured best per (precision, N): MMA_WS, except FP32 N=1,2,3,6,9 and
-                            FP64 N=1 -> FFMA (tools/variant_sweep.py) */
+  DG_VARIANT_AUTO = 0,   /* measured best per (precision, N): FP64 MMA_WS (N >= 2) / FFMA (N = 1);
+                            FP32 TC (N >= 4) / FFMA (N <= 3) (tools/variant_sweep.py) */
   DG_VARIANT_BASIC = 1,  /* one fused element-tile kernel per stage, FMA contractions */
   DG_VARIANT_MMA = 2,    /* FP64: DMMA contractions, cp.async-pipelined persistent kernel
                             (FP32: same as BASIC) */
   DG_VARIANT_MMA_WS = 3, /* warp-specialized TMA/mbarrier pipeline; contractions on tensor
                             cores: FP64 DMMA, FP32 3xTF32 HMMA */
-  DG_VARIANT_TC = 4,     /* FP32, N <= 4: tcgen05.mma kind::tf32 (3xTF32) with TMEM
-                            accumulators (5th-generation tensor cores) */
+  DG_VARIANT_TC = 4,     /* FP32, N = 1..9: the whole RHS of a 21-element tile as one K-chunked
+                            tcgen05.mma kind::tf32 GEMM (3xTF32): chain rule + curl folded into
+                            the generated operand (written to tensor memory), upwind flux as
+                            the lift operand, TMEM accumulators, LSERK update in the epilogue
+                            (5th-generation tensor cores; stage_tc.cuh) */
   DG_VARIANT_FUSED = 5,  /* FP64, single rank: the MMA_WS kernel running all 5 x nsteps stages of a
                             dg_lserk_step call in ONE persistent launch, tiles ordered by per-tile
                             completion counters instead of kernel boundaries.  Bitwise equal to

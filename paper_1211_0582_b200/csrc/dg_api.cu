@@ -181,13 +181,12 @@ void release_device(dg_solver* s) {
 
 
 // DG_VARIANT_AUTO: the measured-best kernel per (precision, order) on the bench
-// config (NEXT-4 sweep, tools/variant_sweep.py, profiles/r1_pdl_sweep.jsonl):
-// FP64 -> FFMA (register-tiled DFMA) at N = 1, MMA_WS (DMMA) otherwise; FP32 -> FFMA
-// (register-tiled SIMT) at N = 1, 2, 3, 6 and 9, MMA_WS (3xTF32 HMMA) at N = 4, 5, 7, 8.
+// config (NEXT-4 sweep, tools/variant_sweep.py, tools/tc_check.py): FP64 -> FFMA
+// (register-tiled DFMA) at N = 1, MMA_WS (DMMA) otherwise; FP32 -> FFMA (register-tiled
+// SIMT) at N = 1, 2, 3, TC (tcgen05 kind::tf32 3xTF32, TMEM operands) at N >= 4.
 int auto_variant(bool fp64, int N) {
-  if (fp64 && N == 1) return DG_VARIANT_FFMA;
-  if (!fp64 && (N <= 3 || N == 6 || N == 9)) return DG_VARIANT_FFMA;
-  return DG_VARIANT_MMA_WS;
+  if (fp64) return N == 1 ? DG_VARIANT_FFMA : DG_VARIANT_MMA_WS;
+  return N <= 3 ? DG_VARIANT_FFMA : DG_VARIANT_TC;
 }
 
 dg_status need_device(dg_solver* s) {
@@ -390,7 +389,6 @@ dg_status upload_setup(dg_solver* s) {
   }
   s->ES = s->lay.TS;
   s->ntiles = s->lay.ntiles(Kl);
-  const int64_t Kpad = s->ntiles * s->lay.E;
   const int64_t twords = s->ntiles * s->lay.TS;
   s->ghost_base = twords;
   s->ghost_words = P.n_ghost_faces * s->nc * Nfp;
@@ -663,10 +661,15 @@ dg_status time_stage(dg_solver* s, int reps, double* ms) {
 
 #ifdef DG_WS_PROFILE
 namespace dg {
-#define DG_PDECL(n) void ws_prof_N##n(unsigned long long*, int);
+#define DG_PDECL(n) void ws_prof_N##n(unsigned long long*, int); void tc_dbg_N##n(float*);
 DG_PDECL(1) DG_PDECL(2) DG_PDECL(3) DG_PDECL(4) DG_PDECL(5) DG_PDECL(6) DG_PDECL(7) DG_PDECL(8) DG_PDECL(9)
 }  // namespace dg
 // profiling builds only (libdg_prof.so): read/reset the WS kernel's cycle counters
+extern "C" __attribute__((visibility("default"))) void dg_debug_tc_dump(int N, float* dev) {
+  static void (*const t[9])(float*) = {dg::tc_dbg_N1, dg::tc_dbg_N2, dg::tc_dbg_N3, dg::tc_dbg_N4, dg::tc_dbg_N5,
+                                       dg::tc_dbg_N6, dg::tc_dbg_N7, dg::tc_dbg_N8, dg::tc_dbg_N9};
+  if (N >= 1 && N <= 9) t[N - 1](dev);
+}
 extern "C" __attribute__((visibility("default"))) void dg_debug_ws_profile(int N, unsigned long long* out, int reset) {
   static void (*const t[9])(unsigned long long*, int) = {dg::ws_prof_N1, dg::ws_prof_N2, dg::ws_prof_N3,
                                                          dg::ws_prof_N4, dg::ws_prof_N5, dg::ws_prof_N6,

@@ -65,6 +65,7 @@ bool DG_FN(launch_fused_f64)(const StageParams<double>& p, const FusedParams<dou
 }
 
 #ifdef DG_WS_PROFILE
+void DG_FN(tc_dbg)(float* p) { tc_dbg_set(p); }
 void DG_FN(ws_prof)(unsigned long long* out, int reset) {
   if (reset) {
     ws_prof_reset();

@@ -42,6 +42,25 @@
 
 #include "stage_ws.cuh"
 
+#ifndef DG_TC_WB
+#define DG_TC_WB 3
+#endif
+#ifndef DG_TC_RA
+#define DG_TC_RA 12
+#endif
+#ifndef DG_TC_RB
+#define DG_TC_RB 12
+#endif
+#ifndef DG_TC_LF
+#define DG_TC_LF 6
+#endif
+#ifndef DG_TC_RS
+#define DG_TC_RS 4
+#endif
+#ifndef DG_TC_RM
+#define DG_TC_RM 4
+#endif
+
 namespace dg {
 
 // the MMA's fixed interleave of the NV volume and NFQ flux chunks of a tile
@@ -70,22 +89,30 @@ struct TcCfg {
   static constexpr int FTH = 32 * PW;
   static constexpr int LT = 4;                      // per-thread cp.async trace pipeline depth (chunks)
   static constexpr int TRC = FTH * 12;              // floats per trace-staging chunk: [6 pairs][FTH][2]
-  static constexpr int LF = 6;                      // flux staging ring (chunks) [128 rows][8]
+  static constexpr int LF = DG_TC_LF;               // flux staging ring (chunks) [128 rows][8]
   static constexpr int FSC = 128 * 8;
-  static constexpr int RS = 4, RM = 4;
-  static constexpr int WB = 3;                      // operand chunks per writer batch (one wait::st)
+  static constexpr int RS = DG_TC_RS, RM = DG_TC_RM;
+  static constexpr int WB = DG_TC_WB;               // operand chunks per writer batch (one wait::st)
   static constexpr int WUNR = NQ <= 36 ? (NQ + WB - 1) / WB : 1;
   // generated operand G in TENSOR memory (kind::tf32 A operand: lane = row, one column per k):
   // ring slots of 16 columns (8 G | 8 G_lo) after the two accumulators
-  static constexpr int A0 = 2 * NP16;
-  static constexpr int RA = (512 - A0) / 16 < 12 ? (512 - A0) / 16 : 12;
+#ifdef DG_TC_ONEACC
+  static constexpr int NACC = 1;                    // accumulators (tiles in flight between MMA and epilogue)
+#else
+  static constexpr int NACC = 2;
+#endif
+  static constexpr int ACC1 = NP16;                 // column of accumulator 1
+  static constexpr int NA = (512 - NACC * NP16) / 16;
+  static constexpr int RA_T = NA < DG_TC_RA ? NA : DG_TC_RA;
+  static __host__ __device__ constexpr int a_col(int k) { return NACC * NP16 + 16 * k; }
   static constexpr int al1k(int b) { return (b + 1023) / 1024 * 1024; }
   static constexpr int NTAB = NF + 24 * Nfp + 6 * Nfp + 8 * NFQ;  // int16: Fmask | node | ghost | chunk-slot tables
   static constexpr int FIXED = RS * SLABF * 4 + RM * 2816 + LT * TRC * 4 + LF * FSC * 4 +
                                (NTAB * 2 + 15) / 16 * 16 + 1024;
   static constexpr bool OP_RES = FIXED + al1k(NQ * OPC * 4) <= 226 * 1024;  // operators resident in smem
   static constexpr int RB_MAX = (226 * 1024 - FIXED) / (OPC * 4);
-  static constexpr int RB = OP_RES ? NQ : (RB_MAX < 12 ? RB_MAX : 12);
+  static constexpr int RA = RA_T;
+  static constexpr int RB = OP_RES ? NQ : (RB_MAX < DG_TC_RB ? RB_MAX : DG_TC_RB);
   // 16 warps: 4 per SMSP, so every thread can have 128 registers
   static constexpr int W_LD = 4, W_MMA = 5, W_VG0 = 6, W_FG0 = 10;
   static constexpr int NW = W_FG0 + PW;
@@ -139,6 +166,10 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
 // mbarrier wait with a suspend-time hint: a waiting warp sleeps until the phase completes
 // instead of spinning try_wait and stealing issue slots from the producer warps
 __device__ __forceinline__ void tc_wait(uint64_t* b, unsigned parity) {
+#ifdef DG_TC_SPIN
+  mbar_wait(b, parity);
+  return;
+#endif
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
@@ -159,6 +190,8 @@ __host__ __device__ constexpr int tc_cm(int r, int kk) { return ((r >> 3) * 2 + 
 // 6 FG work (loads + flux) | 7 MMA wait V chunk | 8 MMA wait F chunk | 9 MMA wait operator chunk |
 // 10 MMA issue | 11 slab loader wait | 12 tiles (epilogue warp 0) | 13 CTA cycles (epilogue warp 0)
 __device__ unsigned long long g_tc_prof[16];
+__device__ float* g_tc_dbg = nullptr;  // debug dump of the generated operand G [tile][NQ][128][8]
+inline void tc_dbg_set(float* p) { cudaMemcpyToSymbol(g_tc_dbg, &p, sizeof(p)); }
 #define TC_T(v) long long v = clock64()
 #define TC_A(i, t0) \
   do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_tc_prof[i], (unsigned long long)(clock64() - (t0))); } while (0)
@@ -276,7 +309,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
     const bool res_in = UPDATE && !p.first_stage;
     TC_T(tcta);
     for (int j = 0; j < J; ++j) {
-      const int a = int(j & 1);
+      const int a = j % C::NACC;
       const int tile = tile_of(j);
       const bool valid = r < ROWS && e < count_of(tile);
       const int base = tile * TS + r;
@@ -296,7 +329,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
             "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
             : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
               "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-            : "r"(tmem + (uint32_t(32 * warp) << 16) + uint32_t(a * NP16 + c0)));
+            : "r"(tmem + (uint32_t(32 * warp) << 16) + uint32_t(a * C::ACC1 + c0)));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (valid) {
           float* rp = p.res + base + c0 * ROWS;
@@ -319,7 +352,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
       float ua[16], ra[16], ub[16], rb[16];
       ld_grp(0, ua, ra);
       TC_T(t0);
-      tc_wait(acc_full + a, unsigned(j >> 1) & 1);
+      tc_wait(acc_full + a, unsigned(j / C::NACC) & 1);
       TC_A(0, t0);
       TC_T(t1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -404,9 +437,9 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
       if constexpr (C::OP_RES) tc_wait(b_full, 0);
       int ga = 0;
       for (int j = 0; j < J; ++j) {
-        const int a = int(j & 1);
-        tc_wait(acc_empty + a, (unsigned(j >> 1) & 1) ^ 1);
-        const uint32_t d = tmem + uint32_t(a * NP16);
+        const int a = j % C::NACC;
+        tc_wait(acc_empty + a, (unsigned(j / C::NACC) & 1) ^ 1);
+        const uint32_t d = tmem + uint32_t(a * C::ACC1);
         for (int s = 0; s < NQ; ++s, ++ga) {
           const int slot = ga % RA;
           TC_T(t0);
@@ -426,15 +459,15 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
           }
           TC_T(t1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t ta = tmem + uint32_t(C::A0 + 16 * slot);  // G at ta, G_lo at ta + 8
+          const uint32_t ta = tmem + uint32_t(C::a_col(slot));  // G at ta, G_lo at ta + 8
           tc_mma_ts(d, ta, tc_desc(B), idesc, s > 0 ? 1u : 0u);      // G . Op
           tc_mma_ts(d, ta + 8, tc_desc(B), idesc, 1u);              // G_lo . Op
           tc_mma_ts(d, ta, tc_desc(B + 8 * NP16), idesc, 1u);       // G . Op_lo
-          tc_commit(a_empty + slot);
-          if constexpr (!C::OP_RES) tc_commit(b_empty + b);
+          tc_commit(a_empty + slot);                                // frees the TMEM operand slot
+          if constexpr (!C::OP_RES) tc_commit(b_empty + b);         // frees the operator slot
+          if (s == NQ - 1) tc_commit(acc_full + a);                 // accumulator complete
           TC_A(10, t1);
         }
-        tc_commit(acc_full + a);
       }
     }
   } else if (warp < C::W_FG0) {
@@ -467,6 +500,9 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
           be[dd] = valid ? -sg * g[3 * dd + x2] : 0.0f;
         }
       }
+      // generic-proxy reads of a TMA-written (async-proxy) buffer must be ordered before the
+      // next TMA write into it: proxy fence before releasing the slot (cross-proxy WAR)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(m_empty + j % RM);
       float u1[8], u2[8];
@@ -495,6 +531,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
                   u1[jj] = ok ? sl[jj * ROWS + f1] : 0.0f;
                   u2[jj] = ok ? sl[jj * ROWS + f2] : 0.0f;
                 }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // cross-proxy WAR (see above)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(s_empty + ss);
                 ++gs;
@@ -534,7 +571,14 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
           if (bq < nb) {
             const int slot = (ga + bq) % RA;
             tc_wait(a_empty + slot, (unsigned((ga + bq) / RA) & 1) ^ 1);
-            if (bq == 0) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            // orders this store after the MMAs that read the slot (their commit completed the wait)
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#ifdef DG_WS_PROFILE
+            if (g_tc_dbg) {
+              float* dp = g_tc_dbg + ((size_t(tile) * NQ + (s0 + bq)) * 128 + r) * 8;
+              for (int jj = 0; jj < 8; ++jj) dp[jj] = vv[bq][jj];
+            }
+#endif
             uint32_t w[16];
 #pragma unroll
             for (int jj = 0; jj < 8; ++jj) {
@@ -543,7 +587,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
             }
             asm volatile(
                 "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::
-                    "r"(trow + uint32_t(C::A0 + 16 * slot)),
+                    "r"(trow + uint32_t(C::a_col(slot))),
                 "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(w[8]),
                 "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15])
                 : "memory");
@@ -640,7 +684,11 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
         issue();
       else
         cp_commit();
+#ifdef DG_TC_SYNCFLUX
+      cp_wait<0>();
+#else
       cp_wait<LT - 1>();  // this thread's copies for chunk G have landed
+#endif
       const int code = sQ[q * 8 + kk];
       float fl[6] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
       if (act && code != 0xffff) {
@@ -679,6 +727,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
 #pragma unroll
         for (int c = 0; c < 6; ++c) F[8 * c] = fl[c];
       }
+      if (q == NFQ - 1) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // meta slot: cross-proxy WAR
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(f_full + fsl);

@@ -176,7 +176,102 @@ void run() {
   cudaFree(dA); cudaFree(dB); cudaFree(dD); cudaFree(dc);
 }
 
+
+// Canary: does an MMA with D at columns [0, N) write TMEM columns >= N?  Columns N..N+63
+// are filled with 12345.0 by tcgen05.st before the MMA and read back after it.
+template <int N>
+__global__ void __launch_bounds__(128, 1) canary(const float* A, const float* B, int* changed) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  float* sB = reinterpret_cast<float*>(sm);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int w = tid; w < N * 8; w += 128) sB[cm(w / 8, w % 8)] = B[w];
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tslot)), "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tslot;
+  const uint32_t lrow = uint32_t(32 * warp) << 16;
+  {
+    uint32_t v[8];
+    for (int k = 0; k < 8; ++k) v[k] = __float_as_uint(A[(32 * warp + lane) * 8 + k]);
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(tmem + lrow + 448),
+                 "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]));
+    const uint32_t c = __float_as_uint(12345.0f);
+    for (int c0 = N; c0 < N + 64 && c0 < 448; c0 += 8)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(tmem + lrow + c0),
+                   "r"(c), "r"(c), "r"(c), "r"(c), "r"(c), "r"(c), "r"(c), "r"(c));
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (tid == 0) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem),
+        "r"(tmem + 448), "l"(desc(sB)), "r"(idesc_tf32(128, N)), "r"(0));
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar))
+                 : "memory");
+  }
+  asm volatile(
+      "{\n.reg .pred P1;\nW2:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+      "@!P1 bra W2;\n}\n" ::"r"(su32(&bar)));
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  int bad = 0;
+  for (int c0 = N; c0 < N + 64 && c0 < 448; c0 += 8) {
+    uint32_t v[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(tmem + lrow + c0));
+    asm volatile("tcgen05.wait::ld.sync.aligned;");
+    for (int i = 0; i < 8; ++i)
+      if (__uint_as_float(v[i]) != 12345.0f) bad = max(bad, c0 + i - N + 1);
+  }
+  atomicMax(changed, bad);
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+}
+
+template <int N>
+void run_canary() {
+  std::vector<float> A(128 * 8, 0.5f), B(N * 8, 0.25f);
+  float *dA, *dB;
+  int* dc;
+  cudaMalloc(&dA, A.size() * 4); cudaMalloc(&dB, B.size() * 4); cudaMalloc(&dc, 4);
+  cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemset(dc, 0, 4);
+  cudaFuncSetAttribute(canary<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  canary<N><<<1, 128, 64 * 1024>>>(dA, dB, dc);
+  cudaError_t e = cudaDeviceSynchronize();
+  int c = 0;
+  cudaMemcpy(&c, dc, 4, cudaMemcpyDeviceToHost);
+  printf("{\"canary_N\": %d, \"err\": \"%s\", \"columns_written_beyond_N\": %d}\n", N, cudaGetErrorString(e), c);
+  cudaFree(dA); cudaFree(dB); cudaFree(dc);
+}
+
 int main() {
+  run_canary<48>();
+  run_canary<80>();
+  run_canary<96>();
+  run_canary<112>();
+  run_canary<128>();
+  run_canary<144>();
+  run_canary<176>();
+  run_canary<224>();
+  return 0;
   run<48, true>();
   run<48, false>();
   run<16, true>();
