@@ -74,8 +74,12 @@ def load_peaks():
         peaks["fp64_tflops"] = float(ap["fp64_dfma_tflops"])
         peaks["fp32_tflops"] = float(ap["fp32_ffma_tflops"])
         peaks["dmma_tflops"] = float(ap["fp64_dmma_tflops"])
-        peaks["tf32x3_tflops"] = float(ap.get("tf32_mma_sync_tflops", 301.3)) / 3.0
-        peaks["alu_src"] = "measured (profiles/alu_peaks.json, tools/alu_peaks.cu, tools/tf32_mma.cu)"
+        # FP32 on tensor cores is 3xTF32 (3 MMA passes per algorithmic FMA): the denominator is the
+        # measured tcgen05 kind::tf32 peak / 3, for the tcgen05 (TC) and the mma.sync (WS) kernels alike
+        peaks["tf32x3_tflops"] = float(ap.get("tf32_tcgen05_tflops", 1113.7)) / 3.0
+        peaks["tf32_mma_sync_tflops"] = float(ap.get("tf32_mma_sync_tflops", 301.3))
+        peaks["alu_src"] = ("measured (profiles/alu_peaks.json: tools/alu_peaks.cu DFMA/FFMA/DMMA, "
+                            "tools/tcgen05_peak.cu tcgen05 kind::tf32)")
     else:
         # unit counts x max clock: 148 SMs x 64 DFMA (128 FFMA) lanes x 2 flop x 1.965 GHz
         peaks["fp64_tflops"] = 148 * 64 * 2 * 1.965e9 / 1e12
@@ -125,8 +129,11 @@ def roofline(N, prec, K_total, kernel_ms, peaks, variant=0, traffic=None, fpe=No
         return {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": traffic, "ai_flop_per_byte": round(ai, 2)}
     ach = F / (kernel_ms * 1e-3) / 1e12
-    return {"bound": "tensor" if tensor else "alu", "achieved": round(ach, 3), "peak": round(pipe, 2), "unit": "TFLOP/s",
-            "frac": round(ach / pipe, 4), "traffic": traffic, "ai_flop_per_byte": round(ai, 2)}
+    out = {"bound": "tensor" if tensor else "alu", "achieved": round(ach, 3), "peak": round(pipe, 2), "unit": "TFLOP/s",
+           "frac": round(ach / pipe, 4), "traffic": traffic, "ai_flop_per_byte": round(ai, 2)}
+    if prec != 8:  # FP32: also against the FFMA pipe (the SIMT side of the TF32-or-FFMA choice)
+        out["frac_ffma"] = round(ach / peaks["fp32_tflops"], 4)
+    return out
 
 
 class ClockSampler:

@@ -117,10 +117,17 @@ typedef struct {
                            gather locality and intra-tile faces; dg_local_elements reports the
                            storage order.  0 (default): ascending global id within each group */
   int32_t system;       /* dg_system (default DG_SYSTEM_MAXWELL) */
+  int32_t partition;    /* element owner when dg_mesh_upload gets part = NULL:
+                           DG_PARTITION_RANGES (default): contiguous element-index ranges
+                           (z-slabs on the cell-ordered Kuhn box); DG_PARTITION_RCB: recursive
+                           coordinate bisection of the element centroids (longest extent,
+                           rank-weighted median, ties by element id) */
 } dg_config;
 
+typedef enum { DG_PARTITION_RANGES = 0, DG_PARTITION_RCB = 1 } dg_partition;
+
 /* Fill *cfg with defaults: N=3, FP64, alpha=1, device 0, own stream, 1 rank, AUTO,
- * no reorder, Maxwell. */
+ * no reorder, Maxwell, range partition. */
 DG_API void dg_config_default(dg_config* cfg);
 
 /* Create a solver.  Builds the reference element of order N on the host (FP64).
@@ -216,6 +223,16 @@ DG_API dg_status dg_get_geometry(dg_solver* s, double* J, double* rst_x, double*
  * unchanged; the residual is clobbered, which is harmless because the next
  * step's first stage ignores it (a_0 = 0). */
 DG_API dg_status dg_time_stage_kernel(dg_solver* s, int32_t reps, double* ms_per_launch);
+
+/* Padding hygiene, for tests.  dg_poison_padding writes NaN
+ * into every padding word (layout padding, absent elements of the last tile) of both field
+ * buffers, the residual and the RHS scratch buffer; dg_check_padding fills counts[8] with,
+ * for each of those four buffers in that order, (padding words that are no longer NaN, real
+ * DOFs that are not finite).  A kernel that reads padding into its arithmetic, or writes
+ * outside the real DOFs, shows up as non-zero counts.  Both synchronise.  Errors: DG_ERR_ARG,
+ * DG_ERR_STATE (host-only solver, no fields), DG_ERR_CUDA. */
+DG_API dg_status dg_poison_padding(dg_solver* s);
+DG_API dg_status dg_check_padding(dg_solver* s, int64_t* counts);
 
 /* Number of kernel launches one LSERK4 step enqueues on this rank. */
 DG_API dg_status dg_launches_per_step(dg_solver* s, int32_t* n);

@@ -24,6 +24,10 @@ template <typename T, typename D>
 void tiles_to_cm(const T* src, D* dst, int64_t K, int Np, const TileLayout& L, void* st);
 template <typename T>
 void pack_traces(const T* u, T* buf, const int32_t* sidx, int64_t nfaces, int Nfp, const TileLayout& L, void* st);
+template <typename T>
+void poison_padding(T* buf, int64_t K, int Np, const TileLayout& L, void* st);
+template <typename T>
+void check_padding(const T* buf, int64_t K, int Np, const TileLayout& L, unsigned long long* counts, void* st);
 }  // namespace dg
 
 namespace {
@@ -693,6 +697,7 @@ void dg_config_default(dg_config* c) {
   c->nccl_id = nullptr;
   c->variant = DG_VARIANT_AUTO;
   c->reorder = 0;
+  c->partition = DG_PARTITION_RANGES;
   c->system = DG_SYSTEM_MAXWELL;
 }
 
@@ -715,6 +720,8 @@ dg_status dg_create(const dg_config* cfg, dg_solver** out) {
   if (cfg->variant == DG_VARIANT_TC && cfg->precision != 4)
     return fail(DG_ERR_ARG, "DG_VARIANT_TC is the FP32 tcgen05 kernel");
   if (cfg->system != DG_SYSTEM_MAXWELL && cfg->system != DG_SYSTEM_ACOUSTICS) return fail(DG_ERR_ARG, "bad system");
+  if (cfg->partition != DG_PARTITION_RANGES && cfg->partition != DG_PARTITION_RCB)
+    return fail(DG_ERR_ARG, "bad partition method");
   if (cfg->system == DG_SYSTEM_ACOUSTICS && cfg->variant != DG_VARIANT_AUTO && cfg->variant != DG_VARIANT_BASIC &&
       cfg->variant != DG_VARIANT_FFMA)
     return fail(DG_ERR_ARG, "DG_SYSTEM_ACOUSTICS runs on the BASIC and FFMA kernels only");
@@ -775,7 +782,13 @@ dg_status dg_mesh_upload(dg_solver* s, int64_t nv, const double* VX, int64_t K, 
   try {
     err = dg::build_mesh(s->ref, nv, VX, K, EToV, s->mesh);
     if (err.empty())
+    if (err.empty() && !part && s->cfg.partition == DG_PARTITION_RCB && s->cfg.nranks > 1) {
+      std::vector<int32_t> own;
+      dg::rcb_owners(s->mesh, s->cfg.nranks, own);
+      err = dg::build_partition(s->mesh, s->cfg.rank, s->cfg.nranks, own.data(), s->part, s->cfg.reorder != 0);
+    } else if (err.empty()) {
       err = dg::build_partition(s->mesh, s->cfg.rank, s->cfg.nranks, part, s->part, s->cfg.reorder != 0);
+    }
   } catch (const std::exception& e) {
     err = e.what();
   }
@@ -1022,6 +1035,7 @@ dg_status dg_get_maps(dg_solver* s, int64_t* EToE, int8_t* EToF, int64_t* vmapM,
   const auto& m = s->mesh;
   if (EToE) std::memcpy(EToE, m.EToE.data(), m.EToE.size() * sizeof(int64_t));
   if (EToF) std::memcpy(EToF, m.EToF.data(), m.EToF.size());
+  if (vmapM || vmapP) dg::build_maps(s->ref, s->mesh);
   if (vmapM) std::memcpy(vmapM, m.vmapM.data(), m.vmapM.size() * sizeof(int64_t));
   if (vmapP) std::memcpy(vmapP, m.vmapP.data(), m.vmapP.size() * sizeof(int64_t));
   return DG_OK;
@@ -1067,6 +1081,46 @@ dg_status dg_get_geometry(dg_solver* s, double* J, double* rst_x, double* nrm) {
   if (J) std::memcpy(J, m.J.data(), m.J.size() * sizeof(double));
   if (rst_x) std::memcpy(rst_x, m.rst_x.data(), m.rst_x.size() * sizeof(double));
   if (nrm) std::memcpy(nrm, m.nrm.data(), m.nrm.size() * sizeof(double));
+  return DG_OK;
+}
+
+dg_status dg_poison_padding(dg_solver* s) {
+  dg_status st = need_device(s);
+  if (st != DG_OK) return st;
+  if (!s->has_fields) return fail(DG_ERR_STATE, "dg_poison_padding before dg_fields_upload");
+  void* bufs[4] = {s->d_u[0], s->d_u[1], s->d_res, s->d_scratch};
+  for (void* b : bufs) {
+    if (s->fp64)
+      dg::poison_padding<double>(static_cast<double*>(b), s->Kl, s->Np, s->lay, s->stream);
+    else
+      dg::poison_padding<float>(static_cast<float*>(b), s->Kl, s->Np, s->lay, s->stream);
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s->stream));
+  return DG_OK;
+}
+
+dg_status dg_check_padding(dg_solver* s, int64_t* counts) {
+  dg_status st = need_device(s);
+  if (st != DG_OK) return st;
+  if (!counts) return fail(DG_ERR_ARG, "null counts");
+  if (!s->has_fields) return fail(DG_ERR_STATE, "dg_check_padding before dg_fields_upload");
+  unsigned long long* d = nullptr;
+  CK(cudaMalloc((void**)&d, 8 * sizeof(unsigned long long)));
+  CK(cudaMemsetAsync(d, 0, 8 * sizeof(unsigned long long), s->stream));
+  void* bufs[4] = {s->d_u[0], s->d_u[1], s->d_res, s->d_scratch};
+  for (int i = 0; i < 4; ++i) {
+    if (s->fp64)
+      dg::check_padding<double>(static_cast<const double*>(bufs[i]), s->Kl, s->Np, s->lay, d + 2 * i, s->stream);
+    else
+      dg::check_padding<float>(static_cast<const float*>(bufs[i]), s->Kl, s->Np, s->lay, d + 2 * i, s->stream);
+  }
+  unsigned long long h[8];
+  cudaError_t e = cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(e, "dg_check_padding");
+  for (int i = 0; i < 8; ++i) counts[i] = int64_t(h[i]);
   return DG_OK;
 }
 

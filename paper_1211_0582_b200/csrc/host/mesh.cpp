@@ -149,9 +149,8 @@ std::string build_mesh(const RefElem& ref, int64_t nv, const double* VX, int64_t
       if (m.fperm[c * Nfp + i] < 0) return "internal: face permutation";
     }
 
-  // ---- maps
-  m.vmapM.resize(4 * K * Nfp);
-  m.vmapP.resize(4 * K * Nfp);
+  // ---- orientation codes (the per-node maps are built on demand by build_maps: they are
+  // O(K Nfp) int64 per rank, 7.9 GB for C5 at N = 9, and only the parity export needs them)
   for (int64_t k = 0; k < K; ++k)
     for (int f = 0; f < 4; ++f) {
       const int64_t k2 = m.EToE[4 * k + f];
@@ -176,6 +175,21 @@ std::string build_mesh(const RefElem& ref, int64_t nv, const double* VX, int64_t
         if (code < 0) return "unmatched face nodes";
       }
       m.orient[4 * k + f] = (int8_t)code;
+    }
+  return "";
+}
+
+void build_maps(const RefElem& ref, MeshData& m) {
+  if (!m.vmapM.empty() || m.K == 0) return;
+  const int Np = ref.Np, Nfp = ref.Nfp;
+  const int64_t K = m.K;
+  m.vmapM.resize(4 * K * Nfp);
+  m.vmapP.resize(4 * K * Nfp);
+  for (int64_t k = 0; k < K; ++k)
+    for (int f = 0; f < 4; ++f) {
+      const int64_t k2 = m.EToE[4 * k + f];
+      const int f2 = m.EToF[4 * k + f];
+      const int code = m.orient[4 * k + f];
       for (int i = 0; i < Nfp; ++i) {
         const int64_t slot = (4 * k + f) * Nfp + i;
         m.vmapM[slot] = k * Np + ref.Fmask[f * Nfp + i];
@@ -185,7 +199,6 @@ std::string build_mesh(const RefElem& ref, int64_t nv, const double* VX, int64_t
           m.vmapP[slot] = k2 * Np + ref.Fmask[f2 * Nfp + m.fperm[code * Nfp + i]];
       }
     }
-  return "";
 }
 
 void node_coords(const RefElem& ref, const MeshData& m, double* x, double* y, double* z) {

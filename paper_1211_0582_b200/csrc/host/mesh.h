@@ -24,7 +24,7 @@ struct MeshData {
   std::vector<double> J;         // [K]
   std::vector<double> rst_x;     // [K][9]  rx ry rz sx sy sz tx ty tz
   std::vector<double> nrm;       // [K][4][4]  nx ny nz Fscale
-  std::vector<int64_t> vmapM;    // [K][4][Nfp]  global node id k*Np + n
+  std::vector<int64_t> vmapM;    // [K][4][Nfp]  global node id k*Np + n (built on demand: build_maps)
   std::vector<int64_t> vmapP;    // [K][4][Nfp]
   std::vector<int32_t> fperm;    // [6][Nfp]  neighbour face-node index for each orientation code
 };
@@ -33,6 +33,10 @@ struct MeshData {
 // (non-positive Jacobian, face shared by > 2 elements, unmatched face nodes, bad ids).
 std::string build_mesh(const RefElem& ref, int64_t nv, const double* VX, int64_t K,
                        const int64_t* EToV, MeshData& out);
+
+// vmapM / vmapP of the global mesh from EToE, EToF, orient and fperm (parity export only;
+// the device path uses the compressed per-face connectivity or the local gather index).
+void build_maps(const RefElem& ref, MeshData& m);
 
 // Physical node coordinates [K][Np] of element k: x = 1/2[-(1+r+s+t)va + (1+r)vb + (1+s)vc + (1+t)vd]
 void node_coords(const RefElem& ref, const MeshData& m, double* x, double* y, double* z);

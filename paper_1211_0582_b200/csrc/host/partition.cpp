@@ -44,6 +44,47 @@ void morton_sort(const MeshData& m, std::vector<int64_t>& ids, size_t b, size_t 
 }
 }  // namespace
 
+void rcb_owners(const MeshData& m, int nranks, std::vector<int32_t>& owner) {
+  const int64_t K = m.K;
+  std::vector<double> cen(static_cast<size_t>(3 * K));
+  for (int64_t k = 0; k < K; ++k)
+    for (int d = 0; d < 3; ++d) {
+      double c = 0;
+      for (int q = 0; q < 4; ++q) c += m.VX[3 * m.EToV[4 * k + q] + d];
+      cen[3 * k + d] = 0.25 * c;
+    }
+  std::vector<int64_t> ids(static_cast<size_t>(K));
+  for (int64_t k = 0; k < K; ++k) ids[k] = k;
+  owner.assign(size_t(K), 0);
+  struct Job { size_t b, e; int r0, nr; };
+  std::vector<Job> stack{{0, size_t(K), 0, nranks}};
+  while (!stack.empty()) {
+    const Job j = stack.back();
+    stack.pop_back();
+    if (j.nr == 1 || j.e - j.b <= 1) {
+      for (size_t i = j.b; i < j.e; ++i) owner[ids[i]] = j.r0;
+      continue;
+    }
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (size_t i = j.b; i < j.e; ++i)
+      for (int d = 0; d < 3; ++d) {
+        lo[d] = std::min(lo[d], cen[3 * ids[i] + d]);
+        hi[d] = std::max(hi[d], cen[3 * ids[i] + d]);
+      }
+    int ax = 0;
+    for (int d = 1; d < 3; ++d)
+      if (hi[d] - lo[d] > hi[ax] - lo[ax]) ax = d;  // largest extent; ties keep the lower axis
+    const int nl = j.nr / 2;
+    const size_t cut = j.b + size_t((j.e - j.b) * uint64_t(nl) / uint64_t(j.nr));
+    std::nth_element(ids.begin() + j.b, ids.begin() + cut, ids.begin() + j.e, [&](int64_t a, int64_t b) {
+      const double ca = cen[3 * a + ax], cb = cen[3 * b + ax];
+      return ca < cb || (ca == cb && a < b);
+    });
+    stack.push_back({j.b, cut, j.r0, nl});
+    stack.push_back({cut, j.e, j.r0 + nl, j.nr - nl});
+  }
+}
+
 std::string build_partition(const MeshData& m, int rank, int nranks, const int32_t* owner,
                             Partition& P, bool reorder) {
   const int64_t K = m.K;

@@ -47,6 +47,11 @@ struct Partition {
 std::string build_partition(const MeshData& m, int rank, int nranks, const int32_t* owner,
                             Partition& out, bool reorder = false);
 
+// Recursive coordinate bisection: owner[k] for every element, by recursively
+// splitting the element set at the rank-weighted median centroid coordinate along the axis
+// of largest extent (ties broken by element id, so every rank computes the same owners).
+void rcb_owners(const MeshData& m, int nranks, std::vector<int32_t>& owner);
+
 // Gather index of the exterior trace for every local face node (see
 // stage_params.h): L.off(k2_local, 0, n2), or ghost_base + g*6*Nfp + j, or -1
 // (PEC).  Rows are padded to ntiles*E elements (padding rows = -1).

@@ -56,6 +56,68 @@ __global__ void k_cm_to_tiles(const S* __restrict__ src, T* __restrict__ dst, in
   }
 }
 
+// Padding hygiene: is word r of a tile a real DOF (element k < K, component,
+// node n < Np) of layout L?  Mirrors the placement of k_cm_to_tiles.
+__device__ inline bool tile_word_valid(int64_t t, int64_t r, int64_t K, int Np, const TileLayout& L) {
+  const int cols = L.nc * L.E;
+  int col, n;
+  if (L.perm == 3) {
+    const int64_t q = r / L.E;
+    const int e3 = int(r - q * L.E), c3 = int(q / L.LD);
+    n = int(q - int64_t(c3) * L.LD);
+    col = c3 * L.E + e3;
+  } else if (L.perm == 4) {
+    n = int(r / cols);
+    col = int(r - int64_t(n) * cols);
+  } else if (L.perm == 2) {
+    const int chunk = int(r >> 5), q = int(r & 31), kc = L.LD >> 2;
+    col = (chunk / kc) * 8 + (q >> 2);
+    n = (chunk % kc) * 4 + (q & 3);
+  } else {
+    col = int(r / L.LD);
+    n = int(r - int64_t(col) * L.LD);
+  }
+  if (col >= cols || n >= Np) return false;
+  int e;
+  if (L.perm == 1) {
+    const int g = col / 24, q = col - 24 * g;
+    e = 4 * g + ((q & 7) >> 1);
+  } else if (L.perm == 3) {
+    e = col % L.E;
+  } else {
+    e = col / L.nc;
+  }
+  return t * L.E + e < K;
+}
+
+template <typename T>
+__global__ void k_poison_padding(T* __restrict__ buf, int64_t K, int Np, TileLayout L) {
+  const int64_t total = L.ntiles(K) * L.TS;
+  for (int64_t w = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; w < total; w += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = w / L.TS;
+    if (!tile_word_valid(t, w - t * L.TS, K, Np, L)) buf[w] = T(NAN);
+  }
+}
+
+// counts[0] += padding words that are not NaN, counts[1] += real DOFs that are not finite
+template <typename T>
+__global__ void k_check_padding(const T* __restrict__ buf, int64_t K, int Np, TileLayout L,
+                                unsigned long long* counts) {
+  const int64_t total = L.ntiles(K) * L.TS;
+  unsigned long long a = 0, b = 0;
+  for (int64_t w = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; w < total; w += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = w / L.TS;
+    const T v = buf[w];
+    if (tile_word_valid(t, w - t * L.TS, K, Np, L)) {
+      if (!isfinite(double(v))) ++b;
+    } else if (!isnan(double(v))) {
+      ++a;
+    }
+  }
+  if (a) atomicAdd(counts, a);
+  if (b) atomicAdd(counts + 1, b);
+}
+
 // device layout L -> [6][K][Np]
 template <typename T, typename D>
 __global__ void k_tiles_to_cm(const T* __restrict__ src, D* __restrict__ dst, int64_t K, int Np, TileLayout L) {
@@ -75,6 +137,19 @@ static unsigned grid_for(int64_t n) {
   if (g < 1) g = 1;
   return unsigned(g);
 }
+
+template <typename T>
+void poison_padding(T* buf, int64_t K, int Np, const TileLayout& L, void* st) {
+  k_poison_padding<T><<<grid_for(L.ntiles(K) * L.TS), 256, 0, static_cast<cudaStream_t>(st)>>>(buf, K, Np, L);
+}
+template <typename T>
+void check_padding(const T* buf, int64_t K, int Np, const TileLayout& L, unsigned long long* counts, void* st) {
+  k_check_padding<T><<<grid_for(L.ntiles(K) * L.TS), 256, 0, static_cast<cudaStream_t>(st)>>>(buf, K, Np, L, counts);
+}
+template void poison_padding<double>(double*, int64_t, int, const TileLayout&, void*);
+template void poison_padding<float>(float*, int64_t, int, const TileLayout&, void*);
+template void check_padding<double>(const double*, int64_t, int, const TileLayout&, unsigned long long*, void*);
+template void check_padding<float>(const float*, int64_t, int, const TileLayout&, unsigned long long*, void*);
 
 template <typename S, typename T>
 void cm_to_tiles(const S* src, T* dst, int64_t K, int Np, const TileLayout& L, void* st) {

@@ -25,6 +25,7 @@ DG_OK, DG_ERR_ARG, DG_ERR_ORDER, DG_ERR_MESH, DG_ERR_STATE, DG_ERR_CUDA, DG_ERR_
 (DG_VARIANT_AUTO, DG_VARIANT_BASIC, DG_VARIANT_MMA, DG_VARIANT_MMA_WS, DG_VARIANT_TC, DG_VARIANT_FUSED,
  DG_VARIANT_FFMA) = 0, 1, 2, 3, 4, 5, 6
 DG_SYSTEM_MAXWELL, DG_SYSTEM_ACOUSTICS = 0, 1
+DG_PARTITION_RANGES, DG_PARTITION_RCB = 0, 1
 STATUS_NAMES = {0: "DG_OK", 1: "DG_ERR_ARG", 2: "DG_ERR_ORDER", 3: "DG_ERR_MESH", 4: "DG_ERR_STATE",
                 5: "DG_ERR_CUDA", 6: "DG_ERR_NCCL", 7: "DG_ERR_OOM"}
 
@@ -33,7 +34,7 @@ class dg_config(C.Structure):
     _fields_ = [("order", C.c_int32), ("precision", C.c_int32), ("alpha", C.c_double),
                 ("device", C.c_int32), ("stream", C.c_void_p), ("rank", C.c_int32),
                 ("nranks", C.c_int32), ("nccl_id", C.c_void_p), ("variant", C.c_int32),
-                ("reorder", C.c_int32), ("system", C.c_int32)]
+                ("reorder", C.c_int32), ("system", C.c_int32), ("partition", C.c_int32)]
 
 
 _P = C.c_void_p
@@ -64,6 +65,8 @@ _SIGS = {
     "dg_get_reference": (C.c_int, [_P, _D, _D, _D, _D, _D, _D, _D, _D, _I32]),
     "dg_get_geometry": (C.c_int, [_P, _D, _D, _D]),
     "dg_time_stage_kernel": (C.c_int, [_P, C.c_int32, _D]),
+    "dg_poison_padding": (C.c_int, [_P]),
+    "dg_check_padding": (C.c_int, [_P, _I64]),
     "dg_launches_per_step": (C.c_int, [_P, _I32]),
     "dg_kernel_variant": (C.c_int, [_P, _I32]),
     "dg_last_error": (C.c_char_p, []),
@@ -107,13 +110,15 @@ class Solver:
     torch tensors (data_ptr)."""
 
     def __init__(self, order, precision=8, alpha=1.0, device=0, stream=None, rank=0, nranks=1,
-                 nccl_id=None, variant=DG_VARIANT_AUTO, reorder=False, system=DG_SYSTEM_MAXWELL):
+                 nccl_id=None, variant=DG_VARIANT_AUTO, reorder=False, system=DG_SYSTEM_MAXWELL,
+                 partition=0):
         cfg = dg_config()
         dg_config_default(C.byref(cfg))
         cfg.order, cfg.precision, cfg.alpha, cfg.device = order, precision, alpha, device
         cfg.stream = stream
         cfg.rank, cfg.nranks, cfg.variant, cfg.reorder = rank, nranks, variant, int(bool(reorder))
         cfg.system = system
+        cfg.partition = partition
         self.nfields = 4 if system == DG_SYSTEM_ACOUSTICS else 6
         self._io_refs = []  # host arrays borrowed by pending async copies
         self._id_buf = None
@@ -237,6 +242,16 @@ class Solver:
         ms = C.c_double()
         check(dg_time_stage_kernel(self.h, int(reps), C.byref(ms)), "dg_time_stage_kernel")
         return ms.value
+
+    def poison_padding(self):
+        """NaN into every padding word of the device field buffers (test hook)."""
+        check(dg_poison_padding(self.h), "dg_poison_padding")
+
+    def check_padding(self):
+        """[(padding words no longer NaN, real DOFs not finite)] for u0, u1, res, rhs scratch."""
+        c = np.zeros(8, np.int64)
+        check(dg_check_padding(self.h, _ptr(c, _I64)), "dg_check_padding")
+        return [tuple(int(x) for x in c[2 * i:2 * i + 2]) for i in range(4)]
 
     def kernel_variant(self):
         """The stage kernel in use (dg_variant; AUTO resolved by the library)."""

@@ -564,3 +564,30 @@ def test_pipelined_async_io_equals_synchronous(prec):
         assert np.array_equal(outs[k], ref.fields_download())
     a.close()
     ref.close()
+
+
+@pytest.mark.parametrize("prec,variant", VARIANTS, ids=VIDS)
+@pytest.mark.parametrize("N", [1, 3, 4, 8])
+def test_nan_poisoned_padding(N, prec, variant):
+    # SPEC.md:230 / SURVEY §4 item 4: every padding word of the field buffers (tile / LD padding,
+    # absent elements of the ragged last tile) is NaN; the RHS and two steps must leave the
+    # real DOFs finite and equal to the oracle, and must neither read nor overwrite the padding
+    VX, E = mesh(3, 1, 2, 3)                      # K = 162: ragged last tile for every tile size
+    st = setup("m3", VX, E, N)
+    U = di.random_fields(st.K, N, seed=0)
+    s = Solver(N, precision=prec, variant=variant)
+    s.mesh_upload(VX, E)
+    s.fields_upload(U)
+    s.poison_padding()
+    R = s.rhs()
+    assert np.isfinite(R).all()
+    assert relerr(R, oracle.rhs(st, U)) < TOL_RHS[prec]
+    dt = di.dt_rule(VX, E, N)
+    s.lserk_step(dt, 2)
+    Un = s.fields_download()
+    assert np.isfinite(Un).all()
+    assert relerr(Un, oracle.lserk4(st, U, dt, 2)) < TOL_STEP[prec]
+    for name, (pad_not_nan, bad_dofs) in zip(("u0", "u1", "res", "scratch"), s.check_padding()):
+        assert bad_dofs == 0, (name, bad_dofs)
+        assert pad_not_nan == 0, (name, pad_not_nan)
+    s.close()

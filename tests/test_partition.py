@@ -13,8 +13,8 @@ import dg_inputs as di
 from paper_1211_0582_b200.dg import Solver
 
 
-def _local(rank, P, VX, E, part=None):
-    s = Solver(2, device=-1, rank=rank, nranks=P)
+def _local(rank, P, VX, E, part=None, partition=0):
+    s = Solver(2, device=-1, rank=rank, nranks=P, partition=partition)
     s.mesh_upload(VX, E, part)
     ids = s.local_elements()
     EToE, EToF, _, _ = s.get_maps()
@@ -54,6 +54,30 @@ def test_default_partition_is_z_slabs_on_weak_scaling_mesh():
         assert zc.min() > r - 1e-12 and zc.max() < r + 1 - 1e-12   # z-slab [r, r+1)
 
 
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+def test_rcb_partition_balanced_compact_and_shared(P):
+    # recursive coordinate bisection (DG_PARTITION_RCB): every element owned once, part sizes
+    # within one element of K/P, and far fewer partition faces than a random owner map
+    VX, E = di.kuhn_box(4)
+    E, _ = di.shuffle_elements(E, 3)
+    K = E.shape[0]
+    owner = -np.ones(K, np.int64)
+    for r in range(P):
+        ids, EToE, _ = _local(r, P, VX, E, partition=1)
+        assert np.all(owner[ids] == -1)
+        owner[ids] = r
+        assert abs(len(ids) - K / P) <= 1
+    assert np.all(owner >= 0)
+    cross = int(sum(owner[k] != owner[EToE[k, f]] for k in range(K) for f in range(4)))
+    rnd = np.random.default_rng(0).integers(0, P, K)
+    cross_rnd = int(sum(rnd[k] != rnd[EToE[k, f]] for k in range(K) for f in range(4)))
+    assert cross < 0.35 * cross_rnd
+    # P = 2 on a cube: the split is the median plane of the first (x) axis
+    if P == 2:
+        xc = VX[E].mean(axis=1)[:, 0]
+        assert xc[owner == 0].max() <= xc[owner == 1].min() + 1e-12
+
+
 def _cross_faces(rank, peer, ids, EToE, EToF, part):
     """This rank's send order to `peer`: its faces toward peer sorted by the lower rank's slot."""
     out = []
@@ -67,15 +91,21 @@ def _cross_faces(rank, peer, ids, EToE, EToF, part):
     return out
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, how="random"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         VX, E = di.kuhn_box(3)
         E, _ = di.shuffle_elements(E, 4)
         K = E.shape[0]
-        part = np.random.default_rng(11).integers(0, world, K).astype(np.int32)
-        ids, EToE, EToF = _local(rank, world, VX, E, part)
+        if how == "rcb":  # the library's recursive coordinate bisection, computed by each process
+            part = np.zeros(K, np.int32)
+            for r in range(world):
+                part[_local(r, world, VX, E, partition=1)[0]] = r
+            ids, EToE, EToF = _local(rank, world, VX, E, partition=1)
+        else:
+            part = np.random.default_rng(11).integers(0, world, K).astype(np.int32)
+            ids, EToE, EToF = _local(rank, world, VX, E, part)
         peer = 1 - rank
         mine = _cross_faces(rank, peer, ids, EToE, EToF, part)
         # exchange my (my_slot, their_slot) sequence; the peer's sequence must be the mirror
@@ -102,11 +132,12 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_two_process_gloo_ghost_face_order_agrees():
+@pytest.mark.parametrize("how", ["random", "rcb"])
+def test_two_process_gloo_ghost_face_order_agrees(how):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29500 + (os.getpid() % 1000)
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    port = 29500 + (os.getpid() % 1000) + (7 if how == "rcb" else 0)
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, how)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=240) for _ in procs]
