@@ -193,8 +193,10 @@ __device__ unsigned long long g_tc_prof[16];
 __device__ float* g_tc_dbg = nullptr;  // debug dump of the generated operand G [tile][NQ][128][8]
 inline void tc_dbg_set(float* p) { cudaMemcpyToSymbol(g_tc_dbg, &p, sizeof(p)); }
 #define TC_T(v) long long v = clock64()
-#define TC_A(i, t0) \
-  do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_tc_prof[i], (unsigned long long)(clock64() - (t0))); } while (0)
+#define TC_A(i, t0)                                             \
+  do {                                                          \
+    tcp[i] += (unsigned long long)(clock64() - (t0));           \
+  } while (0)
 inline void tc_prof_read(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_tc_prof, sizeof(g_tc_prof)); }
 inline void tc_prof_reset() {
   static unsigned long long z[16] = {0};
@@ -221,6 +223,9 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
   extern __shared__ __align__(1024) unsigned char smem_tc[];
   unsigned char* smem = smem_tc;
   pdl_trigger();
+#ifdef DG_WS_PROFILE
+  unsigned long long tcp[12] = {0};  // per-thread role counters, flushed once at the end
+#endif
   float* sB = reinterpret_cast<float*>(smem + C::OFF_B);
   float* sFS = reinterpret_cast<float*>(smem + C::OFF_FS);
   float* sS = reinterpret_cast<float*>(smem + C::OFF_S);
@@ -744,6 +749,11 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
     }
     TC_A(6, tw);
   }
+#ifdef DG_WS_PROFILE
+  if (lane == 0)
+    for (int i = 0; i < 12; ++i)
+      if (tcp[i]) atomicAdd(&g_tc_prof[i], tcp[i]);
+#endif
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == C::W_MMA) {

@@ -577,7 +577,9 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
           const double ar = ap[kk], as = ap[M8 * C::LDA + kk], at = ap[2 * M8 * C::LDA + kk];
 #pragma unroll
           for (int nt = 0; nt < 3; ++nt) {
-            const double bv = bp[nt * 8 * LD + kk];
+            // node rows k >= Np are layout padding: masked, so the K padding never multiplies
+            // whatever the padding holds (NaN-poisoned padding test)
+            const double bv = (kk + 4 <= Np || kk + tig < Np) ? bp[nt * 8 * LD + kk] : 0.0;
             dmma(acc[0][nt], ar, bv);
             dmma(acc[1][nt], as, bv);
             dmma(acc[2][nt], at, bv);
@@ -599,7 +601,9 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
           const double at = __ldg(ap + size_t(2) * M8 * KV + kk);
 #pragma unroll
           for (int nt = 0; nt < 3; ++nt) {
-            const double bv = bp[nt * 8 * LD + kk];
+            // node rows k >= Np are layout padding: masked, so the K padding never multiplies
+            // whatever the padding holds (NaN-poisoned padding test)
+            const double bv = (kk + 4 <= Np || kk + tig < Np) ? bp[nt * 8 * LD + kk] : 0.0;
             dmma(acc[0][nt], ar, bv);
             dmma(acc[1][nt], as, bv);
             dmma(acc[2][nt], at, bv);

@@ -372,8 +372,9 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
         unsigned bh[3][2], bl[3][2];
 #pragma unroll
         for (int nt = 0; nt < 3; ++nt) {
-          tf32_split(bp[nt * 8 * LD + kk], bh[nt][0], bl[nt][0]);
-          tf32_split(bp[nt * 8 * LD + kk + 4], bh[nt][1], bl[nt][1]);
+          // node rows k >= Np are layout padding: masked (NaN-poisoned padding test)
+          tf32_split((kk + 4 <= Np || kk + tig < Np) ? bp[nt * 8 * LD + kk] : 0.0f, bh[nt][0], bl[nt][0]);
+          tf32_split((kk + 8 <= Np || kk + 4 + tig < Np) ? bp[nt * 8 * LD + kk + 4] : 0.0f, bh[nt][1], bl[nt][1]);
         }
 #pragma unroll
         for (int b = 0; b < 3; ++b) {

@@ -262,7 +262,81 @@ void run_canary() {
   cudaFree(dA); cudaFree(dB); cudaFree(dc);
 }
 
+// Issue-path cost: per "chunk" 3 TS MMAs (K=8) then, optionally, tcgen05.fence::after_thread_sync
+// and a tcgen05.commit to an mbarrier (as the stage kernel's MMA warp does).
+template <int N, bool FENCE, bool COMMIT>
+__global__ void __launch_bounds__(128, 1) issue_cost(int chunks, unsigned long long* cyc) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  float* sB = reinterpret_cast<float*>(sm);
+  __shared__ uint64_t bar[2];
+  __shared__ uint32_t tslot;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int w = tid; w < 2 * N * 8; w += 128) sB[w] = 1e-3f;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tslot)), "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1000000;" ::"r"(su32(&bar[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tslot;
+  if (tid == 0) {
+    const long long t0 = clock64();
+    constexpr uint32_t id = idesc_tf32(128, N);
+    for (int c = 0; c < chunks; ++c) {
+      if (FENCE) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t ta = tmem + 256 + 16 * (c & 7);
+      const uint64_t db = desc(sB), dbl = desc(sB + N * 8);
+      const uint32_t acc = c ? 1u : 0u;
+      asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n"
+                   ::"r"(tmem), "r"(ta), "l"(db), "r"(id), "r"(acc));
+      asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n"
+                   ::"r"(tmem), "r"(ta + 8), "l"(db), "r"(id), "r"(1u));
+      asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n"
+                   ::"r"(tmem), "r"(ta), "l"(dbl), "r"(id), "r"(1u));
+      if (COMMIT)
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar[1]))
+                     : "memory");
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar[0]))
+                 : "memory");
+    asm volatile("{\n.reg .pred P1;\nW3:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n@!P1 bra W3;\n}\n" ::"r"(su32(&bar[0])));
+    if (blockIdx.x == 0) *cyc = clock64() - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+}
+
+template <int N, bool FENCE, bool COMMIT>
+void run_issue() {
+  unsigned long long* dc;
+  cudaMalloc(&dc, 8);
+  cudaFuncSetAttribute(issue_cost<N, FENCE, COMMIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  const int chunks = 4000;
+  issue_cost<N, FENCE, COMMIT><<<148, 128, 64 * 1024>>>(chunks, dc);
+  cudaError_t e = cudaDeviceSynchronize();
+  unsigned long long c = 0;
+  cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
+  printf("{\"issue_N\": %d, \"fence\": %d, \"commit\": %d, \"err\": \"%s\", \"cycles_per_chunk_of_3_mma\": %.1f}\n", N, FENCE,
+         COMMIT, cudaGetErrorString(e), double(c) / chunks);
+  cudaFree(dc);
+}
+
 int main() {
+  run_issue<48, false, false>();
+  run_issue<48, true, false>();
+  run_issue<48, false, true>();
+  run_issue<48, true, true>();
+  run_issue<224, false, false>();
+  run_issue<224, true, true>();
+  return 0;
   run_canary<48>();
   run_canary<80>();
   run_canary<96>();
