@@ -111,7 +111,7 @@ struct TcCfg {
                                (NTAB * 2 + 15) / 16 * 16 + 1024;
   static constexpr bool OP_RES = FIXED + al1k(NQ * OPC * 4) <= 226 * 1024;  // operators resident in smem
   static constexpr int RB_MAX = (226 * 1024 - FIXED) / (OPC * 4);
-  static constexpr int RA = RA_T;
+  static constexpr int RA = RA_T & ~1;  // even: slots are released in pairs
   static constexpr int RB = OP_RES ? NQ : (RB_MAX < DG_TC_RB ? RB_MAX : DG_TC_RB);
   // 16 warps: 4 per SMSP, so every thread can have 128 registers
   static constexpr int W_LD = 4, W_MMA = 5, W_VG0 = 6, W_FG0 = 10;
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
     }
     for (int i = 0; i < RA; ++i) {
       mbar_init(a_full + i, 4);
-      mbar_init(a_empty + i, 1);
+      mbar_init(a_empty + i, 1);  // (only the first RA / 2: one per slot pair)
     }
     for (int i = 0; i < LF; ++i) {
       mbar_init(f_full + i, C::PW);
@@ -439,6 +439,11 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
     // ============================ MMA issuer ============================
     if (lane == 0) {
       constexpr uint32_t idesc = tc_idesc(128, NP16);
+      // descriptor of operator slot/chunk 0; other chunks differ only in the start-address
+      // field (bits 0..13, address >> 4), so they are db0 + (byte offset >> 4)
+      const uint64_t db0 = tc_desc(sB);
+      constexpr uint64_t DLO = uint64_t(8 * NP16 * 4) >> 4;  // hi -> lo half of a chunk
+      constexpr uint64_t DCH = uint64_t(C::OPC * 4) >> 4;    // next chunk / slot
       if constexpr (C::OP_RES) tc_wait(b_full, 0);
       int ga = 0;
       for (int j = 0; j < J; ++j) {
@@ -450,25 +455,26 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
           TC_T(t0);
           tc_wait(a_full + slot, unsigned(ga / RA) & 1);
           TC_A(7, t0);
-          const float* B;
+          uint64_t db;
           int b = 0;
           if constexpr (C::OP_RES) {
-            B = sB + s * C::OPC;
+            db = db0 + uint64_t(s) * DCH;
           } else {
             const int g = j * NQ + s;
             b = g % RB;
             TC_T(t2);
             tc_wait(b_full + b, unsigned(g / RB) & 1);
             TC_A(9, t2);
-            B = sB + b * C::OPC;
+            db = db0 + uint64_t(b) * DCH;
           }
           TC_T(t1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t ta = tmem + uint32_t(C::a_col(slot));  // G at ta, G_lo at ta + 8
-          tc_mma_ts(d, ta, tc_desc(B), idesc, s > 0 ? 1u : 0u);      // G . Op
-          tc_mma_ts(d, ta + 8, tc_desc(B), idesc, 1u);              // G_lo . Op
-          tc_mma_ts(d, ta, tc_desc(B + 8 * NP16), idesc, 1u);       // G . Op_lo
-          tc_commit(a_empty + slot);                                // frees the TMEM operand slot
+          tc_mma_ts(d, ta, db, idesc, s > 0 ? 1u : 0u);              // G . Op
+          tc_mma_ts(d, ta + 8, db, idesc, 1u);                      // G_lo . Op
+          tc_mma_ts(d, ta, db + DLO, idesc, 1u);                    // G . Op_lo
+          // frees the TMEM operand slots in pairs (one commit per two chunks: ~45 cycles each)
+          if (slot & 1) tc_commit(a_empty + (slot >> 1));
           if constexpr (!C::OP_RES) tc_commit(b_empty + b);         // frees the operator slot
           if (s == NQ - 1) tc_commit(acc_full + a);                 // accumulator complete
           TC_A(10, t1);
@@ -575,7 +581,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
         for (int bq = 0; bq < C::WB; ++bq) {
           if (bq < nb) {
             const int slot = (ga + bq) % RA;
-            tc_wait(a_empty + slot, (unsigned((ga + bq) / RA) & 1) ^ 1);
+            tc_wait(a_empty + (slot >> 1), (unsigned((ga + bq) / RA) & 1) ^ 1);  // the slot pair's release
             // orders this store after the MMAs that read the slot (their commit completed the wait)
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #ifdef DG_WS_PROFILE
