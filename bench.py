@@ -228,7 +228,8 @@ def run_dg(args, N, prec, rank, world, local, dist, stream, flush, nccl_id, peak
                nccl_id=nccl_id, variant=args.variant, reorder=args.reorder, system=system)
     s.mesh_upload(VX, E)
     Kl = s.K_local
-    U0 = di.random_fields(K_total, N, seed=0, nfields=nf)[:, s.local_elements()]
+    # this rank's elements only (per-rank host memory O(K_local)); identical to the global draw
+    U0 = di.random_fields_local(s.local_elements(), K_total, N, seed=0, nfields=nf)
     s.fields_upload(U0)
     dt = di.dt_rule(VX, E, N)
     with torch.cuda.stream(stream):

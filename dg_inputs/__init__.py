@@ -139,6 +139,34 @@ def random_fields(K: int, N: int, seed: int = 0, nfields: int = 6):
     return rng.uniform(-1.0, 1.0, size=(nfields, K, np_of(N)))
 
 
+def random_fields_local(ids, K: int, N: int, seed: int = 0, nfields: int = 6):
+    """random_fields(K, N, seed, nfields)[:, ids] without materialising the global array:
+    the PCG64 stream behind rng.uniform is one 64-bit draw per value, so the values of global
+    element k, field c are draws (c K + k) Np .. + Np, reached with bit_generator.advance
+    (per-rank host memory O(K_local), for multi-GPU runs)."""
+    Np = np_of(N)
+    ids = np.asarray(ids, dtype=np.int64)
+    out = np.empty((nfields, ids.size, Np))
+    if ids.size == 0:
+        return out
+    order = np.argsort(ids, kind="stable")
+    for c in range(nfields):
+        bg = np.random.PCG64(seed)
+        pos = 0
+        i = 0
+        while i < ids.size:  # runs of consecutive global ids in one draw
+            j = i
+            while j + 1 < ids.size and ids[order[j + 1]] == ids[order[j]] + 1:
+                j += 1
+            start = (c * K + int(ids[order[i]])) * Np
+            bg.advance(start - pos)
+            vals = np.random.Generator(bg).uniform(-1.0, 1.0, size=(j - i + 1) * Np).reshape(j - i + 1, Np)
+            out[c, order[i:j + 1]] = vals
+            pos = start + (j - i + 1) * Np
+            i = j + 1
+    return out
+
+
 def cavity_mode_101(x, y, z, t=0.0):
     """Exact PEC eigenmode (1,0,1) of the unit cube, omega = pi*sqrt(2).
 

@@ -40,3 +40,15 @@ def test_roofline_bound_follows_kernel_and_ridge():
     assert bench.roofline(9, 8, K, 1.7, peaks, 6)["peak"] == 34.17
     # kernel families of resolved variants
     assert [bench.ws_kind(4, 8, v) for v in (1, 2, 3, 4, 5, 6)] == ["basic", "mma", "ws", "tc", "ws", "ffma"]
+
+
+def test_random_fields_local_equals_global_draw():
+    # bench.py draws each rank's fields by global element id without the global array
+    # (per-rank host memory O(K_local)); the values must be exactly the global draw's
+    import numpy as np
+
+    import dg_inputs as di
+    K, N = 777, 4
+    full = di.random_fields(K, N, seed=3, nfields=6)
+    for ids in (np.arange(K), np.arange(200, 389), np.random.default_rng(5).permutation(K)[:301], np.array([], int)):
+        assert np.array_equal(di.random_fields_local(ids, K, N, seed=3, nfields=6), full[:, ids])
