@@ -77,6 +77,10 @@ NcclApi& nccl() {
   return api;
 }
 
+// SMs the interior-range launch leaves to the concurrent NCCL send/recv kernels (one channel
+// per peer direction on a slab partition; RCB has up to 3 peers per cut level)
+constexpr int kNcclSmReserve = 4;
+
 // LSERK4 coefficients: Carpenter & Kennedy (5,4), as tabulated in HW (reading R5)
 const double kRkA[5] = {0.0, -567301805773.0 / 1357537059087.0, -2404267990393.0 / 2016746695238.0,
                         -3550918686646.0 / 2091501179385.0, -1275806237668.0 / 842570457699.0};
@@ -272,7 +276,11 @@ dg_status enqueue_stage(dg_solver* s, int stage, double dt, int cur) {
     if (st != DG_OK) return st;
     CK(cudaEventRecord(s->ev_join, s->comm));
     const int64_t split = (s->part.K_interior / s->lay.E) * s->lay.E;  // tile-aligned
-    launch_stage<T>(s, p, 1, 0, split, s->stream);
+    // the interior range runs while the NCCL send/recv kernels move the traces: leave them SMs
+    // (a persistent grid of every SM would otherwise hold the exchange until it drains)
+    dg::StageParams<T> pi = p;
+    pi.sm_reserve = s->loopback ? 0 : kNcclSmReserve;
+    launch_stage<T>(s, pi, 1, 0, split, s->stream);
     CK(cudaStreamWaitEvent(s->stream, s->ev_join, 0));
     launch_stage<T>(s, p, 1, split, s->Kl, s->stream);
   } else {

@@ -541,7 +541,8 @@ void launch_stage_ffma_sys(const StageParams<T>& p, const T* opsT, int mode, cud
   if (p.K <= 0) return;
   const int64_t t0 = p.k_begin / C::E;
   const int64_t tc = (p.k_begin + p.K + C::E - 1) / C::E - t0;
-  const unsigned grid = unsigned(tc < sms ? tc : sms);
+  const int cap = sms - p.sm_reserve > 1 ? sms - p.sm_reserve : 1;  // SMs left to concurrent NCCL kernels
+  const unsigned grid = unsigned(tc < cap ? tc : cap);
   if (mode == 1)
     launch_pdl(true, dg_stage_ffma<T, N, true, SYS>, grid, C::NT, C::SMEM_BYTES, st, p, opsT, t0, tc);
   else

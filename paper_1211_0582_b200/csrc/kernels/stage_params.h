@@ -106,6 +106,7 @@ struct StageParams {
   int64_t ghost_base;  // offset of the ghost-trace region
   T rk_a, rk_b, dt, alpha;
   int first_stage;     // 1: a_s == 0, do not read res
+  int sm_reserve;      // persistent kernels leave this many SMs free (interior range overlapping an NCCL exchange)
   int system;          // dg_system: 0 Maxwell, 1 acoustics (BASIC kernel)
 };
 

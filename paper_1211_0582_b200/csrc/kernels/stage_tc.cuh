@@ -779,7 +779,8 @@ void launch_stage_tc(const StageParams<float>& p, const float* ops, int mode, cu
   if (p.K <= 0) return;
   const int64_t t0 = p.k_begin / C::E;
   const int64_t tc = (p.k_begin + p.K + C::E - 1) / C::E - t0;
-  const unsigned grid = unsigned(tc < sms ? tc : sms);
+  const int cap = sms - p.sm_reserve > 1 ? sms - p.sm_reserve : 1;  // SMs left to concurrent NCCL kernels
+  const unsigned grid = unsigned(tc < cap ? tc : cap);
   if (mode == 1)
     launch_pdl(true, dg_stage_tc<N, true>, grid, C::NT, C::SMEM_BYTES, st, p, ops, t0, tc);
   else

@@ -722,7 +722,8 @@ void launch_stage_ws(const StageParams<double>& p, const double* opsA, int mode,
   // element range [k_begin, k_begin+K) must start on a tile boundary
   const int64_t t0 = p.k_begin / C::E;
   const int64_t tc = (p.k_begin + p.K + C::E - 1) / C::E - t0;
-  const unsigned grid = unsigned(tc < sms ? tc : sms);
+  const int cap = sms - p.sm_reserve > 1 ? sms - p.sm_reserve : 1;  // SMs left to concurrent NCCL kernels
+  const unsigned grid = unsigned(tc < cap ? tc : cap);
   const FusedParams<double> nf{};
   if (mode == 1)
     launch_pdl(true, dg_stage_ws<N, true, false>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc, nf);
