@@ -80,10 +80,8 @@ typedef enum {
                             the generated operand (written to tensor memory), upwind flux as
                             the lift operand, TMEM accumulators, LSERK update in the epilogue
                             (5th-generation tensor cores; stage_tc.cuh) */
-  DG_VARIANT_FUSED = 5,  /* FP64, single rank: the MMA_WS kernel running all 5 x nsteps stages of a
-                            dg_lserk_step call in ONE persistent launch, tiles ordered by per-tile
-                            completion counters instead of kernel boundaries.  Bitwise equal to
-                            MMA_WS; measured slower on B200, hence not AUTO */
+  DG_VARIANT_FUSED = 5,  /* withdrawn in round 2 (dg_create returns DG_ERR_ARG): the stage-fused
+                            WS launch was slower than per-stage launches */
   DG_VARIANT_FFMA = 6    /* the warp-specialized TMA pipeline with both contractions as
                             register-tiled FFMA (FP32) / DFMA (FP64), no tensor cores: the
                             SIMT side of the TF32-or-FFMA and DMMA-or-DFMA comparisons

@@ -723,8 +723,8 @@ dg_status dg_create(const dg_config* cfg, dg_solver** out) {
   if (cfg->precision != 4 && cfg->precision != 8) return fail(DG_ERR_ARG, "precision must be 4 or 8");
   if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks) return fail(DG_ERR_ARG, "bad rank/nranks");
   if (cfg->variant < 0 || cfg->variant > 6) return fail(DG_ERR_ARG, "bad variant");
-  if (cfg->variant == DG_VARIANT_FUSED && (cfg->precision != 8 || cfg->nranks != 1))
-    return fail(DG_ERR_ARG, "DG_VARIANT_FUSED is the single-rank FP64 stage-fused WS kernel");
+  if (cfg->variant == DG_VARIANT_FUSED)
+    return fail(DG_ERR_ARG, "DG_VARIANT_FUSED was withdrawn (slower than the per-stage WS launches; DESIGN.md §8)");
   if (cfg->variant == DG_VARIANT_TC && cfg->precision != 4)
     return fail(DG_ERR_ARG, "DG_VARIANT_TC is the FP32 tcgen05 kernel");
   if (cfg->system != DG_SYSTEM_MAXWELL && cfg->system != DG_SYSTEM_ACOUSTICS) return fail(DG_ERR_ARG, "bad system");

@@ -716,7 +716,6 @@ void launch_stage_ws(const StageParams<double>& p, const double* opsA, int mode,
   const int sms = sms_for_device(pd, [] {
       cudaFuncSetAttribute(dg_stage_ws<N, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
       cudaFuncSetAttribute(dg_stage_ws<N, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
-      cudaFuncSetAttribute(dg_stage_ws<N, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
   });
   if (p.K <= 0) return;
   // element range [k_begin, k_begin+K) must start on a tile boundary

@@ -58,7 +58,7 @@ def test_argument_errors():
         assert e.value.status == dg.DG_ERR_ARG
     s = Solver(3, device=-1, system=dg.DG_SYSTEM_ACOUSTICS)
     assert s.nfields == 4
-    for kw in (dict(precision=4), dict(rank=0, nranks=2)):  # fused: single-rank FP64 only
+    for kw in (dict(precision=4), dict(precision=8), dict(rank=0, nranks=2)):  # FUSED: withdrawn in round 2
         with pytest.raises(DGError) as e:
             Solver(3, device=-1, variant=dg.DG_VARIANT_FUSED, **kw)
         assert e.value.status == dg.DG_ERR_ARG
@@ -222,6 +222,3 @@ def test_kernel_variant_auto_resolution():
         s = Solver(3, precision=8, device=-1, variant=v)
         assert s.kernel_variant() == v
         s.close()
-    s = Solver(3, precision=8, device=-1, variant=dg.DG_VARIANT_FUSED)
-    assert s.kernel_variant() == dg.DG_VARIANT_FUSED
-    s.close()

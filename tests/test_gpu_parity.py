@@ -496,46 +496,6 @@ def test_acoustics_convergence_rigid_wall_mode(N):
     assert rates[-1] >= N + 0.5, (errs, rates)
 
 
-# ------------------------------------------------------------------ stage-fused launches
-@pytest.mark.parametrize("N", range(1, 10))
-@pytest.mark.parametrize("n,sh", [(6, 51), (2, 52), (15, None)], ids=["shuffled6", "tiny2", "c2"])
-def test_stage_fused_bitwise_equal_to_per_stage(N, n, sh):
-    # DG_VARIANT_FUSED (single-rank FP64) runs all stages of a dg_lserk_step call in one
-    # launch with per-tile dependency counters; MMA_WS launches one kernel per stage with
-    # the same arithmetic, so the fields must agree bit for bit.  Shuffled: every tile
-    # depends on far-away tiles; tiny: fewer tiles than ring slots; c2: the bench mesh.
-    if n == 15 and N not in (1, 4, 9):
-        pytest.skip("c2 size: N = 1, 4, 9")
-    VX, E = di.kuhn_box(n)
-    if sh is not None:
-        E, _ = di.shuffle_elements(E, sh)
-        E = di.rotate_local_vertices(E, sh + 1)
-    U0 = di.random_fields(E.shape[0], N, seed=7)
-    dt = di.dt_rule(VX, E, N)
-    a = Solver(N, variant=5)
-    a.mesh_upload(VX, E)
-    a.fields_upload(U0)
-    assert a.launches_per_step() == 1                     # fused
-    for k in (2, 1, 3):
-        a.lserk_step(dt, k)
-    Ua = a.fields_download()
-    Ra = a.rhs()
-    a.fields_upload(U0)                                  # re-upload resets the counters
-    a.lserk_step(dt, 6)
-    Ua2 = a.fields_download()
-    a.close()
-    b = Solver(N, variant=3)
-    b.mesh_upload(VX, E)
-    b.fields_upload(U0)
-    assert b.launches_per_step() == 5
-    b.lserk_step(dt, 6)                                  # per-stage launches
-    Ub = b.fields_download()
-    Rb = b.rhs()
-    b.close()
-    assert np.array_equal(Ua, Ub) and np.array_equal(Ua2, Ub) and np.array_equal(Ra, Rb)
-    if n == 6 and N <= 4:
-        st = setup("fz6", VX, E, N)
-        assert relerr(Ua, oracle.lserk4(st, U0, dt, 6)) < 1e-12
 
 
 # ------------------------------------------------------------------ pipelined host I/O

@@ -12,7 +12,7 @@ import numpy as np  # noqa: E402
 import dg_inputs as di  # noqa: E402
 from paper_1211_0582_b200.dg import Solver  # noqa: E402
 
-CASES = [(8, 1, 3), (8, 2, 3), (8, 3, 3), (8, 5, 3), (8, 6, 3), (4, 1, 3), (4, 3, 3), (4, 4, 3), (4, 4, 8), (4, 6, 3)]
+CASES = [(8, 1, 3), (8, 2, 3), (8, 3, 3), (8, 6, 3), (4, 1, 3), (4, 3, 3), (4, 4, 3), (4, 4, 8), (4, 6, 3)]
 only = sys.argv[1] if len(sys.argv) > 1 else ""
 VX, E = di.kuhn_box(2)
 for prec, var, N in CASES:
