@@ -111,7 +111,7 @@ typedef struct {
                            process and are stepped together by dg_group_lserk_step */
   int32_t variant;      /* dg_variant */
   int32_t reorder;      /* 1: renumber this rank's elements along a Morton curve of their
-                           centroids (within the interior and partition-boundary groups) for
+                           centroids (within the partition-boundary and interior groups) for
                            gather locality and intra-tile faces; dg_local_elements reports the
                            storage order.  0 (default): ascending global id within each group */
   int32_t system;       /* dg_system (default DG_SYSTEM_MAXWELL) */
@@ -144,7 +144,9 @@ DG_API dg_status dg_create(const dg_config* cfg, dg_solver** out);
 DG_API dg_status dg_mesh_upload(dg_solver* s, int64_t nv, const double* VX, int64_t K,
                          const int64_t* EToV, const int32_t* part);
 
-/* Number of elements this rank owns and (optional) their global ids, ascending. */
+/* Number of elements this rank owns and (optional) their global ids in storage order: the
+ * partition-boundary elements (a face on another rank) first, then the interior ones, each
+ * group ascending (or Morton-ordered with reorder = 1). */
 DG_API dg_status dg_local_elements(dg_solver* s, int64_t* K_local, int64_t* global_ids);
 
 /* Sizes: Np, Nfp, local and global element counts (any may be NULL). */
@@ -161,18 +163,22 @@ DG_API dg_status dg_rhs(dg_solver* s, double* rhs);
 DG_API dg_status dg_rhs_device(dg_solver* s, void* rhs_dev);
 
 /* Advance nsteps >= 0 LSERK4 steps of size dt (5 stages each; asynchronous,
- * graph-launched).  With nranks > 1 each stage exchanges partition-face traces
- * through NCCL.  Loopback solvers return DG_ERR_STATE (use dg_group_lserk_step). */
+ * graph-launched).  With nranks > 1 every stage is ONE launch over the local tiles,
+ * partition-boundary tiles first; once those are written (a counter the comm stream
+ * waits for with cuStreamWaitValue32 — no kernel waits on anything) the comm stream
+ * packs their face traces and exchanges them through NCCL send/recv into the ghost
+ * region the NEXT stage reads, beside the interior tiles (DESIGN.md
+ * §10).  The first step after a field upload primes the ghosts with one exchange.
+ * Loopback solvers return DG_ERR_STATE (use dg_group_lserk_step). */
 DG_API dg_status dg_lserk_step(dg_solver* s, double dt, int32_t nsteps);
 
 /* Advance a group of loopback partition solvers (same mesh, order, precision and
  * variant; group[i] may be given in any order but must cover ranks 0..n-1 once)
- * by nsteps LSERK4 steps in lockstep.  Per stage each rank packs its partition-
- * face traces, the records are copied device-to-device into the peers' ghost
- * regions (the NCCL path's data movement, without NCCL), and
- * every rank runs its interior range concurrently with the copies, then its
- * partition-boundary range.  Results are bitwise identical to one solver on the
- * whole mesh (reading R15).  Asynchronous.  Errors: DG_ERR_ARG,
+ * by nsteps LSERK4 steps in lockstep.  The NCCL path's stage structure (one launch,
+ * boundary tiles first, boundary signal, pack beside the interior tiles) with the
+ * records copied device-to-device into the peers' ghost regions instead of
+ * ncclSend/Recv.  Results are bitwise identical to one solver
+ * on the whole mesh (reading R15).  Asynchronous.  Errors: DG_ERR_ARG,
  * DG_ERR_STATE (missing fields), DG_ERR_CUDA. */
 DG_API dg_status dg_group_lserk_step(dg_solver* const* group, int32_t n, double dt, int32_t nsteps);
 
@@ -232,12 +238,12 @@ DG_API dg_status dg_time_stage_kernel(dg_solver* s, int32_t reps, double* ms_per
 DG_API dg_status dg_poison_padding(dg_solver* s);
 DG_API dg_status dg_check_padding(dg_solver* s, int64_t* counts);
 
-/* Number of kernel launches one LSERK4 step enqueues on this rank. */
+/* Number of kernel launches one LSERK4 step enqueues on this rank (5 stage kernels, plus 5
+ * pack kernels with partition faces). */
 DG_API dg_status dg_launches_per_step(dg_solver* s, int32_t* n);
 
 /* The stage kernel this solver runs (dg_variant; DG_VARIANT_AUTO resolved at dg_create to the
- * measured-best kernel for its precision, order and system; DG_VARIANT_FUSED reported as
- * itself).  Valid for host-only solvers too.  DG_ERR_ARG on null pointers. */
+ * measured-best kernel for its precision, order and system).  Valid for host-only solvers too.  DG_ERR_ARG on null pointers. */
 DG_API dg_status dg_kernel_variant(dg_solver* s, int32_t* variant);
 
 /* Thread-local description of the last error ("" if none). */

@@ -1,4 +1,5 @@
 // C-ABI implementation of libdg (see include/dg.h for the contract).
+#include <cuda.h>  // CUstream / CUdeviceptr of the stream memory operations (entry points resolved at run time)
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
@@ -77,9 +78,36 @@ NcclApi& nccl() {
   return api;
 }
 
-// SMs the interior-range launch leaves to the concurrent NCCL send/recv kernels (one channel
-// per peer direction on a slab partition; RCB has up to 3 peers per cut level)
+// SMs a multi-rank stage launch leaves to the concurrent pack + NCCL send/recv kernels of the
+// trace exchange (one channel per peer direction on a slab partition; RCB has up to 3 peers per
+// cut level).  Nothing waits for them inside a kernel: without free SMs they would only start later.
 constexpr int kNcclSmReserve = 4;
+
+// Stream memory operations (driver API, resolved through the runtime so libdg needs no -lcuda):
+// the comm stream waits for the stage kernel's boundary-tile counter (kernels/stage_ws.cuh
+// signal_boundary) and resets it.  A front-end wait: no SM is held, no kernel spins.
+struct MemOps {
+  CUresult (*wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+  CUresult (*write32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+  bool ok = false;
+};
+MemOps& memops() {
+  static MemOps m = [] {
+    MemOps a;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &f, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      a.wait32 = reinterpret_cast<decltype(a.wait32)>(f);
+    f = nullptr;
+    if (cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", &f, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      a.write32 = reinterpret_cast<decltype(a.write32)>(f);
+    a.ok = a.wait32 && a.write32;
+    return a;
+  }();
+  return m;
+}
 
 // LSERK4 coefficients: Carpenter & Kennedy (5,4), as tabulated in HW (reading R5)
 const double kRkA[5] = {0.0, -567301805773.0 / 1357537059087.0, -2404267990393.0 / 2016746695238.0,
@@ -116,13 +144,6 @@ struct dg_solver {
   int16_t* d_fmask = nullptr;
   void* d_send = nullptr;      // [n_ghost][nc][Nfp]
   int32_t* d_sidx = nullptr;   // [n_ghost][Nfp] element-node offsets for packing
-  // stage-fused launches (single rank, FP64 MMA_WS): per-tile completed-stage counters and
-  // the tile dependency lists (kernels/stage_params.h FusedParams)
-  bool fused = false;
-  unsigned* d_flags = nullptr;
-  int32_t* d_nbr_off = nullptr;
-  int32_t* d_nbr = nullptr;
-  unsigned stage_count = 0;    // stages completed since the last field upload
   cudaStream_t stream = nullptr, comm = nullptr;
   // pipelined host I/O (dg_fields_upload_async / dg_fields_download_async): copy streams,
   // double-buffered FP64 staging, and the events that order them with the compute stream
@@ -134,6 +155,13 @@ struct dg_solver {
   bool own_stream = false;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
   cudaEvent_t ev_packed = nullptr, ev_copied = nullptr;  // loopback transport
+  cudaEvent_t ev_done = nullptr;  // stage kernel complete (variants without the boundary signal)
+  // boundary-first multi-rank stages: boundary tiles [0, nbt) of the local order;
+  // d_bsig counts the boundary tiles a stage has written; ghosts_valid: the ghost region of
+  // d_u[cur] holds the current partition-face traces (false after a field upload)
+  unsigned* d_bsig = nullptr;
+  int64_t nbt = 0;
+  bool ghosts_valid = false;
   bool loopback = false;  // nranks > 1 without NCCL: stepped only by dg_group_lserk_step
   ncclComm_t ncomm = nullptr;
   int cur = 0;
@@ -175,15 +203,14 @@ void release_device(dg_solver* s) {
   free_dev(s->d_ops_pad);
   p = s->d_fmask; free_dev(p); s->d_fmask = nullptr;
   free_dev(s->d_send);
+  p = s->d_bsig; free_dev(p); s->d_bsig = nullptr;
+  s->nbt = 0;
+  s->ghosts_valid = false;
   p = s->d_sidx; free_dev(p); s->d_sidx = nullptr;
-  p = s->d_flags; free_dev(p); s->d_flags = nullptr;
   for (int i = 0; i < 2; ++i) {
     p = s->d_in[i]; free_dev(p); s->d_in[i] = nullptr;
     p = s->d_out[i]; free_dev(p); s->d_out[i] = nullptr;
   }
-  p = s->d_nbr_off; free_dev(p); s->d_nbr_off = nullptr;
-  p = s->d_nbr; free_dev(p); s->d_nbr = nullptr;
-  s->fused = false;
 }
 
 
@@ -235,13 +262,11 @@ void launch_stage(dg_solver* s, dg::StageParams<T> p, int mode, int64_t k0, int6
   L(p, mode, s->variant, st);
 }
 
-// Exchange partition-face traces of u (multi-rank): pack on the comm stream,
-// grouped ncclSend/ncclRecv into u's ghost region.
+// Send/receive the packed partition-face traces (multi-rank NCCL path): grouped
+// ncclSend/ncclRecv per peer on the comm stream, received straight into u's ghost region.
 template <typename T>
-dg_status enqueue_exchange(dg_solver* s, T* u) {
+dg_status nccl_exchange(dg_solver* s, T* u) {
   const auto& P = s->part;
-  if (P.n_ghost_faces == 0) return DG_OK;
-  dg::pack_traces<T>(u, static_cast<T*>(s->d_send), s->d_sidx, P.n_ghost_faces, s->Nfp, s->lay, s->comm);
   NcclApi& n = nccl();
   const size_t rec = size_t(s->nc) * s->Nfp;
   const int dtype = sizeof(T) == 8 ? ncclFloat64_ : ncclFloat32_;
@@ -257,36 +282,82 @@ dg_status enqueue_exchange(dg_solver* s, T* u) {
   return DG_OK;
 }
 
-// One LSERK stage s: u[cur] -> u[cur^1]; with ghosts: interior range overlaps the exchange.
+// Whether the solver's stage kernel signals its boundary tiles (kernels/stage_ws.cuh
+// signal_boundary): the warp-specialized kernels do; BASIC and MMA do not, and for them the
+// exchange starts after the whole stage kernel.
+bool signals_boundary(const dg_solver* s) {
+  return memops().ok && (s->variant == DG_VARIANT_MMA_WS || s->variant == DG_VARIANT_TC || s->variant == DG_VARIANT_FFMA);
+}
+
+// Blocking-order exchange of u's traces before the next launch (priming after a field upload,
+// and the RHS path): fork -> pack + send/recv on the comm stream -> join.
+template <typename T>
+dg_status exchange_now(dg_solver* s, T* u) {
+  CK(cudaEventRecord(s->ev_fork, s->stream));
+  CK(cudaStreamWaitEvent(s->comm, s->ev_fork, 0));
+  dg::pack_traces<T>(u, static_cast<T*>(s->d_send), s->d_sidx, s->part.n_ghost_faces, s->Nfp, s->lay, s->comm);
+  dg_status st = nccl_exchange<T>(s, u);
+  if (st != DG_OK) return st;
+  CK(cudaEventRecord(s->ev_join, s->comm));
+  CK(cudaStreamWaitEvent(s->stream, s->ev_join, 0));
+  return DG_OK;
+}
+
+// The comm-stream side of a boundary-first stage, up to the pack of u_out: wait until the
+// stage kernel has written its boundary tiles (counter = nbt; the counter is then reset for
+// the next stage), or — for kernels without the signal — until it completed.
+dg_status await_boundary(dg_solver* s) {
+  if (signals_boundary(s)) {
+    MemOps& mo = memops();
+    const CUdeviceptr sig = CUdeviceptr(reinterpret_cast<uintptr_t>(s->d_bsig));
+    if (mo.wait32(CUstream(s->comm), sig, cuuint32_t(s->nbt), CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS ||
+        mo.write32(CUstream(s->comm), sig, 0u, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+      return fail(DG_ERR_CUDA, "cuStreamWaitValue32 / cuStreamWriteValue32 failed");
+  } else {
+    CK(cudaStreamWaitEvent(s->comm, s->ev_done, 0));
+  }
+  return DG_OK;
+}
+
+// One LSERK stage: u[cur] -> u[cur^1], as ONE launch over all local tiles (boundary tiles
+// first).  Multi-rank: the ghost region of u[cur] is already valid (previous stage's
+// exchange, or exchange_now); while the interior tiles run, the comm stream packs the
+// boundary elements' u_out and exchanges them into u[cur^1]'s ghost region for the next
+// stage, which waits for it (ev_join).  DESIGN.md §10.
 template <typename T>
 dg_status enqueue_stage(dg_solver* s, int stage, double dt, int cur) {
   dg::StageParams<T> p = base_params<T>(s);
   T* uin = static_cast<T*>(s->d_u[cur]);
+  T* uout = static_cast<T*>(s->d_u[cur ^ 1]);
   p.u_in = uin;
-  p.u_out = static_cast<T*>(s->d_u[cur ^ 1]);
+  p.u_out = uout;
   p.res = static_cast<T*>(s->d_res);
   p.rk_a = T(kRkA[stage]);
   p.rk_b = T(kRkB[stage]);
   p.dt = T(dt);
   p.first_stage = stage == 0 ? 1 : 0;
-  if (s->part.n_ghost_faces > 0) {
-    CK(cudaEventRecord(s->ev_fork, s->stream));
-    CK(cudaStreamWaitEvent(s->comm, s->ev_fork, 0));
-    dg_status st = enqueue_exchange<T>(s, uin);
-    if (st != DG_OK) return st;
-    CK(cudaEventRecord(s->ev_join, s->comm));
-    const int64_t split = (s->part.K_interior / s->lay.E) * s->lay.E;  // tile-aligned
-    // the interior range runs while the NCCL send/recv kernels move the traces: leave them SMs
-    // (a persistent grid of every SM would otherwise hold the exchange until it drains)
-    dg::StageParams<T> pi = p;
-    pi.sm_reserve = s->loopback ? 0 : kNcclSmReserve;
-    launch_stage<T>(s, pi, 1, 0, split, s->stream);
-    CK(cudaStreamWaitEvent(s->stream, s->ev_join, 0));
-    launch_stage<T>(s, p, 1, split, s->Kl, s->stream);
-  } else {
+  if (s->part.n_ghost_faces == 0) {
     launch_stage<T>(s, p, 1, 0, s->Kl, s->stream);
+    CK(cudaGetLastError());
+    return DG_OK;
   }
+  CK(cudaEventRecord(s->ev_fork, s->stream));  // before the launch: the comm branch runs beside it
+  p.sm_reserve = kNcclSmReserve;
+  if (signals_boundary(s)) {
+    p.bsig = s->d_bsig;
+    p.bsig_tiles = s->nbt;
+  }
+  launch_stage<T>(s, p, 1, 0, s->Kl, s->stream);
   CK(cudaGetLastError());
+  if (!signals_boundary(s)) CK(cudaEventRecord(s->ev_done, s->stream));
+  CK(cudaStreamWaitEvent(s->comm, s->ev_fork, 0));
+  dg_status st = await_boundary(s);
+  if (st != DG_OK) return st;
+  dg::pack_traces<T>(uout, static_cast<T*>(s->d_send), s->d_sidx, s->part.n_ghost_faces, s->Nfp, s->lay, s->comm);
+  st = nccl_exchange<T>(s, uout);
+  if (st != DG_OK) return st;
+  CK(cudaEventRecord(s->ev_join, s->comm));
+  CK(cudaStreamWaitEvent(s->stream, s->ev_join, 0));
   return DG_OK;
 }
 
@@ -303,19 +374,26 @@ dg::StageParams<T> stage_params(dg_solver* s, int stage, double dt, int cur) {
   return p;
 }
 
-// Loopback transport: one LSERK stage for a group of same-process solvers that
-// partition one mesh.  Identical to the NCCL path except that each partition's
-// ghost records are copied device-to-device from its peers' send buffers.
+// Loopback transport: the exchange of a group of same-process solvers that partition one mesh.
+// Identical to the NCCL path except that each partition's ghost records are copied
+// device-to-device from its peers' send buffers.  The packs read u[src] (after `ready`: the
+// previous stage kernel's boundary signal, or — priming — nothing further) and the copies
+// write the ghost regions of u[src].
 template <typename T>
-dg_status group_stage(dg_solver* const* g, int n, int stage, double dt, int cur) {
+dg_status group_exchange(dg_solver* const* g, int n, int src, bool after_stage) {
   const size_t rec = size_t(g[0]->nc) * g[0]->Nfp;
-  for (int i = 0; i < n; ++i) {  // pack (after my previous stage, after peers finished reading my send buffer)
+  for (int i = 0; i < n; ++i) {  // pack (after my boundary tiles, after peers finished reading my send buffer)
     dg_solver* s = g[i];
     if (s->part.n_ghost_faces == 0) continue;
-    CK(cudaEventRecord(s->ev_fork, s->stream));
-    CK(cudaStreamWaitEvent(s->comm, s->ev_fork, 0));
+    if (!after_stage) {
+      CK(cudaEventRecord(s->ev_fork, s->stream));
+      CK(cudaStreamWaitEvent(s->comm, s->ev_fork, 0));
+    } else {
+      dg_status st = await_boundary(s);
+      if (st != DG_OK) return st;
+    }
     for (const auto& pp : s->part.peers) CK(cudaStreamWaitEvent(s->comm, g[pp.rank]->ev_copied, 0));
-    dg::pack_traces<T>(static_cast<T*>(s->d_u[cur]), static_cast<T*>(s->d_send), s->d_sidx, s->part.n_ghost_faces,
+    dg::pack_traces<T>(static_cast<T*>(s->d_u[src]), static_cast<T*>(s->d_send), s->d_sidx, s->part.n_ghost_faces,
                        s->Nfp, s->lay, s->comm);
     CK(cudaEventRecord(s->ev_packed, s->comm));
   }
@@ -329,26 +407,45 @@ dg_status group_stage(dg_solver* const* g, int n, int stage, double dt, int cur)
         if (rp.rank == q) back = &rp;
       if (!back || back->nfaces != pp.nfaces) return fail(DG_ERR_STATE, "inconsistent partition plans in group");
       CK(cudaStreamWaitEvent(s->comm, r->ev_packed, 0));
-      T* dst = static_cast<T*>(s->d_u[cur]) + s->ghost_base + pp.recv_off * rec;
-      const T* src = static_cast<const T*>(r->d_send) + back->send_off * rec;
-      CK(cudaMemcpyAsync(dst, src, pp.nfaces * rec * sizeof(T), cudaMemcpyDeviceToDevice, s->comm));
+      T* dst = static_cast<T*>(s->d_u[src]) + s->ghost_base + pp.recv_off * rec;
+      const T* srcp = static_cast<const T*>(r->d_send) + back->send_off * rec;
+      CK(cudaMemcpyAsync(dst, srcp, pp.nfaces * rec * sizeof(T), cudaMemcpyDeviceToDevice, s->comm));
     }
     CK(cudaEventRecord(s->ev_copied, s->comm));
     CK(cudaEventRecord(s->ev_join, s->comm));
   }
-  for (int i = 0; i < n; ++i) {  // compute: interior range, then (after the ghosts landed) the rest
+  if (!after_stage)
+    for (int q = 0; q < n; ++q)
+      if (g[q]->part.n_ghost_faces > 0) CK(cudaStreamWaitEvent(g[q]->stream, g[q]->ev_join, 0));
+  return DG_OK;
+}
+
+// One LSERK stage of a loopback group: every partition's stage kernel (one launch, boundary
+// tiles first), then the exchange of the boundary traces of u[cur^1] beside the interior tiles.
+template <typename T>
+dg_status group_stage(dg_solver* const* g, int n, int stage, double dt, int cur) {
+  for (int i = 0; i < n; ++i) {
     dg_solver* s = g[i];
     dg::StageParams<T> p = stage_params<T>(s, stage, dt, cur);
     if (s->part.n_ghost_faces > 0) {
-      const int64_t split = (s->part.K_interior / s->lay.E) * s->lay.E;
-      launch_stage<T>(s, p, 1, 0, split, s->stream);
-      CK(cudaStreamWaitEvent(s->stream, s->ev_join, 0));
-      launch_stage<T>(s, p, 1, split, s->Kl, s->stream);
-    } else {
-      launch_stage<T>(s, p, 1, 0, s->Kl, s->stream);
+      CK(cudaEventRecord(s->ev_fork, s->stream));
+      p.sm_reserve = kNcclSmReserve;  // the pack kernel runs beside the interior tiles
+      if (signals_boundary(s)) {
+        p.bsig = s->d_bsig;
+        p.bsig_tiles = s->nbt;
+      }
     }
+    launch_stage<T>(s, p, 1, 0, s->Kl, s->stream);
     CK(cudaGetLastError());
+    if (s->part.n_ghost_faces > 0) {
+      if (!signals_boundary(s)) CK(cudaEventRecord(s->ev_done, s->stream));
+      CK(cudaStreamWaitEvent(s->comm, s->ev_fork, 0));
+    }
   }
+  dg_status st = group_exchange<T>(g, n, cur ^ 1, true);
+  if (st != DG_OK) return st;
+  for (int q = 0; q < n; ++q)
+    if (g[q]->part.n_ghost_faces > 0) CK(cudaStreamWaitEvent(g[q]->stream, g[q]->ev_join, 0));
   return DG_OK;
 }
 
@@ -358,13 +455,10 @@ dg_status enqueue_rhs(dg_solver* s, T* out_tiles) {
   T* uin = static_cast<T*>(s->d_u[s->cur]);
   p.u_in = uin;
   p.rhs_out = out_tiles;
-  if (s->part.n_ghost_faces > 0) {
-    CK(cudaEventRecord(s->ev_fork, s->stream));
-    CK(cudaStreamWaitEvent(s->comm, s->ev_fork, 0));
-    dg_status st = enqueue_exchange<T>(s, uin);
+  if (s->part.n_ghost_faces > 0 && !s->ghosts_valid) {
+    dg_status st = exchange_now<T>(s, uin);
     if (st != DG_OK) return st;
-    CK(cudaEventRecord(s->ev_join, s->comm));
-    CK(cudaStreamWaitEvent(s->stream, s->ev_join, 0));
+    s->ghosts_valid = true;
   }
   launch_stage<T>(s, p, 0, 0, s->Kl, s->stream);
   CK(cudaGetLastError());
@@ -511,6 +605,9 @@ dg_status upload_setup(dg_solver* s) {
   CK(cudaMemcpy(s->d_fmask, fm.data(), NF * sizeof(int16_t), cudaMemcpyHostToDevice));
   if (P.n_ghost_faces > 0) {
     CK(cudaMalloc(&s->d_send, P.n_ghost_faces * s->nc * Nfp * wb));
+    CK(cudaMalloc((void**)&s->d_bsig, sizeof(unsigned)));
+    CK(cudaMemset(s->d_bsig, 0, sizeof(unsigned)));
+    s->nbt = (P.K_boundary + s->lay.E - 1) / s->lay.E;  // tiles holding the boundary elements (local order)
     std::vector<int32_t> sidx(size_t(P.n_ghost_faces) * Nfp);
     for (int64_t g = 0; g < P.n_ghost_faces; ++g)
       for (int j = 0; j < Nfp; ++j)
@@ -520,70 +617,7 @@ dg_status upload_setup(dg_solver* s) {
     CK(cudaMalloc((void**)&s->d_sidx, sidx.size() * sizeof(int32_t)));
     CK(cudaMemcpy(s->d_sidx, sidx.data(), sidx.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   }
-  if (sizeof(T) == 8 && s->cfg.variant == DG_VARIANT_FUSED && P.n_ghost_faces == 0 && dg::fused_launcher_f64(s->N)) {
-    // tile dependency lists: the tiles holding a face neighbour of any element of the tile, and itself
-    const int64_t ntl = s->ntiles, E = s->lay.E;
-    std::vector<int32_t> off(size_t(ntl) + 1, 0), lst;
-    std::vector<int32_t> tmp;
-    for (int64_t t = 0; t < ntl; ++t) {
-      tmp.clear();
-      tmp.push_back(int32_t(t));
-      for (int64_t l = t * E; l < std::min((t + 1) * E, Kl); ++l) {
-        const int64_t k = P.local_ids[l];
-        for (int f = 0; f < 4; ++f) {
-          const int64_t k2 = m.EToE[4 * k + f];
-          if (k2 == k) continue;
-          tmp.push_back(int32_t(P.g2l[k2] / E));
-        }
-      }
-      std::sort(tmp.begin(), tmp.end());
-      tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
-      lst.insert(lst.end(), tmp.begin(), tmp.end());
-      off[t + 1] = int32_t(lst.size());
-    }
-    CK(cudaMalloc((void**)&s->d_flags, std::max<int64_t>(ntl, 1) * sizeof(unsigned)));
-    CK(cudaMemsetAsync(s->d_flags, 0, std::max<int64_t>(ntl, 1) * sizeof(unsigned), s->stream));
-    CK(cudaMalloc((void**)&s->d_nbr_off, off.size() * sizeof(int32_t)));
-    CK(cudaMemcpy(s->d_nbr_off, off.data(), off.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-    CK(cudaMalloc((void**)&s->d_nbr, std::max<size_t>(lst.size(), 1) * sizeof(int32_t)));
-    CK(cudaMemcpy(s->d_nbr, lst.data(), lst.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-    s->fused = true;
-    s->stage_count = 0;
-  }
   CK(cudaStreamSynchronize(s->stream));
-  return DG_OK;
-}
-
-// All nsteps LSERK4 steps as one stage-fused launch (kernels/stage_ws.cuh, FUSED).
-dg_status fused_steps(dg_solver* s, double dt, int nsteps) {
-  if (nsteps <= 0) return DG_OK;
-  dg::StageParams<double> p = base_params<double>(s);
-  dg::FusedParams<double> fp{};
-  fp.u[0] = static_cast<double*>(s->d_u[0]);
-  fp.u[1] = static_cast<double*>(s->d_u[1]);
-  fp.par0 = s->cur;
-  fp.nst = 5 * nsteps;
-  fp.stage0 = 0;
-  fp.g0 = s->stage_count;
-  fp.flags = s->d_flags;
-  fp.nbr_off = s->d_nbr_off;
-  fp.nbr = s->d_nbr;
-  for (int i = 0; i < 5; ++i) {
-    fp.rk_a[i] = kRkA[i];
-    fp.rk_b[i] = kRkB[i];
-  }
-  p.u_in = fp.u[s->cur];
-  p.u_out = fp.u[s->cur ^ 1];
-  p.res = static_cast<double*>(s->d_res);
-  p.dt = dt;
-  p.first_stage = 1;
-  if (!dg::fused_launcher_f64(s->N)(p, fp, s->stream)) {
-    cudaGetLastError();
-    return fail(DG_ERR_CUDA, "stage-fused cooperative launch refused (use DG_VARIANT_MMA_WS)");
-  }
-  CK(cudaGetLastError());
-  s->stage_count += unsigned(fp.nst);
-  s->cur = (s->cur + fp.nst) & 1;
   return DG_OK;
 }
 
@@ -623,7 +657,11 @@ static bool graphs_enabled() {
 
 template <typename T>
 dg_status lserk_steps(dg_solver* s, double dt, int nsteps) {
-  if (sizeof(T) == 8 && s->fused) return fused_steps(s, dt, nsteps);
+  if (nsteps > 0 && s->part.n_ghost_faces > 0 && !s->ghosts_valid) {  // prime: traces of the uploaded fields
+    dg_status st = exchange_now<T>(s, static_cast<T*>(s->d_u[s->cur]));
+    if (st != DG_OK) return st;
+    s->ghosts_valid = true;  // every stage's exchange keeps them valid from here on
+  }
   if (!graphs_enabled()) {
     for (int n = 0; n < nsteps; ++n) {
       for (int stage = 0; stage < 5; ++stage) {
@@ -768,6 +806,7 @@ dg_status dg_create(const dg_config* cfg, dg_solver** out) {
     CK(cudaEventCreate(&s->ev_t1));
     CK(cudaEventCreateWithFlags(&s->ev_packed, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&s->ev_copied, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&s->ev_done, cudaEventDisableTiming));
     if (cfg->nranks > 1 && !s->loopback) {
       NcclApi& n = nccl();
       if (!n.ok) return fail(DG_ERR_NCCL, n.err);
@@ -858,10 +897,7 @@ static dg_status upload_common(dg_solver* s, const void* src, bool from_host) {
   }
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(s->d_res, 0, std::max<int64_t>(s->ntiles * s->lay.TS, 1) * s->wsize, s->stream));
-  if (s->fused) {
-    CK(cudaMemsetAsync(s->d_flags, 0, std::max<int64_t>(s->ntiles, 1) * sizeof(unsigned), s->stream));
-    s->stage_count = 0;
-  }
+  s->ghosts_valid = false;
   if (from_host) CK(cudaStreamSynchronize(s->stream));
   s->has_fields = true;
   return DG_OK;
@@ -947,10 +983,7 @@ dg_status dg_fields_upload_async(dg_solver* s, const double* f) {
   CK(cudaGetLastError());
   CK(cudaEventRecord(s->ev_in_free[i], s->stream));
   CK(cudaMemsetAsync(s->d_res, 0, std::max<int64_t>(s->ntiles * s->lay.TS, 1) * s->wsize, s->stream));
-  if (s->fused) {
-    CK(cudaMemsetAsync(s->d_flags, 0, std::max<int64_t>(s->ntiles, 1) * sizeof(unsigned), s->stream));
-    s->stage_count = 0;
-  }
+  s->ghosts_valid = false;
   s->has_fields = true;
   return DG_OK;
 }
@@ -1014,6 +1047,15 @@ dg_status dg_group_lserk_step(dg_solver* const* group, int32_t n, double dt, int
     if (g[i]->N != g[0]->N || g[i]->fp64 != g[0]->fp64 || g[i]->cur != g[0]->cur || g[i]->mesh.K != g[0]->mesh.K ||
         g[i]->lay.E != g[0]->lay.E || g[i]->lay.perm != g[0]->lay.perm || g[i]->nc != g[0]->nc)
       return fail(DG_ERR_ARG, "group members differ in order, precision, variant, mesh or step parity");
+  bool prime = false;
+  for (int i = 0; i < n; ++i) prime = prime || (g[i]->part.n_ghost_faces > 0 && !g[i]->ghosts_valid);
+  if (nsteps > 0 && prime) {
+    const int cur = g[0]->cur;
+    dg_status st = g[0]->fp64 ? group_exchange<double>(g.data(), n, cur, false)
+                              : group_exchange<float>(g.data(), n, cur, false);
+    if (st != DG_OK) return st;
+    for (int i = 0; i < n; ++i) g[i]->ghosts_valid = true;
+  }
   for (int step = 0; step < nsteps; ++step) {
     for (int stage = 0; stage < 5; ++stage) {
       const int cur = g[0]->cur;
@@ -1144,15 +1186,14 @@ dg_status dg_time_stage_kernel(dg_solver* s, int32_t reps, double* ms) {
 dg_status dg_launches_per_step(dg_solver* s, int32_t* n) {
   if (!s || !n) return fail(DG_ERR_ARG, "null argument");
   const bool halo = s->has_mesh && s->part.n_ghost_faces > 0;
-  // stage-fused: one launch per dg_lserk_step call; otherwise per stage: stage kernel
-  // (+ pack kernel + second stage range)
-  *n = s->fused ? 1 : 5 * (halo ? 3 : 1);
+  // per stage: the stage kernel (+ the pack kernel of the trace exchange)
+  *n = 5 * (halo ? 2 : 1);
   return DG_OK;
 }
 
 dg_status dg_kernel_variant(dg_solver* s, int32_t* variant) {
   if (!s || !variant) return fail(DG_ERR_ARG, "null argument");
-  *variant = s->cfg.variant == DG_VARIANT_FUSED ? int32_t(DG_VARIANT_FUSED) : int32_t(s->variant);
+  *variant = int32_t(s->variant);
   return DG_OK;
 }
 
@@ -1180,6 +1221,7 @@ void dg_destroy(dg_solver* s) {
     if (s->ev_t1) cudaEventDestroy(s->ev_t1);
     if (s->ev_packed) cudaEventDestroy(s->ev_packed);
     if (s->ev_copied) cudaEventDestroy(s->ev_copied);
+    if (s->ev_done) cudaEventDestroy(s->ev_done);
     if (s->comm) cudaStreamDestroy(s->comm);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
   }

@@ -113,15 +113,17 @@ std::string build_partition(const MeshData& m, int rank, int nranks, const int32
       cross[q].push_back({key, mine});
     }
   }
-  for (int64_t k = 0; k < K; ++k)
-    if (own[k] == rank && !is_bnd[k]) P.local_ids.push_back(k);
-  P.K_interior = int64_t(P.local_ids.size());
+  // boundary-first: a stage writes the boundary elements' fields in its first tiles, so the
+  // next stage's trace exchange starts while the interior tiles are still running
   for (int64_t k = 0; k < K; ++k)
     if (own[k] == rank && is_bnd[k]) P.local_ids.push_back(k);
+  P.K_boundary = int64_t(P.local_ids.size());
+  for (int64_t k = 0; k < K; ++k)
+    if (own[k] == rank && !is_bnd[k]) P.local_ids.push_back(k);
   P.K_local = int64_t(P.local_ids.size());
   if (reorder) {
-    morton_sort(m, P.local_ids, 0, size_t(P.K_interior));
-    morton_sort(m, P.local_ids, size_t(P.K_interior), size_t(P.K_local));
+    morton_sort(m, P.local_ids, 0, size_t(P.K_boundary));
+    morton_sort(m, P.local_ids, size_t(P.K_boundary), size_t(P.K_local));
   }
   P.g2l.assign(K, -1);
   for (int64_t l = 0; l < P.K_local; ++l) P.g2l[P.local_ids[l]] = l;

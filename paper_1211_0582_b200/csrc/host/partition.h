@@ -1,10 +1,11 @@
 // Mesh partition for multi-GPU runs (distributed DG, one
 // exchange of face data per stage; volume ~ N^3 vs surface ~ N^2).
 //
-// Each rank owns a set of elements.  Local storage order: elements with no
-// face on another rank ("interior") first, then the partition-boundary
-// elements, each group in ascending global id, so that a stage can run the
-// interior range while the face traces are in flight.
+// Each rank owns a set of elements.  Local storage order: the partition-boundary
+// elements (a face on another rank) first, then the interior elements, each group
+// in ascending global id.  A stage kernel writes the boundary elements in its first
+// tiles and signals their completion, so the next stage's trace exchange runs while
+// the interior tiles are still being computed.
 //
 // Ghost faces: for every rank pair (r, q) the cross faces are ordered by the
 // global slot 4k+f of the face on the LOWER rank; rank r sends, for each of its
@@ -30,7 +31,7 @@ struct PeerPlan {
 
 struct Partition {
   int rank = 0, nranks = 1;
-  int64_t K_global = 0, K_local = 0, K_interior = 0;
+  int64_t K_global = 0, K_local = 0, K_boundary = 0;
   std::vector<int64_t> local_ids;   // [K_local] global id of local element l (storage order)
   std::vector<int64_t> g2l;         // [K_global] local index or -1
   std::vector<PeerPlan> peers;      // ascending peer rank
@@ -43,7 +44,7 @@ struct Partition {
 };
 
 // owner: [K] rank per element, or empty -> contiguous ranges.  reorder: sort each group
-// (interior, boundary) by the Morton code of the element centroids.  Returns "" or an error.
+// (boundary, interior) by the Morton code of the element centroids.  Returns "" or an error.
 std::string build_partition(const MeshData& m, int rank, int nranks, const int32_t* owner,
                             Partition& out, bool reorder = false);
 

@@ -13,7 +13,6 @@ namespace dg {
   size_t tc_ops_count_N##n();                                                       \
   void tc_ops_N##n(const double*, const double*, const double*, const double*, float*); \
   void ws32_ops_N##n(const double*, const double*, const double*, const double*, float*); \
-  bool launch_fused_f64_N##n(const StageParams<double>&, const FusedParams<double>&, void*); \
   TileLayout ffma_layout_N##n();                                                    \
   size_t ffma_ops_count_N##n();                                                     \
   void ffma_ops_N##n(const double*, const double*, const double*, const double*, float*); \
@@ -34,13 +33,6 @@ StageLauncher<float> stage_launcher_f32(int N) {
   static const StageLauncher<float> t[9] = {
       launch_stage_f32_N1, launch_stage_f32_N2, launch_stage_f32_N3, launch_stage_f32_N4, launch_stage_f32_N5,
       launch_stage_f32_N6, launch_stage_f32_N7, launch_stage_f32_N8, launch_stage_f32_N9};
-  return (N >= 1 && N <= 9) ? t[N - 1] : nullptr;
-}
-
-FusedLauncherF64 fused_launcher_f64(int N) {
-  static const FusedLauncherF64 t[9] = {launch_fused_f64_N1, launch_fused_f64_N2, launch_fused_f64_N3,
-                                        launch_fused_f64_N4, launch_fused_f64_N5, launch_fused_f64_N6,
-                                        launch_fused_f64_N7, launch_fused_f64_N8, launch_fused_f64_N9};
   return (N >= 1 && N <= 9) ? t[N - 1] : nullptr;
 }
 

@@ -366,6 +366,7 @@ __global__ void __launch_bounds__(FfCfg<T, N, System<SYS>::NC>::NT, 1)
     constexpr int EPL = C::EPL, EL = C::EL;
     const int el = lane % EL, rg = lane / EL;  // elements el + ep * EL, ep < EPL
     const int64_t total = J * C::MB;
+    const int64_t nb = p.bsig ? bsig_ctiles(p.bsig_tiles) : 0;  // boundary tiles (multi-rank signal)
     int64_t released = 0, waited = -1, lwaited = -1;
     auto release = [&](int64_t jj) {
       if (waited < jj) {
@@ -374,6 +375,7 @@ __global__ void __launch_bounds__(FfCfg<T, N, System<SYS>::NC>::NT, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_empty + int(jj % S));
+      if (jj == nb - 1) signal_boundary(p.bsig, nb, 32 * C::CW, warp == 0 && lane == 0);
     };
     const T* A = C::OPS_SMEM ? sA : opsT;
     auto ld4 = [&](int idx) -> V {  // RB consecutive operator rows, 16 bytes

@@ -60,9 +60,6 @@ void DG_FN(ws32_ops)(const double* Dr, const double* Ds, const double* Dt, const
 }
 
 TileLayout DG_FN(ws_layout)() { return ws_layout<DG_N>(); }
-// DG_VARIANT_FUSED was withdrawn in round 2 (slower than per-stage launches, racecheck reports it
-// unverified): the stage-fused WS instance is no longer built
-bool DG_FN(launch_fused_f64)(const StageParams<double>&, const FusedParams<double>&, void*) { return false; }
 
 #ifdef DG_WS_PROFILE
 void DG_FN(tc_dbg)(float* p) { tc_dbg_set(p); }

@@ -106,28 +106,12 @@ struct StageParams {
   int64_t ghost_base;  // offset of the ghost-trace region
   T rk_a, rk_b, dt, alpha;
   int first_stage;     // 1: a_s == 0, do not read res
-  int sm_reserve;      // persistent kernels leave this many SMs free (interior range overlapping an NCCL exchange)
+  int sm_reserve;      // persistent kernels leave this many SMs free (for the concurrent trace exchange)
+  // multi-rank stages: the launch's tiles [0, bsig_tiles) hold the partition-boundary
+  // elements; the store warps add the number of those tiles to *bsig once they are written (nullptr: off)
+  unsigned* bsig;
+  int64_t bsig_tiles;
   int system;          // dg_system: 0 Maxwell, 1 acoustics (BASIC kernel)
-};
-
-// Stage-fused persistent launch (single rank, WS kernels): one launch runs nst
-// consecutive LSERK stages.  Tile t of stage g starts once every tile in its
-// neighbour list (nbr[nbr_off[t] .. nbr_off[t+1]), itself included) has completed
-// stage g-1: flags[t] counts the completed stages of tile t (absolute, since the
-// last field upload).  That one condition orders the trace gathers after their
-// producers (RAW) and the overwrite of the ping-pong buffer after every reader of
-// the previous stage (WAR).  DESIGN.md §8 "Stage-fused launch".
-template <typename T>
-struct FusedParams {
-  T* u[2];                  // ping-pong buffers: stage g reads u[(par0+g)&1], writes the other
-  int par0;
-  int nst;                  // stages in this launch (0: not fused)
-  int stage0;               // LSERK stage index (0..4) of the first stage
-  unsigned g0;              // absolute index of the first stage (flags compare against g0+g)
-  unsigned* flags;          // [ntiles]
-  const int32_t* nbr_off;   // [ntiles+1]
-  const int32_t* nbr;       // neighbour tiles, self included
-  T rk_a[5], rk_b[5];
 };
 
 // Launchers, one per (order, precision), defined in stage_N*.cu.
@@ -136,9 +120,6 @@ template <typename T>
 using StageLauncher = void (*)(const StageParams<T>&, int mode, int variant, void* stream);
 
 StageLauncher<double> stage_launcher_f64(int N);
-// stage-fused FP64 WS launch (returns false if the kernel cannot run fused for this N)
-using FusedLauncherF64 = bool (*)(const StageParams<double>&, const FusedParams<double>&, void* stream);
-FusedLauncherF64 fused_launcher_f64(int N);
 TileLayout ws_layout_f64(int N);   // tiled layout of the FP64 WS kernel for order N
 TileLayout ws32_layout_f32(int N); // tiled layout of the FP32 (3xTF32) WS kernel
 size_t ws32_ops_count(int N);      // floats in its split hi/lo operator buffer

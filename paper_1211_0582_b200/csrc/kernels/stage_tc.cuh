@@ -312,6 +312,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
     // behind the MMA / the previous group instead of serializing with the stores.
     const int r = 32 * warp + lane, e = r / 6;
     const bool res_in = UPDATE && !p.first_stage;
+    const int nb = p.bsig ? int(bsig_ctiles(p.bsig_tiles)) : 0;  // boundary tiles (multi-rank signal)
     TC_T(tcta);
     for (int j = 0; j < J; ++j) {
       const int a = j % C::NACC;
@@ -373,6 +374,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty + a);
+      if (j == nb - 1) signal_boundary(p.bsig, nb, 128, tid == 0);
       TC_A(1, t1);
 #ifdef DG_WS_PROFILE
       if (tid == 0) atomicAdd(&g_tc_prof[12], 1ull);

@@ -130,10 +130,8 @@ struct WsCfg {
   static constexpr int SLOT = OFF_F + r16(6 * E * LDF * 8);
   static constexpr int A_BYTES = OPS_SMEM ? r16((3 * M8 * LDA + M8 * LDL) * 8) : 0;
   static constexpr int FM_BYTES = r16(NF * 2);
-  static constexpr int NTF = NT + 32;  // fused launches: + one publisher warp
-  static constexpr int VB = 8;         // fused: tiles verified per dependency poll round
-  // mbarriers load/tr/full/empty [S] (+ fused: done[2S], published counter, verify flags)
-  static constexpr int BAR_BYTES = 6 * S * 8 + 16 + r16(VB * 4);
+  // mbarriers load/tr/full/empty [S]
+  static constexpr int BAR_BYTES = 4 * S * 8;
   static constexpr size_t SMEM_BYTES = size_t(S) * SLOT + A_BYTES + FM_BYTES + BAR_BYTES;
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   static_assert(E % 4 == 0, "tile = whole 4-element column groups");
@@ -172,6 +170,23 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
 }
 __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Multi-rank stages ("boundary-first stage"): the tiles [0, p.bsig_tiles) of the
+// launch hold the partition-boundary elements.  bsig_ctiles() is the number of them this CTA
+// processes (its first tiles, j < nb).  Once every store warp of the CTA has finished them,
+// signal_boundary() adds nb to *p.bsig with release semantics; the comm stream waits for the
+// total (cuStreamWaitValue32: a front-end wait, no SM is held) and then packs and sends the
+// next stage's traces while the interior tiles are still running.  No kernel ever waits on it.
+__device__ __forceinline__ int64_t bsig_ctiles(int64_t nbt) {
+  return nbt > int64_t(blockIdx.x) ? (nbt - int64_t(blockIdx.x) + gridDim.x - 1) / gridDim.x : 0;
+}
+// called by all threads of the CTA's store warps (nthreads = 32 x warps), exactly once
+__device__ __forceinline__ void signal_boundary(unsigned* bsig, int64_t nb, int nthreads, bool leader) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");  // their stores precede the barrier
+  if (leader) {
+    __threadfence();  // cumulative: every store ordered before the barrier is visible GPU-wide
+    atomicAdd(bsig, unsigned(nb));
+  }
 }
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
@@ -230,13 +245,9 @@ __device__ unsigned long long g_ws_prof[16];
 // ---------------------------------------------------------------- kernel
 // Tiles [t_begin, t_begin + t_count) of the tiled arrays; p.k_begin/p.K give the
 // element range (tile-aligned start) used to count elements in the last tile.
-// FUSED: one launch runs fp.nst LSERK stages (StageParams supplies the geometry, indices
-// and operators; FusedParams the buffers, coefficients and tile dependencies).  The
-// ring position jj = g * J + j walks stage g's tiles j = 0..J-1 of this CTA.
-template <int N, bool UPDATE, bool FUSED>
-__global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
-    dg_stage_ws(const StageParams<double> p, const double* __restrict__ opsA, int64_t t_begin, int64_t t_count,
-                const FusedParams<double> fp) {
+template <int N, bool UPDATE>
+__global__ void __launch_bounds__(WsCfg<N>::NT, 1)
+    dg_stage_ws(const StageParams<double> p, const double* __restrict__ opsA, int64_t t_begin, int64_t t_count) {
   using C = WsCfg<N>;
   constexpr int Np = C::Np, Nfp = C::Nfp, NF = C::NF, M8 = C::M8, KV = C::KV, KL = C::KL;
   constexpr int E = C::E, LD = C::LD, LDF = C::LDF, S = C::S, TS = C::TS;
@@ -250,9 +261,7 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
   uint64_t* bar_tr = bars + S;
   uint64_t* bar_full = bars + 2 * S;
   uint64_t* bar_empty = bars + 3 * S;
-  uint64_t* bar_done = bars + 4 * S;  // fused [2S]: MMA warps done with tile jj (-> publisher)
-  volatile long long* published = reinterpret_cast<volatile long long*>(bars + 6 * S);  // fused
-  constexpr int NTK = FUSED ? C::NTF : C::NT;
+  constexpr int NTK = C::NT;
   auto sU = [&](int s) { return reinterpret_cast<double*>(smem + size_t(s) * C::SLOT + C::OFF_U); };
   auto sR = [&](int s) { return reinterpret_cast<double*>(smem + size_t(s) * C::SLOT + C::OFF_R); };
   auto sG = [&](int s) { return reinterpret_cast<double*>(smem + size_t(s) * C::SLOT + C::OFF_G); };
@@ -260,18 +269,12 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
   auto sF = [&](int s) { return reinterpret_cast<double*>(smem + size_t(s) * C::SLOT + C::OFF_F); };
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // tiles of this CTA: t_begin + blockIdx.x + j * gridDim.x, j < J; fused: JJ = nst * J positions
+  // tiles of this CTA: t_begin + blockIdx.x + j * gridDim.x, j < J
   const int64_t J = t_count > blockIdx.x ? (t_count - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  const int64_t JJ = FUSED ? int64_t(fp.nst) * J : J;
+  const int64_t JJ = J;
   const int64_t kend = p.k_begin + p.K;
-  auto stage_of = [&](int64_t jj) { return FUSED ? int(jj / J) : 0; };
-  auto tile_of = [&](int64_t jj) { return t_begin + blockIdx.x + (FUSED ? jj % J : jj) * gridDim.x; };
-  auto stage_end = [&](int64_t jj) { return FUSED ? (jj / J + 1) * J : JJ; };
-  auto u_in_of = [&](int g) -> const double* { return FUSED ? fp.u[(fp.par0 + g) & 1] : p.u_in; };
-  auto u_out_of = [&](int g) -> double* { return FUSED ? fp.u[(fp.par0 + g + 1) & 1] : p.u_out; };
-  auto res_in_of = [&](int g) { return UPDATE && (FUSED ? (fp.stage0 + g) % 5 != 0 : !p.first_stage); };
-  auto rk_a_of = [&](int g) { return FUSED ? fp.rk_a[(fp.stage0 + g) % 5] : p.rk_a; };
-  auto rk_b_of = [&](int g) { return FUSED ? fp.rk_b[(fp.stage0 + g) % 5] : p.rk_b; };
+  auto tile_of = [&](int64_t jj) { return t_begin + blockIdx.x + jj * gridDim.x; };
+  const bool res_in = UPDATE && !p.first_stage;
   auto count_of = [&](int64_t tile) {
     const int64_t k0 = tile * E;
     return int(kend - k0 < E ? kend - k0 : E);
@@ -283,10 +286,7 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
       mbar_init(bar_tr + s, C::PT);
       mbar_init(bar_full + s, C::PT);
       mbar_init(bar_empty + s, C::MW);
-      mbar_init(bar_done + s, C::MW);
-      mbar_init(bar_done + S + s, C::MW);
     }
-    *published = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int m = tid; m < NF; m += NTK) sFm[m] = p.fmask[m];
@@ -311,41 +311,8 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
   if (warp == C::MW) {
     // ====================== TMA loader warp (one lane) ======================
     // Runs ahead of everybody, bounded only by free ring slots: tile j's bulk
-    // loads are issued as soon as the MMA warps release tile j - S (fused launches: as
-    // soon as the publisher has published it).
-    // Fused: the whole warp verifies tile dependencies in batches (verify_from), lane 0
-    // issues the copies.
-    int64_t verified = 0;  // fused: positions < verified have their dependencies satisfied
-    auto verify_from = [&](int64_t j0, bool block) {
-      // candidates j0 .. j1-1 (same stage): poll all their neighbour counters with relaxed
-      // loads, spread over the lanes; take the longest satisfied prefix (at least j0,
-      // waiting for it if needed); one acquire fence + one proxy fence for the batch.
-      const int64_t j1 = j0 + C::VB < stage_end(j0) ? j0 + C::VB : stage_end(j0);
-      const unsigned target = fp.g0 + unsigned(stage_of(j0));
-      const long long t0 = clock64();
-      int64_t hi = j0;
-      for (;;) {
-        // all polls of the batch issued back to back; results in a register bitmask
-        unsigned bad = 0;
-        for (int64_t x = j0; x < j1; ++x) {
-          const int64_t t = tile_of(x);
-          const int q0 = fp.nbr_off[t], q1 = fp.nbr_off[t + 1];
-          for (int q = q0 + lane; q < q1; q += 32)
-            bad |= unsigned(ld_relaxed_gpu(fp.flags + fp.nbr[q]) < target) << int(x - j0);
-        }
-        bad = __reduce_or_sync(0xffffffffu, bad);
-        hi = j0 + (bad ? __ffs(bad) - 1 : int(j1 - j0));
-        if (hi > j0 || !block) break;
-        __nanosleep(64);
-        if (clock64() - t0 > (1ll << 35)) __trap();  // broken dependency graph: no silent hang
-      }
-      if (hi == j0) return;
-      fence_acq_rel_gpu();
-      fence_proxy_async_global();
-      __syncwarp();
-      verified = hi;
-    };
-    if (FUSED || lane == 0) {
+    // loads are issued as soon as the MMA warps release tile j - S.
+    if (lane == 0) {
       DG_T0();
       for (int64_t j = 0; j < JJ; ++j) {
         const int s = int(j % S);
@@ -356,47 +323,13 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
           DG_ACC(0);
         }
         const int64_t tile = tile_of(j);
-        const int g = stage_of(j);
-        const bool res_in = res_in_of(g);
-        if constexpr (FUSED) {
-          if (j >= verified) verify_from(j, true);
-          // done[] phase safety: tile j reuses done[j % 2S] only after tile j - 2S is published
-          while (*published <= j - 2 * S) __nanosleep(32);
-        }
-        if (lane == 0) {
-          unsigned bytes = TS * 8 + C::GEOT * 8 + C::IDXT * 4;
-          if (C::RES_SMEM && res_in) bytes += TS * 8;
-          mbar_arrive_tx(bar_load + s, bytes);
-          bulk_g2s(sU(s), u_in_of(g) + tile * TS, TS * 8, bar_load + s);
-          if (C::RES_SMEM && res_in) bulk_g2s(sR(s), p.res + tile * TS, TS * 8, bar_load + s);
-          bulk_g2s(sG(s), p.geo + tile * C::GEOT, C::GEOT * 8, bar_load + s);
-          bulk_g2s(sI(s), p.gidx + tile * C::IDXT, C::IDXT * 4, bar_load + s);
-        }
-        if constexpr (FUSED) {  // verify ahead while the ring is full (hides the poll + fence latency)
-          __syncwarp();
-          if (verified - j < C::VB / 2 && verified < JJ) verify_from(verified, false);
-        }
-      }
-    }
-  } else if (FUSED && warp == C::MW + 1 + C::PW) {
-    // ===================== publisher warp (fused launches, one lane) =====================
-    // Publishes tile completions in order: waits until the MMA warps are done with tile jj
-    // (done[jj % 2S]), batches every later tile already done (non-blocking test), then one
-    // release fence — cumulative over the MMA warps' stores, which the done barrier ordered
-    // before it at CTA scope — and the counters.  The loader does not load tile x before
-    // tile x - 2S is published, so done[] never runs two phases ahead of this warp.
-    if (lane == 0) {
-      int64_t jj = 0;
-      while (jj < JJ) {
-        mbar_wait(bar_done + int(jj % (2 * S)), unsigned(jj / (2 * S)) & 1);
-        int64_t hi = jj + 1;
-        while (hi < JJ && hi < jj + 2 * S && mbar_test(bar_done + int(hi % (2 * S)), unsigned(hi / (2 * S)) & 1))
-          ++hi;
-        // release stores: cumulative over the MMA warps' stores (ordered before this point
-        // at CTA scope by the done barrier)
-        for (int64_t x = jj; x < hi; ++x) st_release_gpu(fp.flags + tile_of(x), fp.g0 + unsigned(stage_of(x)) + 1u);
-        *published = hi;
-        jj = hi;
+        unsigned bytes = TS * 8 + C::GEOT * 8 + C::IDXT * 4;
+        if (C::RES_SMEM && res_in) bytes += TS * 8;
+        mbar_arrive_tx(bar_load + s, bytes);
+        bulk_g2s(sU(s), p.u_in + tile * TS, TS * 8, bar_load + s);
+        if (C::RES_SMEM && res_in) bulk_g2s(sR(s), p.res + tile * TS, TS * 8, bar_load + s);
+        bulk_g2s(sG(s), p.geo + tile * C::GEOT, C::GEOT * 8, bar_load + s);
+        bulk_g2s(sI(s), p.gidx + tile * C::IDXT, C::IDXT * 4, bar_load + s);
       }
     }
   } else if (warp > C::MW) {
@@ -412,7 +345,7 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
       DG_T0();
       const int32_t* I = sI(s);
       double* F = sF(s);
-      const double* uin = u_in_of(stage_of(j));
+      const double* uin = p.u_in;
       for (int w = ptid; w < E * NF; w += C::PT) {
         const int32_t gi = I[w];
         if (gi >= 0) {  // intra-tile faces (negative codes) need no gather
@@ -489,11 +422,6 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
     };
     // flux warps: tile j's flux, then tile j+LA's trace gather (its bulk load was issued
     // by the loader warp as soon as a slot was free)
-    //
-    // The look-ahead never crosses a stage boundary of a fused launch: the flux warps block
-    // on a stage-g load only after they finished all of stage g-1, so every cross-CTA
-    // dependency wait (loader, verify_from) points at strictly earlier work and the
-    // schedule cannot deadlock.
     DG_T0();
     DG_CNT(7, JJ);
     int64_t issued = 0;  // traces issued for positions < issued
@@ -501,8 +429,8 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
       while (issued < lim) traces(issued++);
     };
     for (int64_t j = 0; j < JJ; ++j) {
-      const int64_t end = stage_end(j);
-      const bool first = j == 0 || (FUSED && j % J == 0);
+      const int64_t end = JJ;
+      const bool first = j == 0;
       issue_upto(first ? (j + C::LA < end ? (C::LA > 0 ? j + C::LA : j + 1) : end) : j + 1);
       flux(j);
       issue_upto(j + 1 + C::LA < end ? j + 1 + C::LA : end);
@@ -512,6 +440,7 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
     // ============================= MMA warps =============================
     const int gid = lane >> 2, tig = lane & 3;
     const int64_t total = JJ * C::T;
+    const int64_t nb = p.bsig ? bsig_ctiles(p.bsig_tiles) : 0;
     int64_t released = 0, waited = -1, lwaited = -1;
     auto release = [&](int64_t jj) {  // this warp is done with tile jj (waits for it to exist first)
       if (waited < jj) {
@@ -519,10 +448,8 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
         waited = jj;
       }
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(bar_empty + int(jj % S));
-        if constexpr (FUSED) mbar_arrive(bar_done + int(jj % (2 * S)));
-      }
+      if (lane == 0) mbar_arrive(bar_empty + int(jj % S));
+      if (jj == nb - 1) signal_boundary(p.bsig, nb, 32 * C::MW, warp == 0 && lane == 0);
     };
     DG_T0();
     for (int64_t q = warp; q < total; q += C::MW) {
@@ -544,10 +471,8 @@ __global__ void __launch_bounds__(FUSED ? WsCfg<N>::NTF : WsCfg<N>::NT, 1)
 #endif
       const int64_t tile = tile_of(j);
       const int ne = count_of(tile);
-      const int gs = stage_of(j);
-      const bool res_in = res_in_of(gs);
-      const double rk_a = rk_a_of(gs), rk_b = rk_b_of(gs);
-      double* const u_out = u_out_of(gs);
+      const double rk_a = p.rk_a, rk_b = p.rk_b;
+      double* const u_out = p.u_out;
       const int t = task % C::MT, g = task / C::MT;
       const int row = 8 * t + gid;
       const double* U = sU(s);
@@ -714,8 +639,8 @@ void launch_stage_ws(const StageParams<double>& p, const double* opsA, int mode,
   using C = WsCfg<N>;
   static PerDevice pd;
   const int sms = sms_for_device(pd, [] {
-      cudaFuncSetAttribute(dg_stage_ws<N, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
-      cudaFuncSetAttribute(dg_stage_ws<N, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+      cudaFuncSetAttribute(dg_stage_ws<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+      cudaFuncSetAttribute(dg_stage_ws<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
   });
   if (p.K <= 0) return;
   // element range [k_begin, k_begin+K) must start on a tile boundary
@@ -723,38 +648,10 @@ void launch_stage_ws(const StageParams<double>& p, const double* opsA, int mode,
   const int64_t tc = (p.k_begin + p.K + C::E - 1) / C::E - t0;
   const int cap = sms - p.sm_reserve > 1 ? sms - p.sm_reserve : 1;  // SMs left to concurrent NCCL kernels
   const unsigned grid = unsigned(tc < cap ? tc : cap);
-  const FusedParams<double> nf{};
   if (mode == 1)
-    launch_pdl(true, dg_stage_ws<N, true, false>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc, nf);
+    launch_pdl(true, dg_stage_ws<N, true>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc);
   else
-    launch_pdl(true, dg_stage_ws<N, false, false>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc, nf);
-}
-
-// Stage-fused launch over all tiles (single rank): grid = min(#tiles, #SMs), one CTA per
-// SM, launched cooperatively so that every CTA is co-resident (the tile-dependency waits
-// need all of them running); returns false if the launch was refused.
-template <int N>
-bool launch_stage_ws_fused(const StageParams<double>& p, const double* opsA, const FusedParams<double>& fp,
-                           cudaStream_t st) {
-  using C = WsCfg<N>;
-  static PerDevice pd;
-  const int sms = sms_for_device(pd, [] {
-      cudaFuncSetAttribute(dg_stage_ws<N, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
-  });
-  if (p.K <= 0 || fp.nst <= 0) return true;
-  const int64_t tc = (p.K + C::E - 1) / C::E;
-  const unsigned grid = unsigned(tc < sms ? tc : sms);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(C::NTF);
-  cfg.dynamicSmemBytes = C::SMEM_BYTES;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, dg_stage_ws<N, true, true>, p, opsA, int64_t(0), tc, fp) == cudaSuccess;
+    launch_pdl(true, dg_stage_ws<N, false>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc);
 }
 
 #ifdef DG_WS_PROFILE

@@ -308,6 +308,7 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
     // ============================= MMA warps =============================
     const int gid = lane >> 2, tig = lane & 3;
     const int64_t total = J * C::T;
+    const int64_t nb = p.bsig ? bsig_ctiles(p.bsig_tiles) : 0;  // boundary tiles (multi-rank signal)
     int64_t released = 0, waited = -1, lwaited = -1;
     auto release = [&](int64_t jj) {
       if (waited < jj) {
@@ -316,6 +317,7 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_empty + int(jj % S));
+      if (jj == nb - 1) signal_boundary(p.bsig, nb, 32 * C::MW, warp == 0 && lane == 0);
     };
     const float* Ahi = C::OPS_SMEM ? sA : opsA;
     const float* Alo = C::OPS_SMEM ? sA + C::A_ONE : opsA + C::OPS_ONE;

@@ -179,8 +179,8 @@ def test_partition_local_order_and_ids():
 
 
 def test_morton_reorder_is_local_permutation():
-    # reorder=1: a permutation of this rank's elements (interior group first, then the
-    # partition-boundary group), with far better centroid locality than a shuffled input
+    # reorder=1: a permutation of this rank's elements (partition-boundary group first, then the
+    # interior group), with far better centroid locality than a shuffled input
     VX, E = di.kuhn_box(6)
     E, _ = di.shuffle_elements(E, 4)
     cen = VX[E].mean(axis=1)

@@ -374,6 +374,38 @@ def test_partitioned_loopback_bitwise_equal_to_one_gpu(P, how, prec, variant):
         assert relerr(U, oracle.lserk4(st, U0, dt, 3)) < 1e-12
 
 
+@pytest.mark.parametrize("prec", [8, 4])
+def test_partitioned_loopback_p8_c4_per_rank_size(prec):
+    # C4 (Kuhn n=56, K = 1 053 696, N = 4) as 8 z-slab partitions of 131 712 elements each
+    # (the per-rank size of the 8-GPU C4 run), AUTO kernels (FP64 DMMA WS, FP32 tcgen05):
+    # boundary-first single-launch stages with the trace exchange beside the interior tiles;
+    # two steps bitwise equal to one solver over the whole mesh (reading R15).
+    N, n, P = 4, 56, 8
+    VX, E = di.kuhn_box(n)
+    K = E.shape[0]
+    U0 = di.random_fields(K, N, seed=8)
+    dt = di.dt_rule(VX, E, N)
+    ref = Solver(N, precision=prec)
+    ref.mesh_upload(VX, E)
+    ref.fields_upload(U0)
+    ref.lserk_step(dt, 2)
+    Uref = ref.fields_download()
+    ref.close()
+    solvers, ids = [], []
+    for r in range(P):
+        sv = Solver(N, precision=prec, rank=r, nranks=P)
+        sv.mesh_upload(VX, E)
+        ids.append(sv.local_elements())
+        assert len(ids[-1]) == K // P
+        sv.fields_upload(U0[:, ids[-1]])
+        solvers.append(sv)
+    group_lserk_step(solvers, dt, 1)
+    group_lserk_step(solvers, dt, 1)                # ghosts stay valid across calls
+    for sv, ix in zip(solvers, ids):
+        assert np.array_equal(sv.fields_download(), Uref[:, ix])
+        sv.close()
+
+
 @pytest.mark.parametrize("N,ns", [(2, (2, 4, 8, 16)), (4, (2, 4, 8)), (6, (1, 2, 4))])
 def test_convergence_study_c3(N, ns):
     # BASELINE.json configs[2] (C3): exact PEC cavity eigenmode (1,1,1) on h-refined

@@ -23,7 +23,7 @@ def _local(rank, P, VX, E, part=None, partition=0):
 
 
 @pytest.mark.parametrize("P", [2, 3, 4])
-def test_local_sets_cover_mesh_interior_first(P):
+def test_local_sets_cover_mesh_boundary_first(P):
     VX, E = di.kuhn_box(4)
     E, _ = di.shuffle_elements(E, 9)
     K = E.shape[0]
@@ -35,11 +35,12 @@ def test_local_sets_cover_mesh_interior_first(P):
         assert np.all(part[ids] == r)
         owner[ids] = r
         allids.append(ids)
-        # interior elements (no face on another rank) first, each group ascending
+        # partition-boundary elements (a face on another rank) first, then the interior ones,
+        # each group ascending (a stage writes the boundary tiles first: DESIGN.md §10)
         bnd = np.array([np.any(part[EToE[k]] != r) for k in ids])
-        nint = int((~bnd).sum())
-        assert not bnd[:nint].any() and bnd[nint:].all()
-        assert np.all(np.diff(ids[:nint]) > 0) and np.all(np.diff(ids[nint:]) > 0)
+        nb = int(bnd.sum())
+        assert bnd[:nb].all() and not bnd[nb:].any()
+        assert np.all(np.diff(ids[:nb]) > 0) and np.all(np.diff(ids[nb:]) > 0)
     assert sorted(np.concatenate(allids).tolist()) == list(range(K))
 
 
