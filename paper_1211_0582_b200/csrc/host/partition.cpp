@@ -201,7 +201,7 @@ void build_face_connectivity(const RefElem& ref, const MeshData& m, const Partit
       const int code = m.orient[4 * k + f];
       const int64_t g = P.ghost_of[4 * l + f];
       if (g >= 0) {
-        fbase[4 * l + f] = int32_t(TileLayout::GHOST_FLAG | (g * L.nc * Nfp));
+        fbase[4 * l + f] = TileLayout::ghost_code(g * L.nc * Nfp);  // negative: local bases reach 2^31 - 1
         fcode[4 * l + f] = uint8_t(code);
       } else {
         fbase[4 * l + f] = int32_t(L.off(P.g2l[k2], 0, 0));

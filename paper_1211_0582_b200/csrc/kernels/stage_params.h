@@ -10,8 +10,8 @@
 //               (component 0); component stride Np for element nodes, Nfp for ghost
 //               traces (offset >= ghost_base); -1 on a PEC boundary face
 //               TC kernel (perm 4): compressed per face instead, per tile [TC_CONNT] int32:
-//               [E][4] word offset of the neighbour's (node 0, component 0), or GHOST_FLAG |
-//               record offset, or -1 (PEC); then [E] x 4 packed u8 codes f2*6 + orientation
+//               [E][4] word offset of the neighbour's (node 0, component 0), or -2 - (ghost
+//               record offset), or -1 (PEC); then [E] x 4 packed u8 codes f2*6 + orientation
 //               (ghost: orientation); the face-node tables ftab rebuild the node (SURVEY §7
 //               hard part 5).  geo is per tile [E][GEO_W] padded to TC_GEOT.
 //   geo         [Kl][GEO_W]: rx ry rz sx sy sz tx ty tz, then 4 x (nx ny nz Fscale)
@@ -78,6 +78,11 @@ struct TileLayout {
   // Ghost records are ghost_base + rec (perm 0/1/3) or GHOST_FLAG | rec (perm 2).
   // -1 is a PEC wall.  Word offsets therefore reach 2^31 - 1 (17 GB of FP64 state per rank).
   static constexpr int32_t GHOST_FLAG = int32_t(1) << 30;
+  // TC kernel (perm 4) per-face connectivity: a ghost record rec is stored as -2 - rec (-1 is a PEC
+  // wall), so the word offsets of local neighbours keep the full int32 range (a flag bit would cut
+  // it to 2^30 words: C4 at N = 9 FP32 holds 1.39e9 words per state copy)
+  static DG_HD int32_t ghost_code(int64_t rec) { return int32_t(-2 - rec); }
+  static DG_HD int32_t ghost_rec(int32_t code) { return -2 - code; }
   // tiled layouts (perm >= 1): a face whose neighbour sits in the SAME tile is encoded as the
   // negative code intra(e2, n2) = -2 - ((e2 << 8) | n2) — the kernel reads u+ from the tile
   // already in shared memory instead of gathering it (the paper's flux-gather granularity,

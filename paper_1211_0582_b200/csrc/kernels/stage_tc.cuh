@@ -656,16 +656,14 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
         for (int c = 0; c < 3; ++c) cp_async8(d + c * PST, src + 2 * c);
         const int32_t b = cn_i[f];
         const int cd = (codes_i >> (8 * f)) & 0xff;
-        if (b >= 0) {
-          if (b & TileLayout::GHOST_FLAG) {
-            const float* g = p.u_in + p.ghost_base + (b & ~TileLayout::GHOST_FLAG) + sGP[cd * Nfp + i];
+        if (b >= 0) {  // local neighbour: word offset of its node 0, component 0
+          const float* g = p.u_in + b + int(sNP[cd * Nfp + i]) * ROWS;
 #pragma unroll
-            for (int c = 0; c < 6; ++c) cp_async4(d + (3 + c / 2) * PST + (c & 1), g + c * Nfp);
-          } else {
-            const float* g = p.u_in + b + int(sNP[cd * Nfp + i]) * ROWS;
+          for (int c = 0; c < 3; ++c) cp_async8(d + (3 + c) * PST, g + 2 * c);
+        } else if (b != -1) {  // partition face: the peer's ghost record (b = -2 - record)
+          const float* g = p.u_in + p.ghost_base + TileLayout::ghost_rec(b) + sGP[cd * Nfp + i];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) cp_async8(d + (3 + c) * PST, g + 2 * c);
-          }
+          for (int c = 0; c < 6; ++c) cp_async4(d + (3 + c / 2) * PST + (c & 1), g + c * Nfp);
         }
       }
       cp_commit();
@@ -708,7 +706,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
         const int f = code & 3;
         const float* gm = gE + 4 * f;
         const float nx = gm[0], ny = gm[1], nz = gm[2], fs = gm[3];
-        const bool wall = cn[f] < 0;
+        const bool wall = cn[f] == -1;  // PEC (ghost records are -2 - record)
         const float* d = stg0 + sc_ * 6 * PST;
         float uM[6], uP[6];
 #pragma unroll

@@ -299,18 +299,20 @@ def test_sampled_oracle_at_c4_size():
     s.close()
 
 
-def test_sampled_oracle_beyond_2pow29_words():
-    # maximum-size edge case: one rank whose state exceeds 2^29 words (FP32 N=9, Kuhn n=41,
-    # K=413,526: 5.46e8 words per copy), so the last elements' gather offsets need bits 29/30
-    # of the int32 index (intra-tile faces are negative codes).  Sampled elements, including
-    # the last one, against the oracle on their face-neighbourhood sub-mesh.
+def test_sampled_oracle_beyond_2pow30_words():
+    # maximum-size edge case: one rank whose state exceeds 2^30 words (FP32 N=9 -> the tcgen05
+    # kernel, Kuhn n=52, K=843,648: 1.11e9 words per copy), so the last elements' neighbour
+    # offsets need bit 30 of the int32 connectivity (ghost records and intra-tile faces are
+    # negative codes; a flag bit here once cut the reach to 2^30 and faulted on C4 at N = 9).
+    # Sampled elements, including the last one, against the oracle on their face-neighbourhood
+    # sub-mesh.
     psutil = pytest.importorskip("psutil")
-    if psutil.virtual_memory().available < 40e9:
-        pytest.skip("needs ~40 GB of host memory for the FP64 host arrays")
-    N, n, prec = 9, 41, 4
+    if psutil.virtual_memory().available < 70e9:
+        pytest.skip("needs ~70 GB of host memory for the FP64 host arrays")
+    N, n, prec = 9, 52, 4
     VX, E = di.kuhn_box(n)
     K = E.shape[0]
-    assert 6 * di.np_of(N) * K > 2 ** 29
+    assert 6 * di.np_of(N) * K > 2 ** 30
     s = Solver(N, precision=prec)
     s.mesh_upload(VX, E)
     EToE, _, _, _ = s.get_maps()
