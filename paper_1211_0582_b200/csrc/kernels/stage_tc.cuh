@@ -60,6 +60,14 @@
 #ifndef DG_TC_RM
 #define DG_TC_RM 4
 #endif
+// Diagnostic knock-outs (timing experiments only; results are wrong when set, never in libdg.so):
+// DG_TC_X = bit mask: 1 flux warps skip the trace gathers and the flux arithmetic (zeros),
+// 2 operand writers skip the slab reads and the G arithmetic, 4 writers skip tcgen05.st,
+// 8 epilogue skips the global loads and stores.  Which removal speeds the kernel up tells which
+// role bounds it (tools/gpu_tc_knockout.sh).
+#ifndef DG_TC_X
+#define DG_TC_X 0
+#endif
 
 namespace dg {
 
@@ -324,7 +332,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
         const float* rp = p.res + base + c0 * ROWS;
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const bool ok = UPDATE && valid && c0 + i < Np;
+          const bool ok = UPDATE && valid && c0 + i < Np && !(DG_TC_X & 8);
           uv[i] = ok ? __ldg(up + i * ROWS) : 0.0f;
           rv[i] = ok && res_in ? rp[i * ROWS] : 0.0f;
         }
@@ -337,7 +345,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
               "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
             : "r"(tmem + (uint32_t(32 * warp) << 16) + uint32_t(a * C::ACC1 + c0)));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (valid) {
+        if (valid && !(DG_TC_X & 8)) {
           float* rp = p.res + base + c0 * ROWS;
           float* op = (UPDATE ? p.u_out : p.rhs_out) + base + c0 * ROWS;
 #pragma unroll
@@ -540,7 +548,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
                 const float* sl = sS + ss * C::SLABF + 6 * e;
 #pragma unroll
                 for (int jj = 0; jj < 8; ++jj) {
-                  const bool ok = valid && 8 * o + jj < Np;
+                  const bool ok = valid && 8 * o + jj < Np && !(DG_TC_X & 2);
                   u1[jj] = ok ? sl[jj * ROWS + f1] : 0.0f;
                   u2[jj] = ok ? sl[jj * ROWS + f2] : 0.0f;
                 }
@@ -598,6 +606,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
               w[jj] = __float_as_uint(vv[bq][jj]);
               w[8 + jj] = __float_as_uint(tf32_lo(vv[bq][jj]));
             }
+            if (!(DG_TC_X & 4))
             asm volatile(
                 "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::
                     "r"(trow + uint32_t(C::a_col(slot))),
@@ -648,7 +657,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
         codes_i = sConn(ji)[4 * E + e];
       }
       const int code = sQ[qi * 8 + kk];  // 0xffff: slot past the last face node
-      if (act_i && code != 0xffff) {
+      if (act_i && code != 0xffff && !(DG_TC_X & 1)) {
         const int f = code & 3, i = (code >> 2) & 63;
         float* d = stg0 + si * 6 * PST;
         const float* src = uT_i + (code >> 8) * ROWS;
@@ -702,7 +711,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
 #endif
       const int code = sQ[q * 8 + kk];
       float fl[6] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
-      if (act && code != 0xffff) {
+      if (act && code != 0xffff && !(DG_TC_X & 1)) {
         const int f = code & 3;
         const float* gm = gE + 4 * f;
         const float nx = gm[0], ny = gm[1], nz = gm[2], fs = gm[3];
