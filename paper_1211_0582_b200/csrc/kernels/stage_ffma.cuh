@@ -102,7 +102,7 @@ struct FfCfg {
   // (tools/gpu_ffma_tune.sh): smaller tiles win where they cost little row padding, since
   // 20 250 / (E x 148) tiles per CTA sets the tail imbalance and the ring depth
   static constexpr int E = (TUNED && DG_FF_E) ? DG_FF_E
-                           : F64 ? (N == 1 ? 32 : N <= 3 ? 16 : N <= 6 ? 8 : 4)
+                           : F64 ? (N <= 3 ? 16 : N <= 6 ? 8 : 4)
                                  : (N == 1 || N == 3) ? 32 : (N == 2 || N == 4 || N == 6) ? 16 : 8;
   static_assert(E == 4 || E == 8 || E == 16 || E == 32, "tile = 4, 8, 16 or 32 elements");
 #ifndef DG_FF_EPL
@@ -142,9 +142,11 @@ struct FfCfg {
   static constexpr int S_DEF = S_FIT > 6 ? 6 : S_FIT;
   // FP32 N = 4: a 3-slot ring with look-ahead 1 beats 4 slots / look-ahead 2 (0.307 vs 0.326 ms,
   // profiles/r1_ffma_tune.jsonl)
-  static constexpr int S = (TUNED && DG_FF_S) ? DG_FF_S : (!F64 && N == 4) ? 3 : S_DEF;
+  // FP64 N = 1: 16-element tiles in an 8-slot ring with a 4-tile trace look-ahead beat 32 / 6 / 2
+  // (C4 1.525 vs 1.590 ms, C2 0.0514 vs 0.0556 ms per step; profiles/r2_ffma_lown.jsonl)
+  static constexpr int S = (TUNED && DG_FF_S) ? DG_FF_S : (!F64 && N == 4) ? 3 : (F64 && N == 1) ? 8 : S_DEF;
   static_assert(S >= 2, "two ring slots at least");
-  static constexpr int LA = (TUNED && DG_FF_LA >= 0) ? DG_FF_LA : S - 2 < 2 ? S - 2 : 2;
+  static constexpr int LA = (TUNED && DG_FF_LA >= 0) ? DG_FF_LA : (F64 && N == 1) ? 4 : S - 2 < 2 ? S - 2 : 2;
   static_assert(LA <= S - 2 || (S == 2 && LA == 0), "look-ahead beyond the ring");
 #ifndef DG_FF_SPLIT
 #define DG_FF_SPLIT -1

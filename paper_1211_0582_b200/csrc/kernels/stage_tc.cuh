@@ -63,7 +63,8 @@
 // Diagnostic knock-outs (timing experiments only; results are wrong when set, never in libdg.so):
 // DG_TC_X = bit mask: 1 flux warps skip the trace gathers and the flux arithmetic (zeros),
 // 2 operand writers skip the slab reads and the G arithmetic, 4 writers skip tcgen05.st,
-// 8 epilogue skips the global loads and stores.  Which removal speeds the kernel up tells which
+// 8 epilogue skips the global loads and stores, 16 the MMA issuer does not wait for its operand
+// chunks (pure issue rate; hangs: kept out of the sweeps), 32 the MMA issuer skips its tcgen05.fence::after_thread_sync.  Which removal speeds the kernel up tells which
 // role bounds it (tools/gpu_tc_knockout.sh).
 #ifndef DG_TC_X
 #define DG_TC_X 0
@@ -109,10 +110,22 @@ struct TcCfg {
 #else
   static constexpr int NACC = 2;
 #endif
-  static constexpr int ACC1 = NP16;                 // column of accumulator 1
-  static constexpr int NA = (512 - NACC * NP16) / 16;
+  // 3xTF32 with two MMAs per chunk where the instruction floor dominates (N <= 6, measured
+  // ~45-60 cycles per M = 128 kind::tf32 MMA up to N ~ 96, tools/tcgen05_peak.cu):
+  //   G . [Op | Op_lo] as ONE MMA of width 2 NP16 (the chunk's hi and lo blocks are adjacent
+  //   8-row core-matrix groups, so they form one B operand), then G_lo . Op into the first half;
+  //   the epilogue adds the halves.  N >= 7: three MMAs of width NP16 (2 NP16 > 192; the pipe is
+  //   throughput-bound there, so fusing would gain nothing).
+#ifdef DG_TC_NOFUSE
+  static constexpr bool FUSE_LO = false;
+#else
+  static constexpr bool FUSE_LO = 2 * NP16 <= 192;
+#endif
+  static constexpr int DW = FUSE_LO ? 2 * NP16 : NP16;  // accumulator columns per tile
+  static constexpr int ACC1 = DW;                   // column of accumulator 1
+  static constexpr int NA = (512 - NACC * DW) / 16;
   static constexpr int RA_T = NA < DG_TC_RA ? NA : DG_TC_RA;
-  static __host__ __device__ constexpr int a_col(int k) { return NACC * NP16 + 16 * k; }
+  static __host__ __device__ constexpr int a_col(int k) { return NACC * DW + 16 * k; }
   static constexpr int al1k(int b) { return (b + 1023) / 1024 * 1024; }
   static constexpr int NTAB = NF + 24 * Nfp + 6 * Nfp + 8 * NFQ;  // int16: Fmask | node | ghost | chunk-slot tables
   static constexpr int FIXED = RS * SLABF * 4 + RM * 2816 + LT * TRC * 4 + LF * FSC * 4 +
@@ -187,6 +200,14 @@ __device__ __forceinline__ void tc_wait(uint64_t* b, unsigned parity) {
       "}\n" ::"r"(smem_u32(b)),
       "r"(parity), "r"(1000000u)
       : "memory");
+}
+// the MMA issuer's waits (DG_TC_MMASPIN: spin instead of the suspend-hint wait, experiment)
+__device__ __forceinline__ void tc_wait_mma(uint64_t* b, unsigned parity) {
+#ifdef DG_TC_MMASPIN
+  mbar_wait(b, parity);
+#else
+  tc_wait(b, parity);
+#endif
 }
 __device__ __forceinline__ float tf32_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 // word offset of (row, kk) inside an 8-k chunk of the canonical K-major layout
@@ -337,14 +358,25 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
           rv[i] = ok && res_in ? rp[i * ROWS] : 0.0f;
         }
       };
-      auto process = [&](int c0, const float (&uv)[16], const float (&rv)[16]) {
-        uint32_t v[16];
+      auto ld16 = [&](uint32_t col, uint32_t (&v)[16]) {
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
             : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
               "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-            : "r"(tmem + (uint32_t(32 * warp) << 16) + uint32_t(a * C::ACC1 + c0)));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            : "r"(tmem + (uint32_t(32 * warp) << 16) + col));
+      };
+      auto process = [&](int c0, const float (&uv)[16], const float (&rv)[16]) {
+        uint32_t v[16];
+        ld16(uint32_t(a * C::ACC1 + c0), v);
+        if constexpr (C::FUSE_LO) {  // D = G.Op_hi + G_lo.Op_hi (first half) + G.Op_lo (second half)
+          uint32_t w[16];
+          ld16(uint32_t(a * C::ACC1 + NP16 + c0), w);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) + __uint_as_float(w[i]));
+        } else {
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        }
         if (valid && !(DG_TC_X & 8)) {
           float* rp = p.res + base + c0 * ROWS;
           float* op = (UPDATE ? p.u_out : p.rhs_out) + base + c0 * ROWS;
@@ -449,21 +481,30 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
     // ============================ MMA issuer ============================
     if (lane == 0) {
       constexpr uint32_t idesc = tc_idesc(128, NP16);
+      constexpr uint32_t idesc2 = tc_idesc(128, C::FUSE_LO ? 2 * NP16 : NP16);  // G . [Op | Op_lo]
       // descriptor of operator slot/chunk 0; other chunks differ only in the start-address
       // field (bits 0..13, address >> 4), so they are db0 + (byte offset >> 4)
       const uint64_t db0 = tc_desc(sB);
       constexpr uint64_t DLO = uint64_t(8 * NP16 * 4) >> 4;  // hi -> lo half of a chunk
       constexpr uint64_t DCH = uint64_t(C::OPC * 4) >> 4;    // next chunk / slot
-      if constexpr (C::OP_RES) tc_wait(b_full, 0);
+      if constexpr (C::OP_RES) tc_wait_mma(b_full, 0);
       int ga = 0;
       for (int j = 0; j < J; ++j) {
         const int a = j % C::NACC;
-        tc_wait(acc_empty + a, (unsigned(j / C::NACC) & 1) ^ 1);
+        tc_wait_mma(acc_empty + a, (unsigned(j / C::NACC) & 1) ^ 1);
         const uint32_t d = tmem + uint32_t(a * C::ACC1);
         for (int s = 0; s < NQ; ++s, ++ga) {
           const int slot = ga % RA;
           TC_T(t0);
-          tc_wait(a_full + slot, unsigned(ga / RA) & 1);
+          // N <= 6: the writers publish a batch of WB chunks together (one tcgen05.wait::st, arrivals
+          // in chunk order), so the batch's last chunk being complete implies the others: one wait +
+          // one fence per batch (N = 1..6 -3..15 %).  N >= 7, where the writers bound the pipe, waiting
+          // per chunk lets the MMA start earlier (per batch: 3-5 % slower there).
+          const bool bstart = !C::FUSE_LO || s % C::WB == 0;
+          if (bstart) {
+            const int last = C::FUSE_LO ? ga + (NQ - s < C::WB ? NQ - s : C::WB) - 1 : ga;
+            tc_wait_mma(a_full + last % RA, unsigned(last / RA) & 1);
+          }
           TC_A(7, t0);
           uint64_t db;
           int b = 0;
@@ -473,16 +514,21 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
             const int g = j * NQ + s;
             b = g % RB;
             TC_T(t2);
-            tc_wait(b_full + b, unsigned(g / RB) & 1);
+            tc_wait_mma(b_full + b, unsigned(g / RB) & 1);
             TC_A(9, t2);
             db = db0 + uint64_t(b) * DCH;
           }
           TC_T(t1);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          if (bstart && !(DG_TC_X & 32)) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t ta = tmem + uint32_t(C::a_col(slot));  // G at ta, G_lo at ta + 8
-          tc_mma_ts(d, ta, db, idesc, s > 0 ? 1u : 0u);              // G . Op
-          tc_mma_ts(d, ta + 8, db, idesc, 1u);                      // G_lo . Op
-          tc_mma_ts(d, ta, db + DLO, idesc, 1u);                    // G . Op_lo
+          if constexpr (C::FUSE_LO) {
+            tc_mma_ts(d, ta, db, idesc2, s > 0 ? 1u : 0u);         // G . [Op | Op_lo]  (2 NP16 columns)
+            tc_mma_ts(d, ta + 8, db, idesc, 1u);                   // G_lo . Op         (first NP16)
+          } else {
+            tc_mma_ts(d, ta, db, idesc, s > 0 ? 1u : 0u);          // G . Op
+            tc_mma_ts(d, ta + 8, db, idesc, 1u);                   // G_lo . Op
+            tc_mma_ts(d, ta, db + DLO, idesc, 1u);                 // G . Op_lo
+          }
           // frees the TMEM operand slots in pairs (one commit per two chunks: ~45 cycles each)
           if (slot & 1) tc_commit(a_empty + (slot >> 1));
           if constexpr (!C::OP_RES) tc_commit(b_empty + b);         // frees the operator slot

@@ -28,7 +28,7 @@ template <int N>
 __global__ void __launch_bounds__(288, 1) probe(int iters, int mode, unsigned long long* cyc) {
   extern __shared__ __align__(1024) unsigned char sm[];
   float* sB = reinterpret_cast<float*>(sm);  // [4 chunks][N x 8] (values irrelevant: timing only)
-  __shared__ uint64_t bar, cbar;
+  __shared__ uint64_t bar, cbar, fbar;
   __shared__ uint32_t tslot;
   __shared__ volatile int done;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(288, 1) probe(int iters, int mode, unsigned lo
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&cbar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&fbar)));  // phase 0 pending: parity 1 passes
     asm volatile("fence.mbarrier_init.release.cluster;");
     done = 0;
   }
@@ -55,6 +56,14 @@ __global__ void __launch_bounds__(288, 1) probe(int iters, int mode, unsigned lo
       constexpr uint32_t id = idesc_tf32(128, N);
       for (int it = 0; it < iters; ++it) {
         for (int q = 0; q < 6; ++q) {
+          if ((mode & 8) && q % 3 == 0) {  // the stage kernel's per-chunk pattern: wait (already complete) + fence
+            asm volatile(
+                "{\n.reg .pred P1;\nWF_%=:\n"
+                "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 1;\n"
+                "@!P1 bra WF_%=;\n}\n" ::"r"(su32(&fbar)));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          }
+          if ((mode & 16) && q % 3 == 0) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           asm volatile(
               "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
               "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem),
@@ -122,9 +131,14 @@ int main() {
   constexpr int N = 48;
   const int smem = 4 * 256 * 8 * 4;
   cudaFuncSetAttribute(probe<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  const char* names[8] = {"alone", "st", "ld", "st+ld", "commit", "st+commit", "ld+commit", "st+ld+commit"};
+  const char* names[32] = {"alone", "st", "ld", "st+ld", "commit", "st+commit", "ld+commit", "st+ld+commit"};
+  names[8] = "wait+fence per 3 MMAs";
+  names[12] = "commit+wait+fence";
+  names[16] = "fence per 3 MMAs";
+  names[23] = "st+ld+commit+fence";
   const int iters = 4000;
-  for (int mode = 0; mode < 8; ++mode) {
+  const int modes[] = {0, 1, 2, 3, 4, 5, 6, 7, 8, 12, 16, 23};
+  for (int mode : modes) {
     probe<N><<<sms, 288, smem>>>(iters, mode, dc);
     cudaError_t e = cudaDeviceSynchronize();
     unsigned long long cyc = 0;
