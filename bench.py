@@ -404,7 +404,8 @@ def main():
     rank, world, local, dist = dist_setup()
     N, prec = args.order, args.precision
     Np = di.np_of(N)
-    workload = (f"C2: Kuhn box n={args.mesh_n} per GPU (K={6 * args.mesh_n ** 3}/GPU), N={N}, LSERK4, "
+    cname = {15: "C2", 56: "C4"}.get(args.mesh_n, "custom")
+    workload = (f"{cname}: Kuhn box n={args.mesh_n} per GPU (K={6 * args.mesh_n ** 3}/GPU), N={N}, LSERK4, "
                 f"PEC walls, upwind flux, U(-1,1) fields (seed 0)")
 
     def config_of(K_total, precision, engine):
