@@ -273,9 +273,10 @@ def run_dg(args, N, prec, rank, world, local, dist, stream, flush, nccl_id, peak
     kernel_ms = ms_step / 5 if world == 1 else s.time_stage_kernel(10)
     res["stage_kernel_ms"] = round(kernel_ms, 5)
     if system == 1:
-        # acoustics runs on the FFMA (AUTO) or BASIC kernel (FMA contractions): alu or hbm by its own F/B
+        # acoustics: the FFMA / BASIC kernels (FMA contractions: alu) or the tcgen05 TC kernel
+        # (3xTF32: tensor), each against its own pipe, or hbm by its own F/B
         res["system"] = "acoustics"
-        res["roofline"] = roofline(N, prec, Kl, kernel_ms, peaks, 1, None, fpe,
+        res["roofline"] = roofline(N, prec, Kl, kernel_ms, peaks, kv, None, fpe,
                                    bytes_per_elem_stage(N, 8 if prec == 8 else 4, 4))
     else:
         res["roofline"] = roofline(N, prec, Kl, kernel_ms, peaks, kv,
@@ -451,7 +452,7 @@ def main():
                     sweep.append({k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()})
         acoustics = []
         if not args.no_sweep:
-            # NEXT-3: the second linear system on the same C2 mesh (AUTO: FFMA kernel, 4 fields)
+            # NEXT-3: the second linear system on the same C2 mesh (AUTO: FFMA / TC kernel, 4 fields)
             import copy
             a3 = copy.copy(args)
             a3.system, a3.variant = 1, 0

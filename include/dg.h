@@ -75,7 +75,7 @@ typedef enum {
                             (FP32: same as BASIC) */
   DG_VARIANT_MMA_WS = 3, /* warp-specialized TMA/mbarrier pipeline; contractions on tensor
                             cores: FP64 DMMA, FP32 3xTF32 HMMA */
-  DG_VARIANT_TC = 4,     /* FP32, N = 1..9: the whole RHS of a 21-element tile as one K-chunked
+  DG_VARIANT_TC = 4,     /* FP32, N = 1..9: the whole RHS of a 21-element (acoustics: 24) tile as one K-chunked
                             tcgen05.mma kind::tf32 GEMM (3xTF32): chain rule + curl folded into
                             the generated operand (written to tensor memory), upwind flux as
                             the lift operand, TMEM accumulators, LSERK update in the epilogue
@@ -95,7 +95,8 @@ typedef enum {
   DG_SYSTEM_ACOUSTICS = 1  /* 4 fields (p, v), rho0 = c = 1: p_t + div v = 0, v_t + grad p = 0;
                               upwind flux (-A_n + alpha |A_n|)[[u]]; rigid walls v.n = 0
                               (mirror p+ = p-, v+ = v- - 2 (n.v-) n); R16/R17.
-                              FFMA (AUTO) and BASIC kernels (MMA/MMA_WS/TC -> DG_ERR_ARG) */
+                              FFMA, TC (FP32) and BASIC kernels; AUTO: FP64 FFMA, FP32 FFMA for
+                              N <= 3 and TC above (MMA/MMA_WS -> DG_ERR_ARG) */
 } dg_system;
 
 typedef struct {

@@ -224,6 +224,13 @@ int auto_variant(bool fp64, int N) {
   return N <= 3 ? DG_VARIANT_FFMA : DG_VARIANT_TC;
 }
 
+// acoustics: FP64 -> FFMA (the DMMA kernels carry the Maxwell curl in their register layout);
+// FP32 -> FFMA below N = 4, TC above (measured, profiles/r2_acoustics_sweep.jsonl)
+int auto_variant_acoustics(bool fp64, int N) {
+  if (fp64) return DG_VARIANT_FFMA;
+  return N <= 3 ? DG_VARIANT_FFMA : DG_VARIANT_TC;
+}
+
 dg_status need_device(dg_solver* s) {
   if (!s) return fail(DG_ERR_ARG, "null solver");
   if (s->host_only) return fail(DG_ERR_STATE, "compute call on a host-only solver (device = -1)");
@@ -484,7 +491,7 @@ dg_status upload_setup(dg_solver* s) {
   } else if (sizeof(T) == 4 && ws) {
     s->lay = dg::ws32_layout_f32(s->N);
   } else if (tc) {
-    s->lay = dg::tc_layout_f32(s->N);
+    s->lay = dg::tc_layout_f32(s->N, s->nc);
   } else {
     s->lay = dg::TileLayout();
     s->lay.nc = s->nc;
@@ -512,9 +519,9 @@ dg_status upload_setup(dg_solver* s) {
   CK(cudaMemsetAsync(s->d_scratch, 0, std::max<int64_t>(twords, 1) * wb, s->stream));
   CK(cudaMalloc((void**)&s->d_stage64, std::max<int64_t>(s->nc * Kl * Np, 1) * sizeof(double)));
   // geometry [Kpad][GEO_W] (padding elements zero); TC kernel (perm 4): per tile [E][GEO_W]
-  // padded to TC_GEOT words, so one tile's record is one 16-B aligned bulk copy
+  // padded to tc_geot(E) words, so one tile's record is one 16-B aligned bulk copy
   const bool tcl = s->lay.perm == 4;
-  const int64_t gstride = tcl ? dg::TC_GEOT : s->lay.E * dg::GEO_W;
+  const int64_t gstride = tcl ? dg::tc_geot(s->lay.E) : s->lay.E * dg::GEO_W;
   std::vector<T> geo(size_t(std::max<int64_t>(s->ntiles * gstride, 1)), T(0));
   for (int64_t l = 0; l < Kl; ++l) {
     const int64_t k = P.local_ids[l];
@@ -769,19 +776,18 @@ dg_status dg_create(const dg_config* cfg, dg_solver** out) {
   if (cfg->partition != DG_PARTITION_RANGES && cfg->partition != DG_PARTITION_RCB)
     return fail(DG_ERR_ARG, "bad partition method");
   if (cfg->system == DG_SYSTEM_ACOUSTICS && cfg->variant != DG_VARIANT_AUTO && cfg->variant != DG_VARIANT_BASIC &&
-      cfg->variant != DG_VARIANT_FFMA)
-    return fail(DG_ERR_ARG, "DG_SYSTEM_ACOUSTICS runs on the BASIC and FFMA kernels only");
+      cfg->variant != DG_VARIANT_FFMA && cfg->variant != DG_VARIANT_TC)
+    return fail(DG_ERR_ARG, "DG_SYSTEM_ACOUSTICS runs on the BASIC, FFMA and (FP32) TC kernels");
   std::unique_ptr<dg_solver> s(new dg_solver());
   s->cfg = *cfg;
   s->N = cfg->order;
   s->fp64 = cfg->precision == 8;
   s->wsize = s->fp64 ? 8 : 4;
   s->nc = cfg->system == DG_SYSTEM_ACOUSTICS ? 4 : 6;
-  // acoustics (NEXT-3): AUTO -> the FFMA kernel (SYS = 1 instance), measured faster than BASIC
-  s->variant = cfg->system == DG_SYSTEM_ACOUSTICS ? (cfg->variant == DG_VARIANT_AUTO ? DG_VARIANT_FFMA : cfg->variant)
-               : cfg->variant == DG_VARIANT_AUTO  ? auto_variant(cfg->precision == 8, cfg->order)
-               : cfg->variant == DG_VARIANT_FUSED ? DG_VARIANT_MMA_WS  // same kernel and layout
-                                                  : cfg->variant;
+  // acoustics (NEXT-3): AUTO -> the measured-best kernel of the SYS = 1 instances
+  s->variant = cfg->variant != DG_VARIANT_AUTO        ? cfg->variant
+               : cfg->system == DG_SYSTEM_ACOUSTICS ? auto_variant_acoustics(cfg->precision == 8, cfg->order)
+                                                    : auto_variant(cfg->precision == 8, cfg->order);
   s->host_only = cfg->device < 0;
   try {
     s->ref = dg::build_ref_elem(s->N);

@@ -9,7 +9,7 @@ namespace dg {
   TileLayout ws_layout_N##n();                                                      \
   TileLayout ws32_layout_N##n();                                                    \
   size_t ws32_ops_count_N##n();                                                     \
-  TileLayout tc_layout_N##n();                                                      \
+  TileLayout tc_layout_N##n(int);                                                   \
   size_t tc_ops_count_N##n();                                                       \
   void tc_ops_N##n(const double*, const double*, const double*, const double*, float*); \
   void ws32_ops_N##n(const double*, const double*, const double*, const double*, float*); \
@@ -62,10 +62,10 @@ void ws32_ops_build(int N, const double* Dr, const double* Ds, const double* Dt,
   if (N >= 1 && N <= 9) t[N - 1](Dr, Ds, Dt, L, out);
 }
 
-TileLayout tc_layout_f32(int N) {
-  static TileLayout (*const t[9])() = {tc_layout_N1, tc_layout_N2, tc_layout_N3, tc_layout_N4, tc_layout_N5,
+TileLayout tc_layout_f32(int N, int nc) {
+  static TileLayout (*const t[9])(int) = {tc_layout_N1, tc_layout_N2, tc_layout_N3, tc_layout_N4, tc_layout_N5,
                                        tc_layout_N6, tc_layout_N7, tc_layout_N8, tc_layout_N9};
-  return (N >= 1 && N <= 9) ? t[N - 1]() : TileLayout{};
+  return (N >= 1 && N <= 9) ? t[N - 1](nc) : TileLayout{};
 }
 size_t tc_ops_count(int N) {
   static size_t (*const t[9])() = {tc_ops_count_N1, tc_ops_count_N2, tc_ops_count_N3, tc_ops_count_N4, tc_ops_count_N5,

@@ -49,7 +49,7 @@ void DG_FN(ffma64_ops)(const double* Dr, const double* Ds, const double* Dt, con
   ffma_ops<double, DG_N>(Dr, Ds, Dt, L, out);
 }
 TileLayout DG_FN(ws32_layout)() { return ws32_layout<DG_N>(); }
-TileLayout DG_FN(tc_layout)() { return tc_layout<DG_N>(); }
+TileLayout DG_FN(tc_layout)(int nc) { return tc_layout<DG_N>(nc); }
 size_t DG_FN(tc_ops_count)() { return TcCfg<DG_N>::OPS_FLOATS; }
 void DG_FN(tc_ops)(const double* Dr, const double* Ds, const double* Dt, const double* L, float* out) {
   tc_ops<DG_N>(Dr, Ds, Dt, L, out);

@@ -13,7 +13,7 @@
 //               [E][4] word offset of the neighbour's (node 0, component 0), or -2 - (ghost
 //               record offset), or -1 (PEC); then [E] x 4 packed u8 codes f2*6 + orientation
 //               (ghost: orientation); the face-node tables ftab rebuild the node (SURVEY §7
-//               hard part 5).  geo is per tile [E][GEO_W] padded to TC_GEOT.
+//               hard part 5).  geo is per tile [E][GEO_W] padded to tc_geot(E).
 //   geo         [Kl][GEO_W]: rx ry rz sx sy sz tx ty tz, then 4 x (nx ny nz Fscale)
 //   ops         Dr | Ds | Dt ([Np][Np] each, row-major) | LIFT ([Np][4Nfp])
 //   fmask       int16 [4*Nfp]
@@ -31,7 +31,8 @@
 namespace dg {
 
 constexpr int GEO_W = 26;  // 25 used (rx..tz, 4 x (n, Fscale)); padded to 16 B for bulk copies
-constexpr int TC_GEOT = 548;   // TC kernel: geometry words per tile (21 x 26, padded to 16 B)
+// TC kernel: geometry words per tile of E elements (E x 26, padded to 16 B; 548 Maxwell, 624 acoustics)
+constexpr int tc_geot(int E) { return (E * GEO_W + 3) / 4 * 4; }
 constexpr int TC_CONNT = 128;  // TC kernel: connectivity words per tile
 
 // Field layout in device memory: element k, component c, node n lives at
@@ -129,7 +130,7 @@ TileLayout ws_layout_f64(int N);   // tiled layout of the FP64 WS kernel for ord
 TileLayout ws32_layout_f32(int N); // tiled layout of the FP32 (3xTF32) WS kernel
 size_t ws32_ops_count(int N);      // floats in its split hi/lo operator buffer
 void ws32_ops_build(int N, const double* Dr, const double* Ds, const double* Dt, const double* LIFT, float* out);
-TileLayout tc_layout_f32(int N);   // tcgen05 (TC) kernel layout, N <= 4 (E = 0 otherwise)
+TileLayout tc_layout_f32(int N, int nc);  // tcgen05 (TC) kernel layout (nc = 6 Maxwell, 4 acoustics)
 TileLayout ffma_layout_f32(int N); // FFMA kernel layout (perm 3)
 size_t ffma_ops_count(int N);      // floats in its transposed operator buffer
 void ffma_ops_build(int N, const double* Dr, const double* Ds, const double* Dt, const double* LIFT, float* out);

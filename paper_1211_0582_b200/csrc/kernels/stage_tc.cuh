@@ -77,19 +77,24 @@ __host__ __device__ constexpr bool tc_is_vol(int v, int f, int NV, int NFQ) {
   return f >= NFQ || (v < NV && v * NFQ <= f * NV);
 }
 
-template <int N>
+template <int N, int SYS = 0>
 struct TcCfg {
   static constexpr int Np = Order<N>::Np, Nfp = Order<N>::Nfp, NF = Order<N>::NF;
-  static constexpr int E = 21;                      // elements per tile
-  static constexpr int ROWS = 6 * E;                // 126 of the 128 MMA rows
+  // SYS 0 Maxwell (6 fields), 1 linear acoustics (4 fields, NEXT-3): the same GEMM with the system's
+  // operand generator and flux.  Acoustics uses 24 elements = 96 rows: 8 x 24 = 192 flux items, one
+  // per flux thread and chunk (32 elements would need 256 flux threads).
+  static constexpr int NC = System<SYS>::NC;
+  static constexpr int E = SYS == 0 ? 21 : 24;      // elements per tile
+  static constexpr int ROWS = NC * E;               // 126 (Maxwell) / 96 (acoustics) of the 128 MMA rows
   static constexpr int NP16 = (Np + 15) / 16 * 16;  // MMA N
   static constexpr int NO = (Np + 7) / 8;           // node octets
   static constexpr int NV = 3 * NO;                 // volume chunks
   static constexpr int NFQ = (NF + 7) / 8;          // flux chunks
   static constexpr int NQ = NV + NFQ;
   static constexpr int TS = (ROWS * Np + 7) / 8 * 8;  // floats per tile (node-major)
-  static constexpr int GEOT = TC_GEOT;              // floats per tile of geometry (21 x 26, padded to 16 B)
-  static constexpr int CONNT = TC_CONNT;            // int32 per tile: fbase [21][4] | fcode [21] (4 x u8) | pad
+  static constexpr int GEOT = tc_geot(E);           // floats per tile of geometry (E x 26, padded to 16 B)
+  static constexpr int CONNT = TC_CONNT;            // int32 per tile: fbase [E][4] | fcode [E] (4 x u8) | pad
+  static constexpr int MSLOT = (GEOT * 4 + CONNT * 4 + 127) / 128 * 128;  // meta ring slot (bytes)
   static_assert(E * GEO_W <= GEOT && 5 * E <= CONNT, "per-tile records");
   static constexpr int SLABF = 1024;                // floats per slab slot (8 x 126 used)
   static constexpr int OPC = 2 * 8 * NP16;          // floats per operator chunk (hi | lo)
@@ -97,7 +102,7 @@ struct TcCfg {
   static constexpr int PW = 6;                      // flux warps: one item per thread and chunk
   static constexpr int FTH = 32 * PW;
   static constexpr int LT = 4;                      // per-thread cp.async trace pipeline depth (chunks)
-  static constexpr int TRC = FTH * 12;              // floats per trace-staging chunk: [6 pairs][FTH][2]
+  static constexpr int TRC = FTH * 2 * NC;          // floats per trace-staging chunk: [NC pairs][FTH][2] (u-, u+)
   static constexpr int LF = DG_TC_LF;               // flux staging ring (chunks) [128 rows][8]
   static constexpr int FSC = 128 * 8;
   static constexpr int RS = DG_TC_RS, RM = DG_TC_RM;
@@ -128,7 +133,7 @@ struct TcCfg {
   static __host__ __device__ constexpr int a_col(int k) { return NACC * DW + 16 * k; }
   static constexpr int al1k(int b) { return (b + 1023) / 1024 * 1024; }
   static constexpr int NTAB = NF + 24 * Nfp + 6 * Nfp + 8 * NFQ;  // int16: Fmask | node | ghost | chunk-slot tables
-  static constexpr int FIXED = RS * SLABF * 4 + RM * 2816 + LT * TRC * 4 + LF * FSC * 4 +
+  static constexpr int FIXED = RS * SLABF * 4 + RM * MSLOT + LT * TRC * 4 + LF * FSC * 4 +
                                (NTAB * 2 + 15) / 16 * 16 + 1024;
   static constexpr bool OP_RES = FIXED + al1k(NQ * OPC * 4) <= 226 * 1024;  // operators resident in smem
   static constexpr int RB_MAX = (226 * 1024 - FIXED) / (OPC * 4);
@@ -142,7 +147,7 @@ struct TcCfg {
   static constexpr int OFF_B = 0;
   static constexpr int OFF_S = OFF_B + al1k(RB * OPC * 4);
   static constexpr int OFF_M = OFF_S + RS * SLABF * 4;   // meta ring: [RM][geo GEOT floats | conn CONNT ints]
-  static constexpr int OFF_TR = OFF_M + RM * 2816;      // trace staging ring [LT][TRC]
+  static constexpr int OFF_TR = OFF_M + RM * MSLOT;     // trace staging ring [LT][TRC]
   static constexpr int OFF_FS = OFF_TR + LT * TRC * 4;  // flux staging ring [LF][FSC]
   static constexpr int OFF_T = OFF_FS + LF * FSC * 4;
   static constexpr int OFF_BAR = OFF_T + (NTAB * 2 + 15) / 16 * 16;
@@ -151,7 +156,7 @@ struct TcCfg {
   static_assert(RA >= 4, "TMEM operand ring depth");
   static_assert(Nfp <= 64 && Np <= 256, "chunk-slot table packing");
   static_assert(RB >= 3, "operator ring depth");
-  static_assert(GEOT * 4 + CONNT * 4 <= 2816, "meta slot");
+  static_assert(8 * ROWS <= SLABF && ROWS <= 128, "slab slot / MMA rows");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   static_assert(FTH >= ITEMS, "one flux item per thread and chunk");
   static_assert(ITEMS <= 2 * 32 * PW, "at most two flux items per thread and chunk");
@@ -240,12 +245,13 @@ inline void tc_prof_reset() {
   } while (0)
 #endif
 
-template <int N, bool UPDATE>
-__global__ void __launch_bounds__(TcCfg<N>::NT, 1)
+template <int N, bool UPDATE, int SYS>
+__global__ void __launch_bounds__(TcCfg<N, SYS>::NT, 1)
     dg_stage_tc(const StageParams<float> p, const float* __restrict__ ops, int t_begin64, int t_count64) {
   // per-CTA counters and word offsets fit 32 bits (dg_mesh_upload bounds a rank's state below 2^31 words)
   const int t_begin = int(t_begin64), t_count = int(t_count64);
-  using C = TcCfg<N>;
+  using C = TcCfg<N, SYS>;
+  constexpr int NC = C::NC;
   constexpr int Np = C::Np, Nfp = C::Nfp, NF = C::NF, E = C::E, ROWS = C::ROWS, NP16 = C::NP16;
   constexpr int NO = C::NO, NV = C::NV, NFQ = C::NFQ, NQ = C::NQ, TS = C::TS;
   constexpr int RB = C::RB, RS = C::RS, RA = C::RA, LF = C::LF, RM = C::RM, LT = C::LT, ITEMS = C::ITEMS;
@@ -262,9 +268,9 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
   int16_t* sFm = reinterpret_cast<int16_t*>(smem + C::OFF_T);
   const int16_t* sNP = sFm + NF;          // [24][Nfp] neighbour node of face node i, by f2*6 + orientation
   const int16_t* sGP = sNP + 24 * Nfp;    // [6][Nfp]  ghost record position, by orientation
-  auto sGeo = [&](int j) { return reinterpret_cast<const float*>(smem + C::OFF_M + int(j % RM) * 2816); };
+  auto sGeo = [&](int j) { return reinterpret_cast<const float*>(smem + C::OFF_M + int(j % RM) * C::MSLOT); };
   auto sConn = [&](int j) {
-    return reinterpret_cast<const int32_t*>(smem + C::OFF_M + int(j % RM) * 2816 + C::GEOT * 4);
+    return reinterpret_cast<const int32_t*>(smem + C::OFF_M + int(j % RM) * C::MSLOT + C::GEOT * 4);
   };
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* b_full = bars;
@@ -339,7 +345,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
     // u and res of a 16-node column group do not depend on the accumulator: they are loaded
     // one group ahead (the first group before waiting for the MMA), so their latency hides
     // behind the MMA / the previous group instead of serializing with the stores.
-    const int r = 32 * warp + lane, e = r / 6;
+    const int r = 32 * warp + lane, e = r / NC;
     const bool res_in = UPDATE && !p.first_stage;
     const int nb = p.bsig ? int(bsig_ctiles(p.bsig_tiles)) : 0;  // boundary tiles (multi-rank signal)
     TC_T(tcta);
@@ -442,8 +448,8 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
             const int ms = j1 % RM;
             if (mbar_test(m_empty + ms, (unsigned(j1 / RM) & 1) ^ 1)) {
               mbar_arrive_tx(m_full + ms, unsigned(C::GEOT * 4 + C::CONNT * 4));
-              bulk_g2s(smem + C::OFF_M + ms * 2816, p.geo + tile * C::GEOT, unsigned(C::GEOT * 4), m_full + ms);
-              bulk_g2s(smem + C::OFF_M + ms * 2816 + C::GEOT * 4, p.gidx + tile * C::CONNT, unsigned(C::CONNT * 4),
+              bulk_g2s(smem + C::OFF_M + ms * C::MSLOT, p.geo + tile * C::GEOT, unsigned(C::GEOT * 4), m_full + ms);
+              bulk_g2s(smem + C::OFF_M + ms * C::MSLOT + C::GEOT * 4, p.gidx + tile * C::CONNT, unsigned(C::CONNT * 4),
                        m_full + ms);
               o1 = 0;
               moved = true;
@@ -543,28 +549,45 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
     // Volume chunk (octet o, derivative d) (a1): G = al_d u_f1 + be_d u_f2 from the slab;
     // flux chunk (a2 + a3): G = the flux warps' values from the staging ring.  Written with
     // tcgen05.st (no generic->async proxy fence on the path), G_lo = G - trunc_tf32(G).
-    const int r = 32 * (warp & 3) + lane, e = r / 6, out = r - 6 * (r / 6);
-    // row -> (first field, its derivative direction, second field, its direction, sign):
+    const int r = 32 * (warp & 3) + lane, e = r / NC, out = r - NC * (r / NC);
+    // Maxwell: row -> (first field, its derivative direction, second field, its direction, sign):
     // rhsE = curl H, rhsH = -curl E;  out: Ex Ey Ez Hx Hy Hz
-    const int f1 = out < 3 ? (out == 0 ? 5 : out == 1 ? 3 : 4) : (out == 3 ? 2 : out == 4 ? 0 : 1);
-    const int f2 = out < 3 ? (out == 0 ? 4 : out == 1 ? 5 : 3) : (out == 3 ? 1 : out == 4 ? 2 : 0);
-    const int x1 = out % 3 == 0 ? 1 : out % 3 == 1 ? 2 : 0;  // curl_x = d_y(.) - d_z(.), cyclic
-    const int x2 = out % 3 == 0 ? 2 : out % 3 == 1 ? 0 : 1;
-    const float sg = out < 3 ? 1.0f : -1.0f;
+    // Acoustics (R16): rhs_p = -div v -> fields vx, vy, vz with directions x, y, z;
+    // rhs_va = -d_a p -> field p with direction a (one term; the others have zero coefficients)
+    int f1, f2, f3 = 0, x1, x2, x3 = 0;
+    float sg;
+    if constexpr (SYS == 0) {
+      f1 = out < 3 ? (out == 0 ? 5 : out == 1 ? 3 : 4) : (out == 3 ? 2 : out == 4 ? 0 : 1);
+      f2 = out < 3 ? (out == 0 ? 4 : out == 1 ? 5 : 3) : (out == 3 ? 1 : out == 4 ? 2 : 0);
+      x1 = out % 3 == 0 ? 1 : out % 3 == 1 ? 2 : 0;  // curl_x = d_y(.) - d_z(.), cyclic
+      x2 = out % 3 == 0 ? 2 : out % 3 == 1 ? 0 : 1;
+      sg = out < 3 ? 1.0f : -1.0f;
+    } else {
+      f1 = out == 0 ? 1 : 0, f2 = out == 0 ? 2 : 0, f3 = out == 0 ? 3 : 0;
+      x1 = out == 0 ? 0 : out - 1, x2 = 1, x3 = 2;
+      sg = -1.0f;
+    }
     const uint32_t trow = tmem + (uint32_t(32 * (warp & 3)) << 16);
     int ga = 0, gs = 0, gf = 0;
     for (int j = 0; j < J; ++j) {
       const int tile = tile_of(j);
       const bool valid = r < ROWS && e < count_of(tile);
       static_assert(C::RA >= C::WB, "TMEM ring holds a writer batch");
-      float al[3], be[3];
+      float al[3], be[3], gm3[3];
       tc_wait(m_full + j % RM, unsigned(j / RM) & 1);
       {
         const float* g = sGeo(j) + (valid ? e : 0) * GEO_W;
 #pragma unroll
-        for (int dd = 0; dd < 3; ++dd) {
-          al[dd] = valid ? sg * g[3 * dd + x1] : 0.0f;
-          be[dd] = valid ? -sg * g[3 * dd + x2] : 0.0f;
+        for (int dd = 0; dd < 3; ++dd) {  // g[3 d + a] = d r_d / d x_a (eq. 6)
+          if constexpr (SYS == 0) {
+            al[dd] = valid ? sg * g[3 * dd + x1] : 0.0f;
+            be[dd] = valid ? -sg * g[3 * dd + x2] : 0.0f;
+            gm3[dd] = 0.0f;
+          } else {
+            al[dd] = valid ? sg * g[3 * dd + x1] : 0.0f;
+            be[dd] = valid && out == 0 ? sg * g[3 * dd + x2] : 0.0f;
+            gm3[dd] = valid && out == 0 ? sg * g[3 * dd + x3] : 0.0f;
+          }
         }
       }
       // generic-proxy reads of a TMA-written (async-proxy) buffer must be ordered before the
@@ -572,7 +595,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(m_empty + j % RM);
-      float u1[8], u2[8];
+      float u1[8], u2[8], u3[8];
       int v = 0, f = 0;
       TC_T(t1);
       // WB steps per batch: one tcgen05.wait::st for WB chunk stores.  For small NQ the whole
@@ -591,12 +614,13 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
                 TC_T(t0);
                 tc_wait(s_full + ss, unsigned(gs / RS) & 1);
                 TC_A(2, t0);
-                const float* sl = sS + ss * C::SLABF + 6 * e;
+                const float* sl = sS + ss * C::SLABF + NC * e;
 #pragma unroll
                 for (int jj = 0; jj < 8; ++jj) {
                   const bool ok = valid && 8 * o + jj < Np && !(DG_TC_X & 2);
                   u1[jj] = ok ? sl[jj * ROWS + f1] : 0.0f;
                   u2[jj] = ok ? sl[jj * ROWS + f2] : 0.0f;
+                  if constexpr (SYS == 1) u3[jj] = ok ? sl[jj * ROWS + f3] : 0.0f;
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // cross-proxy WAR (see above)
                 __syncwarp();
@@ -605,8 +629,14 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
               }
               const float a1 = dd == 0 ? al[0] : dd == 1 ? al[1] : al[2];
               const float b1 = dd == 0 ? be[0] : dd == 1 ? be[1] : be[2];
+              if constexpr (SYS == 0) {
 #pragma unroll
-              for (int jj = 0; jj < 8; ++jj) vv[bq][jj] = a1 * u1[jj] + b1 * u2[jj];
+                for (int jj = 0; jj < 8; ++jj) vv[bq][jj] = a1 * u1[jj] + b1 * u2[jj];
+              } else {
+                const float c1 = dd == 0 ? gm3[0] : dd == 1 ? gm3[1] : gm3[2];
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) vv[bq][jj] = a1 * u1[jj] + b1 * u2[jj] + c1 * u3[jj];
+              }
               ++v;
             } else {
               const int fs = gf % LF;
@@ -615,7 +645,7 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
               TC_A(2, t0);
               const float4* src = reinterpret_cast<const float4*>(sFS + fs * C::FSC + 8 * r);
               const float4 x = src[0], y = src[1];
-              const bool ok = r < ROWS;  // rows 126, 127 of the MMA are padding: keep them zero
+              const bool ok = r < ROWS;  // rows ROWS..127 of the MMA are padding: keep them zero
               vv[bq][0] = ok ? x.x : 0.0f;
               vv[bq][1] = ok ? x.y : 0.0f;
               vv[bq][2] = ok ? x.z : 0.0f;
@@ -685,8 +715,9 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
     const bool item = ft < ITEMS;
     const int TOT = J * NFQ;
     const uint16_t* sQ = reinterpret_cast<const uint16_t*>(sGP + 6 * Nfp);  // [NFQ][8]: f | i << 2 | Fmask << 8
-    float* const stg0 = sTR + 2 * ft;   // this thread's staging words: + (slot * 6 + pair) * 2 * FTH
+    float* const stg0 = sTR + 2 * ft;   // this thread's staging words: + (slot * NC + pair) * 2 * FTH
     constexpr int PST = 2 * C::FTH;     // floats between pairs
+    constexpr int PH = NC / 2;          // component pairs per side (u- pairs 0..PH-1, u+ pairs PH..NC-1)
     // issue side: (tile, chunk) = (ji, qi), staging slot si
     int ji = 0, qi = 0, si = 0;
     bool act_i = false;
@@ -698,27 +729,27 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
         tc_wait(m_full + ji % RM, unsigned(ji / RM) & 1);
         const int tile = tile_of(ji);
         act_i = item && e < count_of(tile);
-        uT_i = p.u_in + tile * TS + 6 * e;
+        uT_i = p.u_in + tile * TS + NC * e;
         cn_i = sConn(ji) + 4 * e;
         codes_i = sConn(ji)[4 * E + e];
       }
       const int code = sQ[qi * 8 + kk];  // 0xffff: slot past the last face node
       if (act_i && code != 0xffff && !(DG_TC_X & 1)) {
         const int f = code & 3, i = (code >> 2) & 63;
-        float* d = stg0 + si * 6 * PST;
+        float* d = stg0 + si * NC * PST;
         const float* src = uT_i + (code >> 8) * ROWS;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) cp_async8(d + c * PST, src + 2 * c);
+        for (int c = 0; c < PH; ++c) cp_async8(d + c * PST, src + 2 * c);
         const int32_t b = cn_i[f];
         const int cd = (codes_i >> (8 * f)) & 0xff;
         if (b >= 0) {  // local neighbour: word offset of its node 0, component 0
           const float* g = p.u_in + b + int(sNP[cd * Nfp + i]) * ROWS;
 #pragma unroll
-          for (int c = 0; c < 3; ++c) cp_async8(d + (3 + c) * PST, g + 2 * c);
+          for (int c = 0; c < PH; ++c) cp_async8(d + (PH + c) * PST, g + 2 * c);
         } else if (b != -1) {  // partition face: the peer's ghost record (b = -2 - record)
           const float* g = p.u_in + p.ghost_base + TileLayout::ghost_rec(b) + sGP[cd * Nfp + i];
 #pragma unroll
-          for (int c = 0; c < 6; ++c) cp_async4(d + (3 + c / 2) * PST + (c & 1), g + c * Nfp);
+          for (int c = 0; c < NC; ++c) cp_async4(d + (PH + c / 2) * PST + (c & 1), g + c * Nfp);
         }
       }
       cp_commit();
@@ -761,37 +792,47 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
         const int f = code & 3;
         const float* gm = gE + 4 * f;
         const float nx = gm[0], ny = gm[1], nz = gm[2], fs = gm[3];
-        const bool wall = cn[f] == -1;  // PEC (ghost records are -2 - record)
-        const float* d = stg0 + sc_ * 6 * PST;
-        float uM[6], uP[6];
+        const bool wall = cn[f] == -1;  // boundary face (ghost records are -2 - record)
+        const float* d = stg0 + sc_ * NC * PST;
+        float uM[NC], uP[NC];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
+        for (int c = 0; c < PH; ++c) {
           const float2 a2 = *reinterpret_cast<const float2*>(d + c * PST);
           uM[2 * c] = a2.x;
           uM[2 * c + 1] = a2.y;
-          const float2 b2 = *reinterpret_cast<const float2*>(d + (3 + c) * PST);
+          const float2 b2 = *reinterpret_cast<const float2*>(d + (PH + c) * PST);
           uP[2 * c] = b2.x;
           uP[2 * c + 1] = b2.y;
         }
-        float dE[3], dH[3];
+        if constexpr (SYS == 0) {
+          float dE[3], dH[3];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {  // PEC wall: E+ = -E-, H+ = H-
-          dE[c] = wall ? -2.0f * uM[c] : uP[c] - uM[c];
-          dH[c] = wall ? 0.0f : uP[c + 3] - uM[c + 3];
+          for (int c = 0; c < 3; ++c) {  // PEC wall: E+ = -E-, H+ = H-
+            dE[c] = wall ? -2.0f * uM[c] : uP[c] - uM[c];
+            dH[c] = wall ? 0.0f : uP[c + 3] - uM[c + 3];
+          }
+          maxwell_flux<float>(nx, ny, nz, p.alpha, dE, dH, fl);
+        } else {  // rigid wall (R17): p+ = p-, v+ = v- - 2 (n.v-) n
+          const float ndv = nx * uM[1] + ny * uM[2] + nz * uM[3];
+          const float dp = wall ? 0.0f : uP[0] - uM[0];
+          float dv[3];
+          dv[0] = wall ? -2.0f * ndv * nx : uP[1] - uM[1];
+          dv[1] = wall ? -2.0f * ndv * ny : uP[2] - uM[2];
+          dv[2] = wall ? -2.0f * ndv * nz : uP[3] - uM[3];
+          acoustic_flux<float>(nx, ny, nz, p.alpha, dp, dv, fl);
         }
-        maxwell_flux<float>(nx, ny, nz, p.alpha, dE, dH, fl);
         const float sc = 0.5f * fs;
 #pragma unroll
-        for (int c = 0; c < 6; ++c) fl[c] *= sc;
+        for (int c = 0; c < NC; ++c) fl[c] *= sc;
       }
       if (++sc_ == LT) sc_ = 0;
       TC_T(t0);
       tc_wait(f_empty + fsl, fph ^ 1);
       TC_A(5, t0);
       if (item) {
-        float* F = sFS + fsl * C::FSC + 48 * e + kk;  // [row 6e + c][kk]
+        float* F = sFS + fsl * C::FSC + 8 * NC * e + kk;  // [row NC e + c][kk]
 #pragma unroll
-        for (int c = 0; c < 6; ++c) F[8 * c] = fl[c];
+        for (int c = 0; c < NC; ++c) F[8 * c] = fl[c];
       }
       if (q == NFQ - 1) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // meta slot: cross-proxy WAR
       __syncwarp();
@@ -823,13 +864,13 @@ __global__ void __launch_bounds__(TcCfg<N>::NT, 1)
   }
 }
 
-template <int N>
-void launch_stage_tc(const StageParams<float>& p, const float* ops, int mode, cudaStream_t st) {
-  using C = TcCfg<N>;
+template <int N, int SYS>
+void launch_stage_tc_sys(const StageParams<float>& p, const float* ops, int mode, cudaStream_t st) {
+  using C = TcCfg<N, SYS>;
   static PerDevice pd;
   const int sms = sms_for_device(pd, [] {
-    cudaFuncSetAttribute(dg_stage_tc<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
-    cudaFuncSetAttribute(dg_stage_tc<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+    cudaFuncSetAttribute(dg_stage_tc<N, true, SYS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+    cudaFuncSetAttribute(dg_stage_tc<N, false, SYS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
   });
   if (p.K <= 0) return;
   const int64_t t0 = p.k_begin / C::E;
@@ -837,20 +878,27 @@ void launch_stage_tc(const StageParams<float>& p, const float* ops, int mode, cu
   const int cap = sms - p.sm_reserve > 1 ? sms - p.sm_reserve : 1;  // SMs left to concurrent NCCL kernels
   const unsigned grid = unsigned(tc < cap ? tc : cap);
   if (mode == 1)
-    launch_pdl(true, dg_stage_tc<N, true>, grid, C::NT, C::SMEM_BYTES, st, p, ops, t0, tc);
+    launch_pdl(true, dg_stage_tc<N, true, SYS>, grid, C::NT, C::SMEM_BYTES, st, p, ops, t0, tc);
   else
-    launch_pdl(true, dg_stage_tc<N, false>, grid, C::NT, C::SMEM_BYTES, st, p, ops, t0, tc);
+    launch_pdl(true, dg_stage_tc<N, false, SYS>, grid, C::NT, C::SMEM_BYTES, st, p, ops, t0, tc);
+}
+template <int N>
+void launch_stage_tc(const StageParams<float>& p, const float* ops, int mode, cudaStream_t st) {
+  if (p.system == 1)
+    launch_stage_tc_sys<N, 1>(p, ops, mode, st);
+  else
+    launch_stage_tc_sys<N, 0>(p, ops, mode, st);
 }
 
-// perm 4: node-major tiles of E elements, (k / E) * TS + n * 6E + 6 (k % E) + c
+// perm 4: node-major tiles of E elements, (k / E) * TS + n * NC E + NC (k % E) + c
 template <int N>
-TileLayout tc_layout() {
-  using C = TcCfg<N>;
+TileLayout tc_layout(int nc) {
   TileLayout L;
-  L.E = C::E;
-  L.LD = C::Np;
+  L.nc = nc;
+  L.E = nc == 4 ? TcCfg<N, 1>::E : TcCfg<N, 0>::E;
+  L.LD = TcCfg<N, 0>::Np;
   L.perm = 4;
-  L.TS = C::TS;
+  L.TS = nc == 4 ? TcCfg<N, 1>::TS : TcCfg<N, 0>::TS;
   return L;
 }
 

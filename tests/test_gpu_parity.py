@@ -449,11 +449,11 @@ from oracle import acoustics as oac  # noqa: E402
 from paper_1211_0582_b200.dg import DG_SYSTEM_ACOUSTICS  # noqa: E402
 
 
-@pytest.mark.parametrize("variant", [1, 6], ids=["basic", "ffma"])
-@pytest.mark.parametrize("prec", [8, 4])
+@pytest.mark.parametrize("prec,variant", [(8, 1), (8, 6), (4, 1), (4, 6), (4, 4)],
+                         ids=["f64-basic", "f64-ffma", "f32-basic", "f32-ffma", "f32-tc"])
 @pytest.mark.parametrize("N", range(1, 10))
 def test_acoustics_rhs_and_steps(N, prec, variant):
-    # the second linear system through the BASIC and FFMA stage kernels (dg_system = 1; AUTO = FFMA):
+    # the second linear system through the BASIC, FFMA and tcgen05 TC stage kernels (dg_system = 1):
     # RHS and 2 LSERK4 steps vs the acoustics oracle on a shuffled/rotated/jittered mesh
     VX, E = mesh(3, 1, 2, 3)
     st = setup("m3", VX, E, N)
@@ -501,6 +501,44 @@ def test_acoustics_alpha0_energy_and_partitions():
         sv.fields_upload(U0[:, ids[-1]])
         solvers.append(sv)
     group_lserk_step(solvers, dt, 3)
+    Up = np.empty_like(U0)
+    for sv, ix in zip(solvers, ids):
+        Up[:, ix] = sv.fields_download()
+        sv.close()
+    assert np.array_equal(Up, Uref)
+
+
+@pytest.mark.parametrize("N", [4, 7])
+def test_acoustics_tc_partitions_and_many_tiles(N):
+    # acoustics through the tcgen05 kernel (24-element tiles, 4-field ghost records, rigid walls) on a
+    # mesh with many tiles per CTA: RHS vs the oracle on sampled elements, and 3 loopback partitions
+    # bitwise equal to one solver after 2 steps (boundary-first single-launch stages)
+    VX, E = mesh(9, 5, 6, 7)
+    K = E.shape[0]
+    U0 = di.random_fields(K, N, seed=9, nfields=4)
+    dt = di.dt_rule(VX, E, N)
+    ref = Solver(N, precision=4, system=DG_SYSTEM_ACOUSTICS, variant=4)
+    ref.mesh_upload(VX, E)
+    EToE, _, _, _ = ref.get_maps()
+    ref.fields_upload(U0)
+    R = ref.rhs()
+    samples = np.array([0, K // 3, K - 1])
+    keep, sVX, sE = _submesh(VX, E, EToE, samples, 1)
+    st = oracle.Setup(sVX, sE, N)
+    Rs = oac.rhs(st, U0[:, keep])
+    assert relerr(R[:, samples], Rs[:, np.searchsorted(keep, samples)]) < TOL_RHS[4]
+    ref.lserk_step(dt, 2)
+    Uref = ref.fields_download()
+    ref.close()
+    part = np.random.default_rng(N).integers(0, 3, K).astype(np.int32)
+    solvers, ids = [], []
+    for r in range(3):
+        sv = Solver(N, precision=4, rank=r, nranks=3, system=DG_SYSTEM_ACOUSTICS, variant=4)
+        sv.mesh_upload(VX, E, part)
+        ids.append(sv.local_elements())
+        sv.fields_upload(U0[:, ids[-1]])
+        solvers.append(sv)
+    group_lserk_step(solvers, dt, 2)
     Up = np.empty_like(U0)
     for sv, ix in zip(solvers, ids):
         Up[:, ix] = sv.fields_download()

@@ -1,5 +1,5 @@
 #!/bin/bash
-# NEXT-3 acoustics: GPU parity (BASIC and FFMA kernels) and C2 timing of both kernels, N=1..9, FP64/FP32.
+# NEXT-3 acoustics: GPU parity (BASIC, FFMA and FP32 TC kernels) and C2 timing of the kernels, N=1..9, FP64/FP32.
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -q -x -k "acoustic" > gpurun_out/pytest_acoustics.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_acoustics.txt
@@ -10,8 +10,8 @@ import torch, bench
 stream = torch.cuda.Stream()
 flush = torch.empty(bench.L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
 peaks = bench.load_peaks()
-for var, name in ((1, "basic"), (6, "ffma")):
-    for prec in (8, 4):
+for var, name in ((6, "ffma"), (4, "tc"), (1, "basic")):
+    for prec in ((8, 4) if var != 4 else (4,)):
         for N in range(1, 10):
             a = argparse.Namespace(mesh_n=15, steps=10, warmup=3, shuffle_seed=None, reorder=False, variant=var, system=1)
             r = bench.run_dg(a, N, prec, 0, 1, 0, None, stream, flush, None, peaks)
