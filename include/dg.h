@@ -95,8 +95,9 @@ typedef enum {
   DG_SYSTEM_ACOUSTICS = 1  /* 4 fields (p, v), rho0 = c = 1: p_t + div v = 0, v_t + grad p = 0;
                               upwind flux (-A_n + alpha |A_n|)[[u]]; rigid walls v.n = 0
                               (mirror p+ = p-, v+ = v- - 2 (n.v-) n); R16/R17.
-                              FFMA, TC (FP32) and BASIC kernels; AUTO: FP64 FFMA, FP32 FFMA for
-                              N <= 3 and TC above (MMA/MMA_WS -> DG_ERR_ARG) */
+                              FFMA, MMA_WS (FP64 DMMA), TC (FP32 tcgen05) and BASIC kernels; AUTO:
+                              FP64 FFMA at N = 1, MMA_WS above; FP32 FFMA for N <= 3, TC above
+                              (MMA, FP32 MMA_WS -> DG_ERR_ARG) */
 } dg_system;
 
 typedef struct {

@@ -224,10 +224,10 @@ int auto_variant(bool fp64, int N) {
   return N <= 3 ? DG_VARIANT_FFMA : DG_VARIANT_TC;
 }
 
-// acoustics: FP64 -> FFMA (the DMMA kernels carry the Maxwell curl in their register layout);
-// FP32 -> FFMA below N = 4, TC above (measured, profiles/r2_acoustics_sweep.jsonl)
+// acoustics (measured on C2, profiles/r2_acoustics_sweep.jsonl): FP64 -> DFMA (FFMA kernel) at N = 1,
+// DMMA (MMA_WS) above; FP32 -> FFMA below N = 4, tcgen05 (TC) above
 int auto_variant_acoustics(bool fp64, int N) {
-  if (fp64) return DG_VARIANT_FFMA;
+  if (fp64) return N == 1 ? DG_VARIANT_FFMA : DG_VARIANT_MMA_WS;
   return N <= 3 ? DG_VARIANT_FFMA : DG_VARIANT_TC;
 }
 
@@ -488,6 +488,8 @@ dg_status upload_setup(dg_solver* s) {
     s->lay.TS = int64_t(s->nc) * s->lay.LD * s->lay.E;
   } else if (sizeof(T) == 8 && ws) {
     s->lay = dg::ws_layout_f64(s->N);
+    s->lay.nc = s->nc;  // acoustics: 4-element column groups of 4 x 4 columns (WsCfg<N, 4>::TS)
+    s->lay.TS = int64_t(s->nc) * s->lay.E * s->lay.LD;
   } else if (sizeof(T) == 4 && ws) {
     s->lay = dg::ws32_layout_f32(s->N);
   } else if (tc) {
@@ -775,9 +777,9 @@ dg_status dg_create(const dg_config* cfg, dg_solver** out) {
   if (cfg->system != DG_SYSTEM_MAXWELL && cfg->system != DG_SYSTEM_ACOUSTICS) return fail(DG_ERR_ARG, "bad system");
   if (cfg->partition != DG_PARTITION_RANGES && cfg->partition != DG_PARTITION_RCB)
     return fail(DG_ERR_ARG, "bad partition method");
-  if (cfg->system == DG_SYSTEM_ACOUSTICS && cfg->variant != DG_VARIANT_AUTO && cfg->variant != DG_VARIANT_BASIC &&
-      cfg->variant != DG_VARIANT_FFMA && cfg->variant != DG_VARIANT_TC)
-    return fail(DG_ERR_ARG, "DG_SYSTEM_ACOUSTICS runs on the BASIC, FFMA and (FP32) TC kernels");
+  if (cfg->system == DG_SYSTEM_ACOUSTICS && (cfg->variant == DG_VARIANT_MMA ||
+                                             (cfg->variant == DG_VARIANT_MMA_WS && cfg->precision != 8)))
+    return fail(DG_ERR_ARG, "DG_SYSTEM_ACOUSTICS runs on the BASIC, FFMA, FP64 MMA_WS (DMMA) and FP32 TC kernels");
   std::unique_ptr<dg_solver> s(new dg_solver());
   s->cfg = *cfg;
   s->N = cfg->order;

@@ -39,7 +39,7 @@ __global__ void k_cm_to_tiles(const S* __restrict__ src, T* __restrict__ dst, in
     if (col < cols && n < Np) {
       int e, c;
       if (L.perm == 1) {
-        const int g = col / 24, q = col - 24 * g, nt = q >> 3, rr = q & 7;
+        const int gw = 4 * L.nc, g = col / gw, q = col - gw * g, nt = q >> 3, rr = q & 7;  // 4-element groups
         e = 4 * g + (rr >> 1);
         c = 2 * nt + (rr & 1);
       } else if (L.perm == 3) {
@@ -80,7 +80,7 @@ __device__ inline bool tile_word_valid(int64_t t, int64_t r, int64_t K, int Np, 
   if (col >= cols || n >= Np) return false;
   int e;
   if (L.perm == 1) {
-    const int g = col / 24, q = col - 24 * g;
+    const int gw = 4 * L.nc, g = col / gw, q = col - gw * g;
     e = 4 * g + ((q & 7) >> 1);
   } else if (L.perm == 3) {
     e = col % L.E;

@@ -59,7 +59,7 @@ struct TileLayout {
   int perm = 0;
   int64_t TS = 0;
   DG_HD int col(int e, int c) const {
-    return perm == 1 ? 24 * (e >> 2) + 8 * (c >> 1) + 2 * (e & 3) + (c & 1) : perm == 3 ? c * E + e : nc * e + c;
+    return perm == 1 ? 4 * nc * (e >> 2) + 8 * (c >> 1) + 2 * (e & 3) + (c & 1) : perm == 3 ? c * E + e : nc * e + c;
   }
   DG_HD int coff(int c) const { return perm == 1 ? 8 * (c >> 1) + (c & 1) : c; }  // perm 0/1: col(e,c) - col(e,0)
   // perm 0/1/3: word offset of component c relative to component 0 of the same (element, node)

@@ -35,9 +35,13 @@ __host__ __device__ constexpr int ldx(int x) {  // smallest >= x with x % 16 in 
 }
 __host__ __device__ constexpr int r16(int bytes) { return (bytes + 15) / 16 * 16; }
 
-template <int N>
+template <int N, int NC = 6>
 struct WsCfg {
   static constexpr int Np = Order<N>::Np, Nfp = Order<N>::Nfp, NF = Order<N>::NF;
+  // NC fields per element (6 Maxwell; 4 linear acoustics, NEXT-3): a 4-element column group is
+  // GW = 4 NC columns = NC / 2 DMMA n-tiles, thread (gid, tig) owning all NC components of
+  // element 4g + tig at node row 8t + gid
+  static constexpr int GW = 4 * NC, NT3 = NC / 2;
   static constexpr int M8 = (Np + 7) / 8 * 8;
   static constexpr int MT = M8 / 8;
   static constexpr int KV = (Np + 3) / 4 * 4;
@@ -118,7 +122,7 @@ struct WsCfg {
 #endif
   static constexpr int G = E / 4;
   static constexpr int T = MT * G;  // tasks per tile
-  static constexpr int TS = 6 * E * LD;
+  static constexpr int TS = NC * E * LD;
   static constexpr int GEOT = E * GEO_W;
   static constexpr int IDXT = E * NF;
   // slot carve-up (bytes, 16-B aligned pieces)
@@ -127,7 +131,7 @@ struct WsCfg {
   static constexpr int OFF_G = OFF_R + (RES_SMEM ? r16(TS * 8) : 0);
   static constexpr int OFF_I = OFF_G + r16(GEOT * 8);
   static constexpr int OFF_F = OFF_I + r16(IDXT * 4);
-  static constexpr int SLOT = OFF_F + r16(6 * E * LDF * 8);
+  static constexpr int SLOT = OFF_F + r16(NC * E * LDF * 8);
   static constexpr int A_BYTES = OPS_SMEM ? r16((3 * M8 * LDA + M8 * LDL) * 8) : 0;
   static constexpr int FM_BYTES = r16(NF * 2);
   // mbarriers load/tr/full/empty [S]
@@ -245,10 +249,11 @@ __device__ unsigned long long g_ws_prof[16];
 // ---------------------------------------------------------------- kernel
 // Tiles [t_begin, t_begin + t_count) of the tiled arrays; p.k_begin/p.K give the
 // element range (tile-aligned start) used to count elements in the last tile.
-template <int N, bool UPDATE>
-__global__ void __launch_bounds__(WsCfg<N>::NT, 1)
+template <int N, bool UPDATE, int SYS = 0>
+__global__ void __launch_bounds__(WsCfg<N, System<SYS>::NC>::NT, 1)
     dg_stage_ws(const StageParams<double> p, const double* __restrict__ opsA, int64_t t_begin, int64_t t_count) {
-  using C = WsCfg<N>;
+  constexpr int NC = System<SYS>::NC, GW = 4 * NC, NT3 = NC / 2;
+  using C = WsCfg<N, NC>;
   constexpr int Np = C::Np, Nfp = C::Nfp, NF = C::NF, M8 = C::M8, KV = C::KV, KL = C::KL;
   constexpr int E = C::E, LD = C::LD, LDF = C::LDF, S = C::S, TS = C::TS;
   extern __shared__ __align__(128) unsigned char smem_ws[];
@@ -352,9 +357,9 @@ __global__ void __launch_bounds__(WsCfg<N>::NT, 1)
           const int e = w / NF, m = w - e * NF;
           const bool ghost = gi >= p.ghost_base;
           const double* src = uin + gi;
-          const int cb = 24 * (e >> 2) + 2 * (e & 3);
+          const int cb = GW * (e >> 2) + 2 * (e & 3);
 #pragma unroll
-          for (int c = 0; c < 6; ++c) {
+          for (int c = 0; c < NC; ++c) {
             const int co = 8 * (c >> 1) + (c & 1);
             cp_async8(F + (cb + co) * LDF + m, src + (ghost ? c * Nfp : co * LD));
           }
@@ -378,44 +383,50 @@ __global__ void __launch_bounds__(WsCfg<N>::NT, 1)
       double* F = sF(s);
       for (int w = ptid; w < E * NF; w += C::PT) {
         const int e = w / NF, m = w - e * NF, f = m / Nfp;
-        const int cb = 24 * (e >> 2) + 2 * (e & 3);
+        const int cb = GW * (e >> 2) + 2 * (e & 3);
+        auto col = [&](int base, int c) { return base + 8 * (c >> 1) + (c & 1); };
         double fl[6] = {0, 0, 0, 0, 0, 0};
         if (e < ne) {
           const double* g = Gm + e * GEO_W + 9 + 4 * f;
           const double nx = g[0], ny = g[1], nz = g[2], fs = g[3];
           const int nM = sFm[m];
-          double uM[6], dE[3], dH[3];
+          double uM[NC], uP[NC];
 #pragma unroll
-          for (int c = 0; c < 6; ++c) uM[c] = U[(cb + 8 * (c >> 1) + (c & 1)) * LD + nM];
+          for (int c = 0; c < NC; ++c) uM[c] = U[col(cb, c) * LD + nM];
           const int32_t gi = I[w];
+          const bool wall = !TileLayout::is_intra(gi) && gi < 0;
           if (TileLayout::is_intra(gi)) {  // neighbour in this tile: u+ from shared memory
             const int e2 = TileLayout::intra_e(gi), n2 = TileLayout::intra_n(gi);
-            const int cb2 = 24 * (e2 >> 2) + 2 * (e2 & 3);
+            const int cb2 = GW * (e2 >> 2) + 2 * (e2 & 3);
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              dE[c] = U[(cb2 + 8 * (c >> 1) + (c & 1)) * LD + n2] - uM[c];
-              dH[c] = U[(cb2 + 8 * ((c + 3) >> 1) + ((c + 3) & 1)) * LD + n2] - uM[c + 3];
-            }
-          } else if (gi >= 0) {
+            for (int c = 0; c < NC; ++c) uP[c] = U[col(cb2, c) * LD + n2];
+          } else {
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              dE[c] = F[(cb + 8 * (c >> 1) + (c & 1)) * LDF + m] - uM[c];
-              dH[c] = F[(cb + 8 * ((c + 3) >> 1) + ((c + 3) & 1)) * LDF + m] - uM[c + 3];
-            }
-          } else {  // PEC wall: E+ = -E-, H+ = H-
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              dE[c] = -2.0 * uM[c];
-              dH[c] = 0.0;
-            }
+            for (int c = 0; c < NC; ++c) uP[c] = wall ? uM[c] : F[col(cb, c) * LDF + m];
           }
-          maxwell_flux<double>(nx, ny, nz, p.alpha, dE, dH, fl);
+          if constexpr (SYS == 0) {
+            double dE[3], dH[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {  // PEC wall: E+ = -E-, H+ = H-
+              dE[c] = wall ? -2.0 * uM[c] : uP[c] - uM[c];
+              dH[c] = wall ? 0.0 : uP[c + 3] - uM[c + 3];
+            }
+            maxwell_flux<double>(nx, ny, nz, p.alpha, dE, dH, fl);
+          } else {  // rigid wall (R17): p+ = p-, v+ = v- - 2 (n.v-) n
+            const double ndv = nx * uM[1] + ny * uM[2] + nz * uM[3];
+            const double dp = wall ? 0.0 : uP[0] - uM[0];
+            double dv[3];
+            dv[0] = wall ? -2.0 * ndv * nx : uP[1] - uM[1];
+            dv[1] = wall ? -2.0 * ndv * ny : uP[2] - uM[2];
+            dv[2] = wall ? -2.0 * ndv * nz : uP[3] - uM[3];
+            acoustic_flux<double>(nx, ny, nz, p.alpha, dp, dv, fl);
+          }
           const double sc = fs * 0.5;
 #pragma unroll
-          for (int c = 0; c < 6; ++c) fl[c] *= sc;
+          for (int c = 0; c < NC; ++c) fl[c] *= sc;
         }
 #pragma unroll
-        for (int c = 0; c < 6; ++c) F[(cb + 8 * (c >> 1) + (c & 1)) * LDF + m] = fl[c];
+        for (int c = 0; c < NC; ++c) F[col(cb, c) * LDF + m] = fl[c];
       }
       DG_ACC(3);
       mbar_arrive(bar_full + s);
@@ -477,31 +488,31 @@ __global__ void __launch_bounds__(WsCfg<N>::NT, 1)
       const int row = 8 * t + gid;
       const double* U = sU(s);
       const double* F = sF(s);
-      double acc[3][3][2];
+      double acc[3][NT3][2];
 #pragma unroll
       for (int b = 0; b < 3; ++b)
 #pragma unroll
-        for (int nt = 0; nt < 3; ++nt) acc[b][nt][0] = acc[b][nt][1] = 0.0;
+        for (int nt = 0; nt < NT3; ++nt) acc[b][nt][0] = acc[b][nt][1] = 0.0;
       // residual through global memory (!RES_SMEM): prefetched into registers now, used
       // in the update after the contractions (hides the load latency behind the DMMAs)
-      double rpre[6];
+      double rpre[NC];
       if constexpr (UPDATE && C::RES_PREFETCH) {
         const int e = 4 * g + tig;
         const int64_t tb = tile * TS + 8 * t + gid;
 #pragma unroll
-        for (int c = 0; c < 6; ++c)
+        for (int c = 0; c < NC; ++c)
           rpre[c] = (res_in && 8 * t + gid < Np && e < ne)
-                        ? p.res[tb + int64_t(24 * g + 8 * (c >> 1) + 2 * tig + (c & 1)) * LD]
+                        ? p.res[tb + int64_t(GW * g + 8 * (c >> 1) + 2 * tig + (c & 1)) * LD]
                         : 0.0;
       }
-      const double* bp = U + (24 * g + gid) * LD + tig;
+      const double* bp = U + (GW * g + gid) * LD + tig;
       if constexpr (C::OPS_SMEM) {
         const double* ap = sA + row * C::LDA + tig;
 #pragma unroll
         for (int kk = 0; kk < KV; kk += 4) {
           const double ar = ap[kk], as = ap[M8 * C::LDA + kk], at = ap[2 * M8 * C::LDA + kk];
 #pragma unroll
-          for (int nt = 0; nt < 3; ++nt) {
+          for (int nt = 0; nt < NT3; ++nt) {
             // node rows k >= Np are layout padding: masked, so the K padding never multiplies
             // whatever the padding holds (NaN-poisoned padding test)
             const double bv = (kk + 4 <= Np || kk + tig < Np) ? bp[nt * 8 * LD + kk] : 0.0;
@@ -525,7 +536,7 @@ __global__ void __launch_bounds__(WsCfg<N>::NT, 1)
           const double as = __ldg(ap + size_t(M8) * KV + kk);
           const double at = __ldg(ap + size_t(2) * M8 * KV + kk);
 #pragma unroll
-          for (int nt = 0; nt < 3; ++nt) {
+          for (int nt = 0; nt < NT3; ++nt) {
             // node rows k >= Np are layout padding: masked, so the K padding never multiplies
             // whatever the padding holds (NaN-poisoned padding test)
             const double bv = (kk + 4 <= Np || kk + tig < Np) ? bp[nt * 8 * LD + kk] : 0.0;
@@ -535,24 +546,32 @@ __global__ void __launch_bounds__(WsCfg<N>::NT, 1)
           }
         }
       }
-      // chain rule (eq. 6) + curl, thread-local (element 4g+tig, node row)
-      double r[3][2];
+      // chain rule (eq. 6) + curl (Maxwell) / -div v, -grad p (acoustics), thread-local
+      // (element 4g+tig, node row); component c lives in r[c >> 1][c & 1]
+      double r[NT3][2];
       {
         const double* Gm = sG(s) + (4 * g + tig) * GEO_W;
-        double dx[6], dy[6], dz[6];
+        double dx[NC], dy[NC], dz[NC];
 #pragma unroll
-        for (int c = 0; c < 6; ++c) {
+        for (int c = 0; c < NC; ++c) {
           const double ur = acc[0][c >> 1][c & 1], us = acc[1][c >> 1][c & 1], ut = acc[2][c >> 1][c & 1];
           dx[c] = Gm[0] * ur + Gm[3] * us + Gm[6] * ut;
           dy[c] = Gm[1] * ur + Gm[4] * us + Gm[7] * ut;
           dz[c] = Gm[2] * ur + Gm[5] * us + Gm[8] * ut;
         }
-        r[0][0] = dy[5] - dz[4];     // d_t Ex = (curl H)_x
-        r[0][1] = dz[3] - dx[5];     // d_t Ey
-        r[1][0] = dx[4] - dy[3];     // d_t Ez
-        r[1][1] = -(dy[2] - dz[1]);  // d_t Hx = -(curl E)_x
-        r[2][0] = -(dz[0] - dx[2]);  // d_t Hy
-        r[2][1] = -(dx[1] - dy[0]);  // d_t Hz
+        if constexpr (SYS == 0) {
+          r[0][0] = dy[5] - dz[4];     // d_t Ex = (curl H)_x
+          r[0][1] = dz[3] - dx[5];     // d_t Ey
+          r[1][0] = dx[4] - dy[3];     // d_t Ez
+          r[1][1] = -(dy[2] - dz[1]);  // d_t Hx = -(curl E)_x
+          r[2][0] = -(dz[0] - dx[2]);  // d_t Hy
+          r[2][1] = -(dx[1] - dy[0]);  // d_t Hz
+        } else {
+          r[0][0] = -(dx[1] + dy[2] + dz[3]);  // d_t p = -div v
+          r[0][1] = -dx[0];                    // d_t v = -grad p
+          r[1][0] = -dy[0];
+          r[1][1] = -dz[0];
+        }
       }
       if (waited < j) {
         long long _tw = clock64();
@@ -565,19 +584,21 @@ __global__ void __launch_bounds__(WsCfg<N>::NT, 1)
         waited = j;
       }
       // lift: r += LIFT . Flux  (two accumulator sets: 6 independent DMMA chains)
-      const double* fp = F + (24 * g + gid) * LDF + tig;
-      double r2[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+      const double* fp = F + (GW * g + gid) * LDF + tig;
+      double r2[NT3][2];
+#pragma unroll
+      for (int nt = 0; nt < NT3; ++nt) r2[nt][0] = r2[nt][1] = 0.0;
       if constexpr (C::OPS_SMEM) {
         const double* lp = sA + 3 * M8 * C::LDA + row * C::LDL + tig;
 #pragma unroll
         for (int kk = 0; kk < KL; kk += 8) {
           const double a0 = lp[kk];
 #pragma unroll
-          for (int nt = 0; nt < 3; ++nt) dmma(r[nt], a0, fp[nt * 8 * LDF + kk]);
+          for (int nt = 0; nt < NT3; ++nt) dmma(r[nt], a0, fp[nt * 8 * LDF + kk]);
           if (kk + 4 < KL) {
             const double a1 = lp[kk + 4];
 #pragma unroll
-            for (int nt = 0; nt < 3; ++nt) dmma(r2[nt], a1, fp[nt * 8 * LDF + kk + 4]);
+            for (int nt = 0; nt < NT3; ++nt) dmma(r2[nt], a1, fp[nt * 8 * LDF + kk + 4]);
           }
         }
       } else {
@@ -592,10 +613,10 @@ __global__ void __launch_bounds__(WsCfg<N>::NT, 1)
           const double a0 = __ldg(lp + kk);
           const double a1 = (kk + 4 < KL) ? __ldg(lp + kk + 4) : 0.0;
 #pragma unroll
-          for (int nt = 0; nt < 3; ++nt) dmma(r[nt], a0, fp[nt * 8 * LDF + kk]);
+          for (int nt = 0; nt < NT3; ++nt) dmma(r[nt], a0, fp[nt * 8 * LDF + kk]);
           if (kk + 4 < KL) {
 #pragma unroll
-            for (int nt = 0; nt < 3; ++nt) dmma(r2[nt], a1, fp[nt * 8 * LDF + kk + 4]);
+            for (int nt = 0; nt < NT3; ++nt) dmma(r2[nt], a1, fp[nt * 8 * LDF + kk + 4]);
           }
         }
       }
@@ -604,8 +625,8 @@ __global__ void __launch_bounds__(WsCfg<N>::NT, 1)
       if (row < Np && e < ne) {
         const int64_t tb = tile * TS + row;
 #pragma unroll
-        for (int c = 0; c < 6; ++c) {
-          const int col = 24 * g + 8 * (c >> 1) + 2 * tig + (c & 1);
+        for (int c = 0; c < NC; ++c) {
+          const int col = GW * g + 8 * (c >> 1) + 2 * tig + (c & 1);
           const int64_t idx = tb + int64_t(col) * LD;
           const double rhs = r[c >> 1][c & 1] + r2[c >> 1][c & 1];
           if (UPDATE) {
@@ -634,13 +655,13 @@ __global__ void __launch_bounds__(WsCfg<N>::NT, 1)
   }
 }
 
-template <int N>
-void launch_stage_ws(const StageParams<double>& p, const double* opsA, int mode, cudaStream_t st) {
-  using C = WsCfg<N>;
+template <int N, int SYS>
+void launch_stage_ws_sys(const StageParams<double>& p, const double* opsA, int mode, cudaStream_t st) {
+  using C = WsCfg<N, System<SYS>::NC>;
   static PerDevice pd;
   const int sms = sms_for_device(pd, [] {
-      cudaFuncSetAttribute(dg_stage_ws<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
-      cudaFuncSetAttribute(dg_stage_ws<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+      cudaFuncSetAttribute(dg_stage_ws<N, true, SYS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+      cudaFuncSetAttribute(dg_stage_ws<N, false, SYS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
   });
   if (p.K <= 0) return;
   // element range [k_begin, k_begin+K) must start on a tile boundary
@@ -649,9 +670,16 @@ void launch_stage_ws(const StageParams<double>& p, const double* opsA, int mode,
   const int cap = sms - p.sm_reserve > 1 ? sms - p.sm_reserve : 1;  // SMs left to concurrent NCCL kernels
   const unsigned grid = unsigned(tc < cap ? tc : cap);
   if (mode == 1)
-    launch_pdl(true, dg_stage_ws<N, true>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc);
+    launch_pdl(true, dg_stage_ws<N, true, SYS>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc);
   else
-    launch_pdl(true, dg_stage_ws<N, false>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc);
+    launch_pdl(true, dg_stage_ws<N, false, SYS>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc);
+}
+template <int N>
+void launch_stage_ws(const StageParams<double>& p, const double* opsA, int mode, cudaStream_t st) {
+  if (p.system == 1)
+    launch_stage_ws_sys<N, 1>(p, opsA, mode, st);
+  else
+    launch_stage_ws_sys<N, 0>(p, opsA, mode, st);
 }
 
 #ifdef DG_WS_PROFILE

@@ -52,11 +52,12 @@ def test_argument_errors():
     with pytest.raises(DGError) as e:
         Solver(3, device=-1, system=2)
     assert e.value.status == dg.DG_ERR_ARG
-    for v, prec in ((2, 4), (3, 4), (3, 8), (4, 8)):  # acoustics: BASIC, FFMA and FP32 TC kernels only
+    for v, prec in ((2, 4), (2, 8), (3, 4), (4, 8)):  # acoustics: BASIC, FFMA, FP64 WS, FP32 TC kernels only
         with pytest.raises(DGError) as e:
             Solver(3, precision=prec, device=-1, variant=v, system=dg.DG_SYSTEM_ACOUSTICS)
         assert e.value.status == dg.DG_ERR_ARG
     Solver(3, precision=4, device=-1, variant=4, system=dg.DG_SYSTEM_ACOUSTICS).close()
+    Solver(3, precision=8, device=-1, variant=3, system=dg.DG_SYSTEM_ACOUSTICS).close()
     s = Solver(3, device=-1, system=dg.DG_SYSTEM_ACOUSTICS)
     assert s.nfields == 4
     for kw in (dict(precision=4), dict(precision=8), dict(rank=0, nranks=2)):  # FUSED: withdrawn in round 2
@@ -207,7 +208,8 @@ def test_morton_reorder_is_local_permutation():
 def test_kernel_variant_auto_resolution():
     # DG_VARIANT_AUTO resolves at dg_create to the measured-best kernel (DESIGN.md §8 NEXT-4 table):
     # FP64 -> FFMA (DFMA) at N=1, MMA_WS (DMMA) otherwise; FP32 -> FFMA at N=1,2,3, TC (tcgen05 3xTF32)
-    # at N=4..9; acoustics -> FFMA (FP64; FP32 N <= 3), TC (FP32 N >= 4).  Explicit variants are reported
+    # at N=4..9; acoustics -> FFMA (FP64 N = 1; FP32 N <= 3), MMA_WS (FP64 N >= 2), TC (FP32 N >= 4).
+    # Explicit variants are reported
     # as requested.
     want = {8: {1: 6, **{n: 3 for n in range(2, 10)}},
             4: {**{n: 6 for n in (1, 2, 3)}, **{n: 4 for n in range(4, 10)}}}
@@ -216,7 +218,8 @@ def test_kernel_variant_auto_resolution():
             s = Solver(N, precision=prec, device=-1)
             assert s.kernel_variant() == v, (prec, N)
             s.close()
-    for prec, N, v in ((8, 4, dg.DG_VARIANT_FFMA), (8, 9, dg.DG_VARIANT_FFMA), (4, 3, dg.DG_VARIANT_FFMA),
+    for prec, N, v in ((8, 1, dg.DG_VARIANT_FFMA), (8, 4, dg.DG_VARIANT_MMA_WS), (8, 9, dg.DG_VARIANT_MMA_WS),
+                       (4, 3, dg.DG_VARIANT_FFMA),
                        (4, 4, dg.DG_VARIANT_TC), (4, 9, dg.DG_VARIANT_TC)):
         s = Solver(N, precision=prec, device=-1, system=dg.DG_SYSTEM_ACOUSTICS)
         assert s.kernel_variant() == v, (prec, N)

@@ -449,11 +449,11 @@ from oracle import acoustics as oac  # noqa: E402
 from paper_1211_0582_b200.dg import DG_SYSTEM_ACOUSTICS  # noqa: E402
 
 
-@pytest.mark.parametrize("prec,variant", [(8, 1), (8, 6), (4, 1), (4, 6), (4, 4)],
-                         ids=["f64-basic", "f64-ffma", "f32-basic", "f32-ffma", "f32-tc"])
+@pytest.mark.parametrize("prec,variant", [(8, 1), (8, 6), (8, 3), (4, 1), (4, 6), (4, 4)],
+                         ids=["f64-basic", "f64-ffma", "f64-ws", "f32-basic", "f32-ffma", "f32-tc"])
 @pytest.mark.parametrize("N", range(1, 10))
 def test_acoustics_rhs_and_steps(N, prec, variant):
-    # the second linear system through the BASIC, FFMA and tcgen05 TC stage kernels (dg_system = 1):
+    # the second linear system through the BASIC, FFMA, FP64 DMMA WS and tcgen05 TC stage kernels:
     # RHS and 2 LSERK4 steps vs the acoustics oracle on a shuffled/rotated/jittered mesh
     VX, E = mesh(3, 1, 2, 3)
     st = setup("m3", VX, E, N)
@@ -508,16 +508,17 @@ def test_acoustics_alpha0_energy_and_partitions():
     assert np.array_equal(Up, Uref)
 
 
-@pytest.mark.parametrize("N", [4, 7])
-def test_acoustics_tc_partitions_and_many_tiles(N):
-    # acoustics through the tcgen05 kernel (24-element tiles, 4-field ghost records, rigid walls) on a
-    # mesh with many tiles per CTA: RHS vs the oracle on sampled elements, and 3 loopback partitions
-    # bitwise equal to one solver after 2 steps (boundary-first single-launch stages)
+@pytest.mark.parametrize("N,prec,variant", [(4, 4, 4), (7, 4, 4), (4, 8, 3), (7, 8, 3)],
+                         ids=["tc-N4", "tc-N7", "ws-N4", "ws-N7"])
+def test_acoustics_tensor_kernels_partitions_and_many_tiles(N, prec, variant):
+    # acoustics through the tensor-core kernels (FP32 tcgen05: 24-element tiles; FP64 DMMA WS: 4 x 4-column
+    # element groups), 4-field ghost records, rigid walls, on a mesh with many tiles per CTA: RHS vs the
+    # oracle on sampled elements, and 3 loopback partitions bitwise equal to one solver after 2 steps
     VX, E = mesh(9, 5, 6, 7)
     K = E.shape[0]
     U0 = di.random_fields(K, N, seed=9, nfields=4)
     dt = di.dt_rule(VX, E, N)
-    ref = Solver(N, precision=4, system=DG_SYSTEM_ACOUSTICS, variant=4)
+    ref = Solver(N, precision=prec, system=DG_SYSTEM_ACOUSTICS, variant=variant)
     ref.mesh_upload(VX, E)
     EToE, _, _, _ = ref.get_maps()
     ref.fields_upload(U0)
@@ -526,14 +527,14 @@ def test_acoustics_tc_partitions_and_many_tiles(N):
     keep, sVX, sE = _submesh(VX, E, EToE, samples, 1)
     st = oracle.Setup(sVX, sE, N)
     Rs = oac.rhs(st, U0[:, keep])
-    assert relerr(R[:, samples], Rs[:, np.searchsorted(keep, samples)]) < TOL_RHS[4]
+    assert relerr(R[:, samples], Rs[:, np.searchsorted(keep, samples)]) < TOL_RHS[prec]
     ref.lserk_step(dt, 2)
     Uref = ref.fields_download()
     ref.close()
     part = np.random.default_rng(N).integers(0, 3, K).astype(np.int32)
     solvers, ids = [], []
     for r in range(3):
-        sv = Solver(N, precision=4, rank=r, nranks=3, system=DG_SYSTEM_ACOUSTICS, variant=4)
+        sv = Solver(N, precision=prec, rank=r, nranks=3, system=DG_SYSTEM_ACOUSTICS, variant=variant)
         sv.mesh_upload(VX, E, part)
         ids.append(sv.local_elements())
         sv.fields_upload(U0[:, ids[-1]])

@@ -10,8 +10,8 @@ import torch, bench
 stream = torch.cuda.Stream()
 flush = torch.empty(bench.L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
 peaks = bench.load_peaks()
-for var, name in ((6, "ffma"), (4, "tc"), (1, "basic")):
-    for prec in ((8, 4) if var != 4 else (4,)):
+for var, name in ((6, "ffma"), (4, "tc"), (3, "ws")):
+    for prec in ((8, 4) if var == 6 else (4,) if var == 4 else (8,)):
         for N in range(1, 10):
             a = argparse.Namespace(mesh_n=15, steps=10, warmup=3, shuffle_seed=None, reorder=False, variant=var, system=1)
             r = bench.run_dg(a, N, prec, 0, 1, 0, None, stream, flush, None, peaks)
