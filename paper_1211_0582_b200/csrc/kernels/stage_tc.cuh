@@ -206,6 +206,16 @@ __device__ __forceinline__ void tc_wait(uint64_t* b, unsigned parity) {
       "r"(parity), "r"(1000000u)
       : "memory");
 }
+// one lane of a converged warp (elect.sync): the MMA issuer's single issuing thread
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p = 0;
+  asm volatile(
+      "{\n.reg .pred P;\n"
+      "elect.sync _|P, 0xffffffff;\n"
+      "selp.b32 %0, 1, 0, P;\n}\n"
+      : "=r"(p));
+  return p != 0;
+}
 // the MMA issuer's waits (DG_TC_MMASPIN: spin instead of the suspend-hint wait, experiment)
 __device__ __forceinline__ void tc_wait_mma(uint64_t* b, unsigned parity) {
 #ifdef DG_TC_MMASPIN
@@ -485,48 +495,60 @@ __global__ void __launch_bounds__(TcCfg<N, SYS>::NT, 1)
     }
   } else if (warp == C::W_MMA) {
     // ============================ MMA issuer ============================
-    if (lane == 0) {
-      constexpr uint32_t idesc = tc_idesc(128, NP16);
-      constexpr uint32_t idesc2 = tc_idesc(128, C::FUSE_LO ? 2 * NP16 : NP16);  // G . [Op | Op_lo]
-      // descriptor of operator slot/chunk 0; other chunks differ only in the start-address
-      // field (bits 0..13, address >> 4), so they are db0 + (byte offset >> 4)
-      const uint64_t db0 = tc_desc(sB);
-      constexpr uint64_t DLO = uint64_t(8 * NP16 * 4) >> 4;  // hi -> lo half of a chunk
-      constexpr uint64_t DCH = uint64_t(C::OPC * 4) >> 4;    // next chunk / slot
-      if constexpr (C::OP_RES) tc_wait_mma(b_full, 0);
-      int ga = 0;
-      for (int j = 0; j < J; ++j) {
-        const int a = j % C::NACC;
-        tc_wait_mma(acc_empty + a, (unsigned(j / C::NACC) & 1) ^ 1);
-        const uint32_t d = tmem + uint32_t(a * C::ACC1);
-        for (int s = 0; s < NQ; ++s, ++ga) {
-          const int slot = ga % RA;
-          TC_T(t0);
-          // N <= 6: the writers publish a batch of WB chunks together (one tcgen05.wait::st, arrivals
-          // in chunk order), so the batch's last chunk being complete implies the others: one wait +
-          // one fence per batch (N = 1..6 -3..15 %).  N >= 7, where the writers bound the pipe, waiting
-          // per chunk lets the MMA start earlier (per batch: 3-5 % slower there).
-          const bool bstart = !C::FUSE_LO || s % C::WB == 0;
-          if (bstart) {
-            const int last = C::FUSE_LO ? ga + (NQ - s < C::WB ? NQ - s : C::WB) - 1 : ga;
-            tc_wait_mma(a_full + last % RA, unsigned(last / RA) & 1);
+    // The whole warp runs the schedule (warp-uniform control flow: ring positions and phases are
+    // kept as incrementing counters, the operand addresses stay in uniform registers) and one
+    // elected lane issues the MMAs and commits.  Round 2 measurement: issued from `if (lane == 0)`
+    // with modulo ring arithmetic, every chunk cost ~70 SASS instructions (R2UR moves, divisions,
+    // an ELECT retry loop per MMA) in one dependent chain, ~450 cycles per chunk at every order.
+    constexpr uint32_t idesc = tc_idesc(128, NP16);
+    constexpr uint32_t idesc2 = tc_idesc(128, C::FUSE_LO ? 2 * NP16 : NP16);  // G . [Op | Op_lo]
+    // descriptor of operator slot/chunk 0; other chunks differ only in the start-address
+    // field (bits 0..13, address >> 4), so they are db0 + (byte offset >> 4)
+    const uint64_t db0 = tc_desc(sB);
+    constexpr uint64_t DLO = uint64_t(8 * NP16 * 4) >> 4;  // hi -> lo half of a chunk
+    constexpr uint64_t DCH = uint64_t(C::OPC * 4) >> 4;    // next chunk / slot
+    const bool leader = elect_one();
+    if constexpr (C::OP_RES) tc_wait_mma(b_full, 0);
+    int slot = 0, bsl = 0;       // operand ring (TMEM) and operator ring positions
+    unsigned aph = 0, bph = 0;   // their phases
+    for (int j = 0; j < J; ++j) {
+      const int a = j % C::NACC;
+      tc_wait_mma(acc_empty + a, (unsigned(j / C::NACC) & 1) ^ 1);
+      const uint32_t d = tmem + uint32_t(a * C::ACC1);
+      int wb = 0;  // position in the writers' batch of WB chunks
+      for (int s = 0; s < NQ; ++s) {
+        TC_T(t0);
+        // N <= 6: the writers publish a batch of WB chunks together (one tcgen05.wait::st, arrivals
+        // in chunk order), so the batch's last chunk being complete implies the others: one wait +
+        // one fence per batch.  N >= 7, where the writers bound the pipe, waiting per chunk lets the
+        // MMA start earlier.
+        const bool bstart = !C::FUSE_LO || wb == 0;
+        if (bstart) {
+          int ls = slot;
+          unsigned lph = aph;
+          if constexpr (C::FUSE_LO) {
+            ls += (NQ - s < C::WB ? NQ - s : C::WB) - 1;
+            if (ls >= RA) {
+              ls -= RA;
+              lph ^= 1u;
+            }
           }
-          TC_A(7, t0);
-          uint64_t db;
-          int b = 0;
-          if constexpr (C::OP_RES) {
-            db = db0 + uint64_t(s) * DCH;
-          } else {
-            const int g = j * NQ + s;
-            b = g % RB;
-            TC_T(t2);
-            tc_wait_mma(b_full + b, unsigned(g / RB) & 1);
-            TC_A(9, t2);
-            db = db0 + uint64_t(b) * DCH;
-          }
-          TC_T(t1);
-          if (bstart && !(DG_TC_X & 32)) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t ta = tmem + uint32_t(C::a_col(slot));  // G at ta, G_lo at ta + 8
+          tc_wait_mma(a_full + ls, lph);
+        }
+        TC_A(7, t0);
+        uint64_t db;
+        if constexpr (C::OP_RES) {
+          db = db0 + uint64_t(s) * DCH;
+        } else {
+          TC_T(t2);
+          tc_wait_mma(b_full + bsl, bph);
+          TC_A(9, t2);
+          db = db0 + uint64_t(bsl) * DCH;
+        }
+        TC_T(t1);
+        if (bstart && !(DG_TC_X & 32)) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t ta = tmem + uint32_t(C::a_col(slot));  // G at ta, G_lo at ta + 8
+        if (leader) {
           if constexpr (C::FUSE_LO) {
             tc_mma_ts(d, ta, db, idesc2, s > 0 ? 1u : 0u);         // G . [Op | Op_lo]  (2 NP16 columns)
             tc_mma_ts(d, ta + 8, db, idesc, 1u);                   // G_lo . Op         (first NP16)
@@ -537,10 +559,22 @@ __global__ void __launch_bounds__(TcCfg<N, SYS>::NT, 1)
           }
           // frees the TMEM operand slots in pairs (one commit per two chunks: ~45 cycles each)
           if (slot & 1) tc_commit(a_empty + (slot >> 1));
-          if constexpr (!C::OP_RES) tc_commit(b_empty + b);         // frees the operator slot
+          if constexpr (!C::OP_RES) tc_commit(b_empty + bsl);       // frees the operator slot
           if (s == NQ - 1) tc_commit(acc_full + a);                 // accumulator complete
-          TC_A(10, t1);
         }
+        __syncwarp();
+        TC_A(10, t1);
+        if (++slot == RA) {
+          slot = 0;
+          aph ^= 1u;
+        }
+        if constexpr (!C::OP_RES) {
+          if (++bsl == RB) {
+            bsl = 0;
+            bph ^= 1u;
+          }
+        }
+        if (++wb == C::WB) wb = 0;
       }
     }
   } else if (warp < C::W_FG0) {

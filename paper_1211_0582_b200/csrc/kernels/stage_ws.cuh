@@ -390,29 +390,46 @@ __global__ void __launch_bounds__(WsCfg<N, System<SYS>::NC>::NT, 1)
           const double* g = Gm + e * GEO_W + 9 + 4 * f;
           const double nx = g[0], ny = g[1], nz = g[2], fs = g[3];
           const int nM = sFm[m];
-          double uM[NC], uP[NC];
+          double uM[NC];
 #pragma unroll
           for (int c = 0; c < NC; ++c) uM[c] = U[col(cb, c) * LD + nM];
           const int32_t gi = I[w];
-          const bool wall = !TileLayout::is_intra(gi) && gi < 0;
-          if (TileLayout::is_intra(gi)) {  // neighbour in this tile: u+ from shared memory
-            const int e2 = TileLayout::intra_e(gi), n2 = TileLayout::intra_n(gi);
-            const int cb2 = GW * (e2 >> 2) + 2 * (e2 & 3);
-#pragma unroll
-            for (int c = 0; c < NC; ++c) uP[c] = U[col(cb2, c) * LD + n2];
-          } else {
-#pragma unroll
-            for (int c = 0; c < NC; ++c) uP[c] = wall ? uM[c] : F[col(cb, c) * LDF + m];
-          }
           if constexpr (SYS == 0) {
             double dE[3], dH[3];
+            if (TileLayout::is_intra(gi)) {  // neighbour in this tile: u+ from shared memory
+              const int e2 = TileLayout::intra_e(gi), n2 = TileLayout::intra_n(gi);
+              const int cb2 = GW * (e2 >> 2) + 2 * (e2 & 3);
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {  // PEC wall: E+ = -E-, H+ = H-
-              dE[c] = wall ? -2.0 * uM[c] : uP[c] - uM[c];
-              dH[c] = wall ? 0.0 : uP[c + 3] - uM[c + 3];
+              for (int c = 0; c < 3; ++c) {
+                dE[c] = U[col(cb2, c) * LD + n2] - uM[c];
+                dH[c] = U[col(cb2, c + 3) * LD + n2] - uM[c + 3];
+              }
+            } else if (gi >= 0) {
+#pragma unroll
+              for (int c = 0; c < 3; ++c) {
+                dE[c] = F[col(cb, c) * LDF + m] - uM[c];
+                dH[c] = F[col(cb, c + 3) * LDF + m] - uM[c + 3];
+              }
+            } else {  // PEC wall: E+ = -E-, H+ = H-
+#pragma unroll
+              for (int c = 0; c < 3; ++c) {
+                dE[c] = -2.0 * uM[c];
+                dH[c] = 0.0;
+              }
             }
             maxwell_flux<double>(nx, ny, nz, p.alpha, dE, dH, fl);
           } else {  // rigid wall (R17): p+ = p-, v+ = v- - 2 (n.v-) n
+            double uP[NC];
+            const bool wall = !TileLayout::is_intra(gi) && gi < 0;
+            if (TileLayout::is_intra(gi)) {
+              const int e2 = TileLayout::intra_e(gi), n2 = TileLayout::intra_n(gi);
+              const int cb2 = GW * (e2 >> 2) + 2 * (e2 & 3);
+#pragma unroll
+              for (int c = 0; c < NC; ++c) uP[c] = U[col(cb2, c) * LD + n2];
+            } else {
+#pragma unroll
+              for (int c = 0; c < NC; ++c) uP[c] = wall ? uM[c] : F[col(cb, c) * LDF + m];
+            }
             const double ndv = nx * uM[1] + ny * uM[2] + nz * uM[3];
             const double dp = wall ? 0.0 : uP[0] - uM[0];
             double dv[3];
