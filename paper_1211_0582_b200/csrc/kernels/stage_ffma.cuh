@@ -178,7 +178,7 @@ struct FfCfg {
   static_assert((TS * W) % 16 == 0 && (GEOT * W) % 16 == 0 && (IDXT * 4) % 16 == 0, "16-B bulk copies");
 };
 
-template <typename T, int N, bool UPDATE, int SYS>
+template <typename T, int N, bool UPDATE, int SYS, bool BSIG = false>
 __global__ void __launch_bounds__(FfCfg<T, N, System<SYS>::NC>::NT, 1)
     dg_stage_ffma(const StageParams<T> p, const T* __restrict__ opsT, int64_t t_begin, int64_t t_count) {
   constexpr int NC = System<SYS>::NC;
@@ -241,15 +241,18 @@ __global__ void __launch_bounds__(FfCfg<T, N, System<SYS>::NC>::NT, 1)
   if (warp == C::CW) {
     // ===================== TMA loader warp (one lane) =====================
     if (lane == 0) {
+      const int64_t nbl = BSIG ? bsig_ctiles(p.bsig_tiles) : 0;  // boundary tiles (multi-rank signal)
       for (int64_t j = 0; j < J; ++j) {
         const int s = int(j % S);
         mbar_wait(bar_empty + s, (unsigned(j / S) & 1) ^ 1);
+        if constexpr (BSIG) loader_signal_after_wait(p.bsig, nbl, j, S);
         const int64_t tile = tile_of(j);
         mbar_arrive_tx(bar_load + s, TS * W + C::GEOT * W + C::IDXT * 4);
         bulk_g2s(sU(s), p.u_in + tile * TS, TS * W, bar_load + s);
         bulk_g2s(sG(s), p.geo + tile * C::GEOT, C::GEOT * W, bar_load + s);
         bulk_g2s(sI(s), p.gidx + tile * C::IDXT, C::IDXT * 4, bar_load + s);
       }
+      if constexpr (BSIG) loader_signal_tail(bar_empty, p.bsig, nbl, J, S);
     }
   } else if (warp > C::CW) {
     // ============================ flux warps ============================
@@ -368,7 +371,6 @@ __global__ void __launch_bounds__(FfCfg<T, N, System<SYS>::NC>::NT, 1)
     constexpr int EPL = C::EPL, EL = C::EL;
     const int el = lane % EL, rg = lane / EL;  // elements el + ep * EL, ep < EPL
     const int64_t total = J * C::MB;
-    const int64_t nb = p.bsig ? bsig_ctiles(p.bsig_tiles) : 0;  // boundary tiles (multi-rank signal)
     int64_t released = 0, waited = -1, lwaited = -1;
     auto release = [&](int64_t jj) {
       if (waited < jj) {
@@ -377,7 +379,6 @@ __global__ void __launch_bounds__(FfCfg<T, N, System<SYS>::NC>::NT, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_empty + int(jj % S));
-      if (jj == nb - 1) signal_boundary(p.bsig, nb, 32 * C::CW, warp == 0 && lane == 0);
     };
     const T* A = C::OPS_SMEM ? sA : opsT;
     auto ld4 = [&](int idx) -> V {  // RB consecutive operator rows, 16 bytes
@@ -541,13 +542,17 @@ void launch_stage_ffma_sys(const StageParams<T>& p, const T* opsT, int mode, cud
                            int(C::SMEM_BYTES));
       cudaFuncSetAttribute(dg_stage_ffma<T, N, false, SYS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            int(C::SMEM_BYTES));
+      cudaFuncSetAttribute(dg_stage_ffma<T, N, true, SYS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(C::SMEM_BYTES));
   });
   if (p.K <= 0) return;
   const int64_t t0 = p.k_begin / C::E;
   const int64_t tc = (p.k_begin + p.K + C::E - 1) / C::E - t0;
   const int cap = sms - p.sm_reserve > 1 ? sms - p.sm_reserve : 1;  // SMs left to concurrent NCCL kernels
   const unsigned grid = unsigned(tc < cap ? tc : cap);
-  if (mode == 1)
+  if (mode == 1 && p.bsig)
+    launch_pdl(true, dg_stage_ffma<T, N, true, SYS, true>, grid, C::NT, C::SMEM_BYTES, st, p, opsT, t0, tc);
+  else if (mode == 1)
     launch_pdl(true, dg_stage_ffma<T, N, true, SYS>, grid, C::NT, C::SMEM_BYTES, st, p, opsT, t0, tc);
   else
     launch_pdl(true, dg_stage_ffma<T, N, false, SYS>, grid, C::NT, C::SMEM_BYTES, st, p, opsT, t0, tc);

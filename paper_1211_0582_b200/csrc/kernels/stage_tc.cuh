@@ -255,7 +255,7 @@ inline void tc_prof_reset() {
   } while (0)
 #endif
 
-template <int N, bool UPDATE, int SYS>
+template <int N, bool UPDATE, int SYS, bool BSIG = false>
 __global__ void __launch_bounds__(TcCfg<N, SYS>::NT, 1)
     dg_stage_tc(const StageParams<float> p, const float* __restrict__ ops, int t_begin64, int t_count64) {
   // per-CTA counters and word offsets fit 32 bits (dg_mesh_upload bounds a rank's state below 2^31 words)
@@ -357,7 +357,6 @@ __global__ void __launch_bounds__(TcCfg<N, SYS>::NT, 1)
     // behind the MMA / the previous group instead of serializing with the stores.
     const int r = 32 * warp + lane, e = r / NC;
     const bool res_in = UPDATE && !p.first_stage;
-    const int nb = p.bsig ? int(bsig_ctiles(p.bsig_tiles)) : 0;  // boundary tiles (multi-rank signal)
     TC_T(tcta);
     for (int j = 0; j < J; ++j) {
       const int a = j % C::NACC;
@@ -430,7 +429,6 @@ __global__ void __launch_bounds__(TcCfg<N, SYS>::NT, 1)
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty + a);
-      if (j == nb - 1) signal_boundary(p.bsig, nb, 128, tid == 0);
       TC_A(1, t1);
 #ifdef DG_WS_PROFILE
       if (tid == 0) atomicAdd(&g_tc_prof[12], 1ull);
@@ -508,12 +506,17 @@ __global__ void __launch_bounds__(TcCfg<N, SYS>::NT, 1)
     constexpr uint64_t DLO = uint64_t(8 * NP16 * 4) >> 4;  // hi -> lo half of a chunk
     constexpr uint64_t DCH = uint64_t(C::OPC * 4) >> 4;    // next chunk / slot
     const bool leader = elect_one();
+    // multi-rank boundary signal (stage_ws.cuh): the epilogue releases tile j's accumulator after its
+    // stores; this warp acquires that release before reusing the accumulator for tile j + NACC
+    const int nbl = BSIG ? int(bsig_ctiles(p.bsig_tiles)) : 0;
     if constexpr (C::OP_RES) tc_wait_mma(b_full, 0);
     int slot = 0, bsl = 0;       // operand ring (TMEM) and operator ring positions
     unsigned aph = 0, bph = 0;   // their phases
     for (int j = 0; j < J; ++j) {
       const int a = j % C::NACC;
       tc_wait_mma(acc_empty + a, (unsigned(j / C::NACC) & 1) ^ 1);
+      if constexpr (BSIG)
+        if (leader) loader_signal_after_wait(p.bsig, nbl, j, C::NACC);
       const uint32_t d = tmem + uint32_t(a * C::ACC1);
       int wb = 0;  // position in the writers' batch of WB chunks
       for (int s = 0; s < NQ; ++s) {
@@ -577,6 +580,8 @@ __global__ void __launch_bounds__(TcCfg<N, SYS>::NT, 1)
         if (++wb == C::WB) wb = 0;
       }
     }
+    if constexpr (BSIG)
+      if (leader) loader_signal_tail(acc_empty, p.bsig, nbl, J, C::NACC);
   } else if (warp < C::W_FG0) {
     // ============ operand writers: G chunks into the TMEM ring, in MMA order ============
     // Lane-owning warps (warp % 4 = TMEM lane quarter): row r = 32 (warp % 4) + lane.
@@ -905,13 +910,16 @@ void launch_stage_tc_sys(const StageParams<float>& p, const float* ops, int mode
   const int sms = sms_for_device(pd, [] {
     cudaFuncSetAttribute(dg_stage_tc<N, true, SYS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
     cudaFuncSetAttribute(dg_stage_tc<N, false, SYS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+    cudaFuncSetAttribute(dg_stage_tc<N, true, SYS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
   });
   if (p.K <= 0) return;
   const int64_t t0 = p.k_begin / C::E;
   const int64_t tc = (p.k_begin + p.K + C::E - 1) / C::E - t0;
   const int cap = sms - p.sm_reserve > 1 ? sms - p.sm_reserve : 1;  // SMs left to concurrent NCCL kernels
   const unsigned grid = unsigned(tc < cap ? tc : cap);
-  if (mode == 1)
+  if (mode == 1 && p.bsig)
+    launch_pdl(true, dg_stage_tc<N, true, SYS, true>, grid, C::NT, C::SMEM_BYTES, st, p, ops, t0, tc);
+  else if (mode == 1)
     launch_pdl(true, dg_stage_tc<N, true, SYS>, grid, C::NT, C::SMEM_BYTES, st, p, ops, t0, tc);
   else
     launch_pdl(true, dg_stage_tc<N, false, SYS>, grid, C::NT, C::SMEM_BYTES, st, p, ops, t0, tc);

@@ -192,6 +192,27 @@ __device__ __forceinline__ void signal_boundary(unsigned* bsig, int64_t nb, int 
     atomicAdd(bsig, unsigned(nb));
   }
 }
+// Ring kernels (WS, WS32, FFMA): the TMA loader lane signals instead of the store warps.  The store
+// warps release tile jj with an mbarrier arrive (release, CTA scope) after their last store of it; the
+// loader acquires that phase (its slot-reuse wait, or an explicit wait after its loop), then fences at
+// GPU scope (cumulative over the acquired stores) and adds nb.  A named barrier in the store warps'
+// release path cost 3-6 % at N = 1..3 even when not taken, so the signal lives here, and only in the
+// BSIG = true kernel instances (multi-rank stages; the code alone cost ~2 % in the single-rank ones).
+// Call with the loader's tile counter j BEFORE its wait for slot reuse (that wait acquires tile j - S).
+__device__ __forceinline__ void loader_signal_after_wait(unsigned* bsig, int64_t nb, int64_t j, int S) {
+  if (bsig && j - S == nb - 1) {
+    __threadfence();
+    atomicAdd(bsig, unsigned(nb));
+  }
+}
+// after the loader's loop: boundary tiles among the CTA's last S tiles were never re-waited
+__device__ __forceinline__ void loader_signal_tail(uint64_t* bar_empty, unsigned* bsig, int64_t nb, int64_t J, int S) {
+  if (bsig && nb > 0 && nb - 1 + S >= J) {
+    mbar_wait(bar_empty + int((nb - 1) % S), unsigned((nb - 1) / S) & 1);
+    __threadfence();
+    atomicAdd(bsig, unsigned(nb));
+  }
+}
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 // no "memory" clobber: consecutive polls may be in flight together (ordering comes from the
@@ -249,7 +270,7 @@ __device__ unsigned long long g_ws_prof[16];
 // ---------------------------------------------------------------- kernel
 // Tiles [t_begin, t_begin + t_count) of the tiled arrays; p.k_begin/p.K give the
 // element range (tile-aligned start) used to count elements in the last tile.
-template <int N, bool UPDATE, int SYS = 0>
+template <int N, bool UPDATE, int SYS = 0, bool BSIG = false>
 __global__ void __launch_bounds__(WsCfg<N, System<SYS>::NC>::NT, 1)
     dg_stage_ws(const StageParams<double> p, const double* __restrict__ opsA, int64_t t_begin, int64_t t_count) {
   constexpr int NC = System<SYS>::NC, GW = 4 * NC, NT3 = NC / 2;
@@ -319,6 +340,7 @@ __global__ void __launch_bounds__(WsCfg<N, System<SYS>::NC>::NT, 1)
     // loads are issued as soon as the MMA warps release tile j - S.
     if (lane == 0) {
       DG_T0();
+      const int64_t nbl = BSIG ? bsig_ctiles(p.bsig_tiles) : 0;  // boundary tiles (multi-rank signal)
       for (int64_t j = 0; j < JJ; ++j) {
         const int s = int(j % S);
         const unsigned u = unsigned(j / S);
@@ -327,6 +349,7 @@ __global__ void __launch_bounds__(WsCfg<N, System<SYS>::NC>::NT, 1)
           mbar_wait(bar_empty + s, (u & 1) ^ 1);
           DG_ACC(0);
         }
+        if constexpr (BSIG) loader_signal_after_wait(p.bsig, nbl, j, S);
         const int64_t tile = tile_of(j);
         unsigned bytes = TS * 8 + C::GEOT * 8 + C::IDXT * 4;
         if (C::RES_SMEM && res_in) bytes += TS * 8;
@@ -336,6 +359,7 @@ __global__ void __launch_bounds__(WsCfg<N, System<SYS>::NC>::NT, 1)
         bulk_g2s(sG(s), p.geo + tile * C::GEOT, C::GEOT * 8, bar_load + s);
         bulk_g2s(sI(s), p.gidx + tile * C::IDXT, C::IDXT * 4, bar_load + s);
       }
+      if constexpr (BSIG) loader_signal_tail(bar_empty, p.bsig, nbl, JJ, S);
     }
   } else if (warp > C::MW) {
     // ============================= flux warps =============================
@@ -468,7 +492,6 @@ __global__ void __launch_bounds__(WsCfg<N, System<SYS>::NC>::NT, 1)
     // ============================= MMA warps =============================
     const int gid = lane >> 2, tig = lane & 3;
     const int64_t total = JJ * C::T;
-    const int64_t nb = p.bsig ? bsig_ctiles(p.bsig_tiles) : 0;
     int64_t released = 0, waited = -1, lwaited = -1;
     auto release = [&](int64_t jj) {  // this warp is done with tile jj (waits for it to exist first)
       if (waited < jj) {
@@ -477,7 +500,6 @@ __global__ void __launch_bounds__(WsCfg<N, System<SYS>::NC>::NT, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_empty + int(jj % S));
-      if (jj == nb - 1) signal_boundary(p.bsig, nb, 32 * C::MW, warp == 0 && lane == 0);
     };
     DG_T0();
     for (int64_t q = warp; q < total; q += C::MW) {
@@ -679,6 +701,7 @@ void launch_stage_ws_sys(const StageParams<double>& p, const double* opsA, int m
   const int sms = sms_for_device(pd, [] {
       cudaFuncSetAttribute(dg_stage_ws<N, true, SYS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
       cudaFuncSetAttribute(dg_stage_ws<N, false, SYS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+      cudaFuncSetAttribute(dg_stage_ws<N, true, SYS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
   });
   if (p.K <= 0) return;
   // element range [k_begin, k_begin+K) must start on a tile boundary
@@ -686,7 +709,9 @@ void launch_stage_ws_sys(const StageParams<double>& p, const double* opsA, int m
   const int64_t tc = (p.k_begin + p.K + C::E - 1) / C::E - t0;
   const int cap = sms - p.sm_reserve > 1 ? sms - p.sm_reserve : 1;  // SMs left to concurrent NCCL kernels
   const unsigned grid = unsigned(tc < cap ? tc : cap);
-  if (mode == 1)
+  if (mode == 1 && p.bsig)
+    launch_pdl(true, dg_stage_ws<N, true, SYS, true>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc);
+  else if (mode == 1)
     launch_pdl(true, dg_stage_ws<N, true, SYS>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc);
   else
     launch_pdl(true, dg_stage_ws<N, false, SYS>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc);

@@ -133,7 +133,7 @@ __device__ __forceinline__ void mma3(float (&c)[4], const unsigned (&ah)[4], con
   hmma_tf32(c, ah, bh0, bh1);
 }
 
-template <int N, bool UPDATE>
+template <int N, bool UPDATE, bool BSIG = false>
 __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
     dg_stage_ws32(const StageParams<float> p, const float* __restrict__ opsA, int64_t t_begin, int64_t t_count) {
   using C = Ws32Cfg<N>;
@@ -199,9 +199,11 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
   if (warp == C::MW) {
     // ===================== TMA loader warp (one lane) =====================
     if (lane == 0) {
+      const int64_t nbl = BSIG ? bsig_ctiles(p.bsig_tiles) : 0;  // boundary tiles (multi-rank signal)
       for (int64_t j = 0; j < J; ++j) {
         const int s = int(j % S);
         mbar_wait(bar_empty + s, (unsigned(j / S) & 1) ^ 1);
+        if constexpr (BSIG) loader_signal_after_wait(p.bsig, nbl, j, S);
         const int64_t tile = tile_of(j);
         unsigned bytes = TS * 4 + C::GEOT * 4 + C::IDXT * 4;
         if (C::RES_SMEM && res_in) bytes += TS * 4;
@@ -211,6 +213,7 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
         bulk_g2s(sG(s), p.geo + tile * C::GEOT, C::GEOT * 4, bar_load + s);
         bulk_g2s(sI(s), p.gidx + tile * C::IDXT, C::IDXT * 4, bar_load + s);
       }
+      if constexpr (BSIG) loader_signal_tail(bar_empty, p.bsig, nbl, J, S);
     }
   } else if (warp > C::MW) {
     // ============================ flux warps ============================
@@ -308,7 +311,6 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
     // ============================= MMA warps =============================
     const int gid = lane >> 2, tig = lane & 3;
     const int64_t total = J * C::T;
-    const int64_t nb = p.bsig ? bsig_ctiles(p.bsig_tiles) : 0;  // boundary tiles (multi-rank signal)
     int64_t released = 0, waited = -1, lwaited = -1;
     auto release = [&](int64_t jj) {
       if (waited < jj) {
@@ -317,7 +319,6 @@ __global__ void __launch_bounds__(Ws32Cfg<N>::NT, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_empty + int(jj % S));
-      if (jj == nb - 1) signal_boundary(p.bsig, nb, 32 * C::MW, warp == 0 && lane == 0);
     };
     const float* Ahi = C::OPS_SMEM ? sA : opsA;
     const float* Alo = C::OPS_SMEM ? sA + C::A_ONE : opsA + C::OPS_ONE;
@@ -490,13 +491,16 @@ void launch_stage_ws32(const StageParams<float>& p, const float* opsA, int mode,
   const int sms = sms_for_device(pd, [] {
       cudaFuncSetAttribute(dg_stage_ws32<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
       cudaFuncSetAttribute(dg_stage_ws32<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
+      cudaFuncSetAttribute(dg_stage_ws32<N, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM_BYTES));
   });
   if (p.K <= 0) return;
   const int64_t t0 = p.k_begin / C::E;
   const int64_t tc = (p.k_begin + p.K + C::E - 1) / C::E - t0;
   const int cap = sms - p.sm_reserve > 1 ? sms - p.sm_reserve : 1;  // SMs left to concurrent NCCL kernels
   const unsigned grid = unsigned(tc < cap ? tc : cap);
-  if (mode == 1)
+  if (mode == 1 && p.bsig)
+    launch_pdl(true, dg_stage_ws32<N, true, true>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc);
+  else if (mode == 1)
     launch_pdl(true, dg_stage_ws32<N, true>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc);
   else
     launch_pdl(true, dg_stage_ws32<N, false>, grid, C::NT, C::SMEM_BYTES, st, p, opsA, t0, tc);
