@@ -43,7 +43,7 @@
 #include "stage_ws.cuh"
 
 #ifndef DG_TC_WB
-#define DG_TC_WB 3
+#define DG_TC_WB 0
 #endif
 #ifndef DG_TC_RA
 #define DG_TC_RA 12
@@ -106,7 +106,9 @@ struct TcCfg {
   static constexpr int LF = DG_TC_LF;               // flux staging ring (chunks) [128 rows][8]
   static constexpr int FSC = 128 * 8;
   static constexpr int RS = DG_TC_RS, RM = DG_TC_RM;
-  static constexpr int WB = DG_TC_WB;               // operand chunks per writer batch (one wait::st)
+  // operand chunks per writer batch (one tcgen05.wait::st): 3, or 4 at N = 6, 9 (measured on C2,
+  // tools/gpu_tc_tune.sh: N = 6 -3.5 %, N = 9 -2 %; N = 3, 4 +1.5 % with 4)
+  static constexpr int WB = DG_TC_WB ? DG_TC_WB : (N == 6 || N == 9) ? 4 : 3;
   static constexpr int WUNR = NQ <= 36 ? (NQ + WB - 1) / WB : 1;
   // generated operand G in TENSOR memory (kind::tf32 A operand: lane = row, one column per k):
   // ring slots of 16 columns (8 G | 8 G_lo) after the two accumulators
