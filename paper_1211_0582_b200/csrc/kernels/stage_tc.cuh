@@ -57,6 +57,9 @@
 #ifndef DG_TC_RS
 #define DG_TC_RS 4
 #endif
+#ifndef DG_TC_LT
+#define DG_TC_LT 4
+#endif
 #ifndef DG_TC_RM
 #define DG_TC_RM 4
 #endif
@@ -101,7 +104,7 @@ struct TcCfg {
   static constexpr int ITEMS = 8 * E;               // flux items (element, face-node slot) per chunk
   static constexpr int PW = 6;                      // flux warps: one item per thread and chunk
   static constexpr int FTH = 32 * PW;
-  static constexpr int LT = 4;                      // per-thread cp.async trace pipeline depth (chunks)
+  static constexpr int LT = DG_TC_LT;               // per-thread cp.async trace pipeline depth (chunks)
   static constexpr int TRC = FTH * 2 * NC;          // floats per trace-staging chunk: [NC pairs][FTH][2] (u-, u+)
   static constexpr int LF = DG_TC_LF;               // flux staging ring (chunks) [128 rows][8]
   static constexpr int FSC = 128 * 8;
