@@ -11,7 +11,8 @@ def main(path):
     e = d["e2e"]
     cpu = d.get("cpu_baseline") or {}
     out = []
-    out.append("## 4. Measured on B200 (round 1; `bench.py`, config C2: Kuhn n=15, K = 20 250, 1 GPU)\n")
+    tag = sys.argv[2] if len(sys.argv) > 2 else "round 2"
+    out.append(f"## 4. Measured on B200 ({tag}; `bench.py`, config C2: Kuhn n=15, K = 20 250, 1 GPU)\n")
     out.append(f"Headline: N={d['config']['order']} {d['dtype'].upper()}, {d['value'] / 1e9:.2f} G DOF-updates/s = "
                f"{r['achieved']:.2f} TFLOP/s ({100 * r['frac']:.1f}% of the measured FP64 DMMA peak), "
                f"{d['ms_per_step']:.4f} ms per LSERK4 step.")
