@@ -96,15 +96,19 @@ def ws_kind(N, prec, variant):
 
 
 def load_traffic(N, prec, variant, K):
-    """Per-launch DRAM bytes of the stage kernel from a committed ncu --set full capture of
-    the same (precision, variant, order, mesh size), if any."""
-    p = os.path.join(ROOT, "profiles", "r1_traffic.json")
-    try:
-        with open(p) as fh:
-            t = json.load(fh)
-        return t.get(f"{'f64' if prec == 8 else 'f32'}:{variant}:{N}:K{K}", {}).get("dram_bytes")
-    except Exception:
-        return None
+    """Per-launch DRAM bytes of the stage kernel from committed ncu captures of the same (precision,
+    variant, order, mesh size), if any: profiles/r2_traffic.json (a stage that reads the residual;
+    tools/traffic_table.py), else round 1's profiles/r1_traffic.json."""
+    key = f"{'f64' if prec == 8 else 'f32'}:{variant}:{N}:K{K}"
+    for name in ("r2_traffic.json", "r1_traffic.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as fh:
+                v = json.load(fh).get(key, {}).get("dram_bytes")
+            if v:
+                return v
+        except Exception:
+            pass
+    return None
 
 
 def roofline(N, prec, K_total, kernel_ms, peaks, variant=0, traffic=None, fpe=None, bpe=None):
