@@ -167,30 +167,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
 __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* b) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
 }
-__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 // Multi-rank stages ("boundary-first stage"): the tiles [0, p.bsig_tiles) of the
 // launch hold the partition-boundary elements.  bsig_ctiles() is the number of them this CTA
-// processes (its first tiles, j < nb).  Once every store warp of the CTA has finished them,
-// signal_boundary() adds nb to *p.bsig with release semantics; the comm stream waits for the
-// total (cuStreamWaitValue32: a front-end wait, no SM is held) and then packs and sends the
-// next stage's traces while the interior tiles are still running.  No kernel ever waits on it.
+// processes (its first tiles, j < nb).  Once the CTA has written all of them, one thread adds nb to
+// *p.bsig (GPU-scope fence first); the comm stream waits for the total (cuStreamWaitValue32: a
+// front-end wait, no SM is held) and then packs and sends the next stage's traces while the interior
+// tiles are still running.  No kernel ever waits on it.
 __device__ __forceinline__ int64_t bsig_ctiles(int64_t nbt) {
   return nbt > int64_t(blockIdx.x) ? (nbt - int64_t(blockIdx.x) + gridDim.x - 1) / gridDim.x : 0;
-}
-// called by all threads of the CTA's store warps (nthreads = 32 x warps), exactly once
-__device__ __forceinline__ void signal_boundary(unsigned* bsig, int64_t nb, int nthreads, bool leader) {
-  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");  // their stores precede the barrier
-  if (leader) {
-    __threadfence();  // cumulative: every store ordered before the barrier is visible GPU-wide
-    atomicAdd(bsig, unsigned(nb));
-  }
 }
 // Ring kernels (WS, WS32, FFMA): the TMA loader lane signals instead of the store warps.  The store
 // warps release tile jj with an mbarrier arrive (release, CTA scope) after their last store of it; the
@@ -198,7 +182,7 @@ __device__ __forceinline__ void signal_boundary(unsigned* bsig, int64_t nb, int 
 // GPU scope (cumulative over the acquired stores) and adds nb.  A named barrier in the store warps'
 // release path cost 3-6 % at N = 1..3 even when not taken, so the signal lives here, and only in the
 // BSIG = true kernel instances (multi-rank stages; the code alone cost ~2 % in the single-rank ones).
-// Call with the loader's tile counter j BEFORE its wait for slot reuse (that wait acquires tile j - S).
+// Call right after the loader's slot-reuse wait for tile j, which acquired the release of tile j - S.
 __device__ __forceinline__ void loader_signal_after_wait(unsigned* bsig, int64_t nb, int64_t j, int S) {
   if (bsig && j - S == nb - 1) {
     __threadfence();
@@ -212,15 +196,6 @@ __device__ __forceinline__ void loader_signal_tail(uint64_t* bar_empty, unsigned
     __threadfence();
     atomicAdd(bsig, unsigned(nb));
   }
-}
-__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
-__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-// no "memory" clobber: consecutive polls may be in flight together (ordering comes from the
-// acquire fence that follows them)
-__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
-  return v;
 }
 __device__ __forceinline__ bool mbar_test(uint64_t* b, unsigned parity) {
   unsigned ok;

@@ -228,3 +228,18 @@ def test_kernel_variant_auto_resolution():
         s = Solver(3, precision=8, device=-1, variant=v)
         assert s.kernel_variant() == v
         s.close()
+
+
+def test_launches_per_step_single_and_partitioned():
+    # one stage kernel per LSERK stage; with partition faces also one pack kernel per stage (the
+    # boundary-first single-launch stage: no interior/boundary split launches)
+    VX, E = di.kuhn_box(3)
+    s = Solver(3, device=-1)
+    s.mesh_upload(VX, E)
+    assert s.launches_per_step() == 5
+    s.close()
+    for r in range(2):
+        s = Solver(3, device=-1, rank=r, nranks=2)
+        s.mesh_upload(VX, E)
+        assert s.launches_per_step() == 10
+        s.close()
