@@ -45,10 +45,12 @@ def executed_flops(m):
             + g("sm__sass_thread_inst_executed_op_fadd_pred_on.sum") + g("sm__sass_thread_inst_executed_op_fmul_pred_on.sum")
             + 4 * g("sm__sass_thread_inst_executed_op_ffma2_pred_on.sum") + 2 * g("sm__sass_thread_inst_executed_op_fadd2_pred_on.sum")
             + 2 * g("sm__sass_thread_inst_executed_op_fmul2_pred_on.sum"))
-    # DMMA.8x8x4 warp instruction = 256 FMA; legacy HMMA m16n8k8 tf32 = 1024 FMA; tcgen05: ops counter (FMA)
+    # DMMA.8x8x4 warp instruction = 256 FMA; legacy HMMA m16n8k8 tf32 = 1024 FMA; the tcgen05 ops-path
+    # counter counts flops (checked: at N = 8 it gives 3.27 x F(N) K, the 3xTF32 multiplicity times the
+    # NP16 / Np and K-chunk padding, 3 x 176/165 x 688/675)
     tensor = (2 * 256 * g("sm__inst_executed_pipe_tensor_subpipe_dmma.sum")
               + 2 * 1024 * g("sm__inst_executed_pipe_tensor_subpipe_hmma.sum")
-              + 2 * g("sm__ops_path_tensor_op_utchmma_src_tf32_dst_fp32.sum"))
+              + g("sm__ops_path_tensor_op_utchmma_src_tf32_dst_fp32.sum"))
     return simt, tensor
 
 
@@ -97,7 +99,7 @@ def main():
         rows.append(row)
     out = os.path.join(ROOT, "profiles", f"{tag}_c4_sweep.json")
     with open(out, "w") as fh:
-        json.dump({"mesh": "C4: Kuhn n=56, K=1053696 (HBM-resident)", "source": "tools/gpu_r2_evidence.sh",
+        json.dump({"mesh": "C4: Kuhn n=56, K=1053696 (HBM-resident)", "source": "tools/gpu_r2_final.sh (tools/gpu_r2_evidence.sh layout)",
                    "rows": rows}, fh, indent=1)
     print("| prec | N | kernel | ms/step | G DOF/s | bound | frac | DRAM % peak | DRAM/alg (st 1-4) | DRAM/alg (st 0) "
           "| tensor % | FP64 % | FMA % | exec/model flops |")
