@@ -624,3 +624,55 @@ def test_nan_poisoned_padding(N, prec, variant):
         assert bad_dofs == 0, (name, bad_dofs)
         assert pad_not_nan == 0, (name, pad_not_nan)
     s.close()
+
+
+@pytest.mark.parametrize("prec,variant", [(8, 3), (4, 4), (4, 6)], ids=["f64-ws", "f32-tc", "f32-ffma"])
+def test_rcb_loopback_p8_bitwise(prec, variant):
+    # 8 partitions by recursive coordinate bisection (several peers per rank, ghost faces on every
+    # side) through the boundary-first single-launch stages: bitwise equal to one solver (R15)
+    from paper_1211_0582_b200.dg import DG_PARTITION_RCB
+    N = 3
+    VX, E = mesh(6, 51, 52, 53)
+    K = E.shape[0]
+    U0 = di.random_fields(K, N, seed=12)
+    dt = di.dt_rule(VX, E, N)
+    ref = Solver(N, precision=prec, variant=variant)
+    ref.mesh_upload(VX, E)
+    ref.fields_upload(U0)
+    ref.lserk_step(dt, 2)
+    Uref = ref.fields_download()
+    ref.close()
+    solvers, ids = [], []
+    for r in range(8):
+        sv = Solver(N, precision=prec, variant=variant, rank=r, nranks=8, partition=DG_PARTITION_RCB)
+        sv.mesh_upload(VX, E)
+        ids.append(sv.local_elements())
+        sv.fields_upload(U0[:, ids[-1]])
+        solvers.append(sv)
+    assert sorted(np.concatenate(ids).tolist()) == list(range(K))
+    group_lserk_step(solvers, dt, 2)
+    U = np.empty_like(U0)
+    for sv, ix in zip(solvers, ids):
+        U[:, ix] = sv.fields_download()
+        sv.close()
+    assert np.array_equal(U, Uref)
+
+
+@pytest.mark.parametrize("prec,variant", [(4, 4), (8, 3)], ids=["f32-tc", "f64-ws"])
+def test_acoustics_alpha0_tensor_kernels(prec, variant):
+    # central acoustic flux (alpha = 0) through the tensor-core kernels: RHS vs the oracle, and the
+    # discrete acoustic energy conserved over 20 steps to the time-integration error
+    N = 4
+    VX, E = mesh(3, 61, 62, 63)
+    st = setup("m3b", VX, E, N)
+    U0 = di.random_fields(st.K, N, seed=13, nfields=4)
+    s = Solver(N, precision=prec, alpha=0.0, system=DG_SYSTEM_ACOUSTICS, variant=variant)
+    s.mesh_upload(VX, E)
+    s.fields_upload(U0)
+    assert relerr(s.rhs(), oac.rhs(st, U0, alpha=0.0)) < TOL_RHS[prec]
+    dt = di.dt_rule(VX, E, N)
+    s.lserk_step(dt, 20)
+    U = s.fields_download()
+    s.close()
+    e0 = oac.energy(st, U0)
+    assert abs(oac.energy(st, U) - e0) / e0 < (1e-5 if prec == 8 else 1e-4)
