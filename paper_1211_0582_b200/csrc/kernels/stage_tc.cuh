@@ -337,6 +337,10 @@ __global__ void __launch_bounds__(TcCfg<N, SYS>::NT, 1)
       mbar_init(acc_empty + a, 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if constexpr (C::OP_RES) {  // resident operators (N <= 5): fetched while the previous stage drains
+      mbar_arrive_tx(b_full, unsigned(C::OPS_FLOATS * 4));
+      bulk_g2s(sB, ops, unsigned(C::OPS_FLOATS * 4), b_full);
+    }
   }
   if (warp == C::W_MMA) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -446,11 +450,8 @@ __global__ void __launch_bounds__(TcCfg<N, SYS>::NT, 1)
     if (lane == 0) {
       // ===== loader: one thread drives both copy streams with non-blocking barrier tests =====
       // stream 1: per tile, geometry + connectivity (meta ring), then its node-octet slabs;
-      // stream 2: the operator chunks in MMA order (streamed orders; resident: one copy).
-      if constexpr (C::OP_RES) {
-        mbar_arrive_tx(b_full, unsigned(C::OPS_FLOATS * 4));
-        bulk_g2s(sB, ops, unsigned(C::OPS_FLOATS * 4), b_full);
-      }
+      // stream 2: the operator chunks in MMA order (streamed orders; resident: one copy, issued in the
+      // prologue before the programmatic-dependency wait: the operators do not depend on the previous stage)
       const int T2 = C::OP_RES ? 0 : J * NQ;
       int j1 = 0, o1 = -1, g1 = 0, g2 = 0;
       while (j1 < J || g2 < T2) {
