@@ -103,7 +103,7 @@ struct FfCfg {
   // 20 250 / (E x 148) tiles per CTA sets the tail imbalance and the ring depth
   static constexpr int E = (TUNED && DG_FF_E) ? DG_FF_E
                            : F64 ? (N <= 3 ? 16 : N <= 6 ? 8 : 4)
-                                 : (N == 1 || N == 3) ? 32 : (N == 2 || N == 4 || N == 6) ? 16 : 8;
+                                 : N <= 3 ? 32 : (N == 4 || N == 6) ? 16 : 8;
   static_assert(E == 4 || E == 8 || E == 16 || E == 32, "tile = 4, 8, 16 or 32 elements");
 #ifndef DG_FF_EPL
 #define DG_FF_EPL 0
@@ -144,9 +144,14 @@ struct FfCfg {
   // profiles/r1_ffma_tune.jsonl)
   // FP64 N = 1: 16-element tiles in an 8-slot ring with a 4-tile trace look-ahead beat 32 / 6 / 2
   // (C4 1.525 vs 1.590 ms, C2 0.0514 vs 0.0556 ms per step; profiles/r2_ffma_lown.jsonl)
-  static constexpr int S = (TUNED && DG_FF_S) ? DG_FF_S : (!F64 && N == 4) ? 3 : (F64 && N == 1) ? 8 : S_DEF;
+  // FP32 N = 1: 8 slots / look-ahead 4 (C4 0.952 vs 1.002 ms, C2 -4 %); FP32 N = 2: 32-element tiles in a 4-slot
+  // ring (C4 2.47 vs 3.27 ms, C2 0.078 vs 0.086 ms; profiles/r2_ffma_lown2.txt)
+  static constexpr int S = (TUNED && DG_FF_S) ? DG_FF_S
+                           : (!F64 && N == 4) ? 3
+                           : (N == 1) ? 8
+                           : (!F64 && N == 2) ? 4 : S_DEF;
   static_assert(S >= 2, "two ring slots at least");
-  static constexpr int LA = (TUNED && DG_FF_LA >= 0) ? DG_FF_LA : (F64 && N == 1) ? 4 : S - 2 < 2 ? S - 2 : 2;
+  static constexpr int LA = (TUNED && DG_FF_LA >= 0) ? DG_FF_LA : (N == 1) ? 4 : S - 2 < 2 ? S - 2 : 2;
   static_assert(LA <= S - 2 || (S == 2 && LA == 0), "look-ahead beyond the ring");
 #ifndef DG_FF_SPLIT
 #define DG_FF_SPLIT -1
