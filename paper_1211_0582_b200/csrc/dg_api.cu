@@ -218,10 +218,11 @@ void release_device(dg_solver* s) {
 // DG_VARIANT_AUTO: the measured-best kernel per (precision, order) on the bench
 // config (NEXT-4 sweep, tools/variant_sweep.py, profiles/r2_final/variant_sweep.jsonl): FP64 ->
 // FFMA (register-tiled DFMA) at N = 1, MMA_WS (DMMA) otherwise; FP32 -> FFMA (register-tiled
-// SIMT) at N = 1, 2, TC (tcgen05 kind::tf32 3xTF32, TMEM operands) at N >= 3.
+// SIMT) at N = 1, 2, 3, TC (tcgen05 kind::tf32 3xTF32, TMEM operands) at N >= 4.  N = 3 is a tie on
+// C2 (TC 0.137-0.142 / FFMA 0.138 ms) and FFMA on the HBM-resident C4 mesh (4.96 vs 5.61 ms).
 int auto_variant(bool fp64, int N) {
   if (fp64) return N == 1 ? DG_VARIANT_FFMA : DG_VARIANT_MMA_WS;
-  return N <= 2 ? DG_VARIANT_FFMA : DG_VARIANT_TC;
+  return N <= 3 ? DG_VARIANT_FFMA : DG_VARIANT_TC;
 }
 
 // acoustics (measured on C2, profiles/r2_acoustics_sweep.jsonl): FP64 -> DFMA (FFMA kernel) at N = 1,

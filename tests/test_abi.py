@@ -207,12 +207,12 @@ def test_morton_reorder_is_local_permutation():
 
 def test_kernel_variant_auto_resolution():
     # DG_VARIANT_AUTO resolves at dg_create to the measured-best kernel (DESIGN.md §8 NEXT-4 table):
-    # FP64 -> FFMA (DFMA) at N=1, MMA_WS (DMMA) otherwise; FP32 -> FFMA at N=1,2, TC (tcgen05 3xTF32)
-    # at N=3..9; acoustics -> FFMA (FP64 N = 1; FP32 N <= 3), MMA_WS (FP64 N >= 2), TC (FP32 N >= 4).
+    # FP64 -> FFMA (DFMA) at N=1, MMA_WS (DMMA) otherwise; FP32 -> FFMA at N=1,2,3, TC (tcgen05 3xTF32)
+    # at N=4..9; acoustics -> FFMA (FP64 N = 1; FP32 N <= 3), MMA_WS (FP64 N >= 2), TC (FP32 N >= 4).
     # Explicit variants are reported
     # as requested.
     want = {8: {1: 6, **{n: 3 for n in range(2, 10)}},
-            4: {**{n: 6 for n in (1, 2)}, **{n: 4 for n in range(3, 10)}}}
+            4: {**{n: 6 for n in (1, 2, 3)}, **{n: 4 for n in range(4, 10)}}}
     for prec, table in want.items():
         for N, v in table.items():
             s = Solver(N, precision=prec, device=-1)
