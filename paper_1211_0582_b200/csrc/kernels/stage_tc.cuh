@@ -52,16 +52,16 @@
 #define DG_TC_RB 12
 #endif
 #ifndef DG_TC_LF
-#define DG_TC_LF 6
+#define DG_TC_LF 0
 #endif
 #ifndef DG_TC_RS
-#define DG_TC_RS 4
+#define DG_TC_RS 0
 #endif
 #ifndef DG_TC_LT
-#define DG_TC_LT 4
+#define DG_TC_LT 0
 #endif
 #ifndef DG_TC_RM
-#define DG_TC_RM 4
+#define DG_TC_RM 0
 #endif
 // Diagnostic knock-outs (timing experiments only; results are wrong when set, never in libdg.so):
 // DG_TC_X = bit mask: 1 flux warps skip the trace gathers and the flux arithmetic (zeros),
@@ -104,11 +104,14 @@ struct TcCfg {
   static constexpr int ITEMS = 8 * E;               // flux items (element, face-node slot) per chunk
   static constexpr int PW = 6;                      // flux warps: one item per thread and chunk
   static constexpr int FTH = 32 * PW;
-  static constexpr int LT = DG_TC_LT;               // per-thread cp.async trace pipeline depth (chunks)
+  // ring depths (0 = per-order default; measured, profiles/r2_tc_tune.jsonl): shallower flux staging and trace
+  // pipelines (LF 4, LT 3) at N = 4, 5, 6, 9 and shallower slab/meta rings at N = 5 (-1..4 %), round-2 defaults otherwise
+  static constexpr bool SHALLOW = N == 4 || N == 5 || N == 6 || N == 9;
+  static constexpr int LT = DG_TC_LT ? DG_TC_LT : SHALLOW ? 3 : 4;  // per-thread cp.async trace pipeline depth (chunks)
   static constexpr int TRC = FTH * 2 * NC;          // floats per trace-staging chunk: [NC pairs][FTH][2] (u-, u+)
-  static constexpr int LF = DG_TC_LF;               // flux staging ring (chunks) [128 rows][8]
+  static constexpr int LF = DG_TC_LF ? DG_TC_LF : SHALLOW ? 4 : 6;  // flux staging ring (chunks) [128 rows][8]
   static constexpr int FSC = 128 * 8;
-  static constexpr int RS = DG_TC_RS, RM = DG_TC_RM;
+  static constexpr int RS = DG_TC_RS ? DG_TC_RS : N == 5 ? 3 : 4, RM = DG_TC_RM ? DG_TC_RM : N == 5 ? 3 : 4;
   // operand chunks per writer batch (one tcgen05.wait::st): 3, or 4 at N = 6, 9 (measured on C2,
   // tools/gpu_tc_tune.sh: N = 6 -3.5 %, N = 9 -2 %; N = 3, 4 +1.5 % with 4)
   static constexpr int WB = DG_TC_WB ? DG_TC_WB : (N == 6 || N == 9) ? 4 : 3;
