@@ -112,9 +112,9 @@ struct TcCfg {
   static constexpr int LF = DG_TC_LF ? DG_TC_LF : SHALLOW ? 4 : 6;  // flux staging ring (chunks) [128 rows][8]
   static constexpr int FSC = 128 * 8;
   static constexpr int RS = DG_TC_RS ? DG_TC_RS : N == 5 ? 3 : 4, RM = DG_TC_RM ? DG_TC_RM : N == 5 ? 3 : 4;
-  // operand chunks per writer batch (one tcgen05.wait::st): 3, or 4 at N = 6, 9 (measured on C2,
-  // tools/gpu_tc_tune.sh: N = 6 -3.5 %, N = 9 -2 %; N = 3, 4 +1.5 % with 4)
-  static constexpr int WB = DG_TC_WB ? DG_TC_WB : (N == 6 || N == 9) ? 4 : 3;
+  // operand chunks per writer batch (one tcgen05.wait::st): 3, or 4 at N = 6, 8, 9 (measured on C2,
+  // tools/gpu_tc_tune.sh: N = 6 -3.5 %, N = 8 -3.5 %, N = 9 -2 %; N = 3, 4 +1.5 % with 4, N = 7 +0.4 %)
+  static constexpr int WB = DG_TC_WB ? DG_TC_WB : (N == 6 || N == 8 || N == 9) ? 4 : 3;
   static constexpr int WUNR = NQ <= 36 ? (NQ + WB - 1) / WB : 1;
   // generated operand G in TENSOR memory (kind::tf32 A operand: lane = row, one column per k):
   // ring slots of 16 columns (8 G | 8 G_lo) after the two accumulators
